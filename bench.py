@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the row-split fp32-accurate GEMM (GigaAPI, arXiv 2504.01266) on B200.
+
+    python bench.py --gpus N --steps K --warmup W            (N > 1: under torchrun)
+    python bench.py --impl reference ...                      (the CPU fp64 oracle arm)
+
+One step = the whole hot path over one synthetic problem: broadcast B from
+rank 0 (N > 1), split A and B into TF32 hi/lo, the 3xTF32 tcgen05 shard GEMM, gather the C
+row blocks on every rank. Default workload: BASELINE.json configs[2], M = N = K = 16384,
+strong scaling (the same problem split over N GPUs). Inputs are seeded synthetic fp32
+(synth "d2", U[-1,1)), resident in HBM before the timed region; A, B, C are each 1 GiB,
+larger than the 126 MB L2, so no flush is needed between steps.
+
+Prints ONE JSON line (rank 0). Metric: logical TFLOP/s = 2 M N K / t (whole job).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (M, N, K)  -- BASELINE.json configs
+    "c1_512": (512, 512, 512),
+    "c2_4096": (4096, 4096, 4096),
+    "c3_16384": (16384, 16384, 16384),
+    "c4_tall": (262144, 1024, 1024),
+    "c5_32768": (32768, 32768, 32768),
+}
+DEFAULT_CONFIG = "c3_16384"
+METRIC = "GEMM TFLOP/s (fp32-accurate) at 1/2/4/8 B200 and % of TF32 tensor roofline"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """NVML clock / throttle-reason sampler running during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period: float = 0.1):
+        self.index, self.period = index, period
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self._err = str(e)
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for b, name in self.REASONS.items():
+                    if bits & b and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(self.period)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+def oracle_sample(M, N, K, dist, budget_s, threads):
+    """Time the oracle, as it stands, on the first R rows of the workload (~budget_s)."""
+    import numpy as np
+    import torch
+    import oracle
+    import synth
+
+    torch.set_num_threads(threads)
+    B = synth.gen_rows_torch(0, K, N, synth.MATRIX_B, dist, device="cpu").numpy()
+    probe = max(1, threads)
+    A = synth.gen_rows(0, probe, K, synth.MATRIX_A, dist)
+    t0 = time.perf_counter()
+    oracle.gemm(A, B, nthreads=threads, want_s=False)
+    t_probe = time.perf_counter() - t0
+    rows = int(max(probe, min(M, probe * max(1.0, budget_s / max(t_probe, 1e-6)))))
+    rows = max(probe, rows // probe * probe)
+    A = synth.gen_rows(0, rows, K, synth.MATRIX_A, dist)
+    t0 = time.perf_counter()
+    oracle.gemm(A, B, nthreads=threads, want_s=False)
+    t = time.perf_counter() - t0
+    return {"rows": rows, "seconds": t, "tflops": 2.0 * rows * N * K / t / 1e12}
+
+
+def run_reference(args):
+    """--impl reference: the CPU fp64 oracle on the host cores, same config and metric."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    M, N, K = CONFIGS[args.config]
+    threads = len(os.sched_getaffinity(0))
+    per_step = max(1.0, args.ref_budget / max(1, args.steps + args.warmup))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = oracle_sample(M, N, K, args.dist, per_step, threads)
+        if i >= args.warmup:
+            vals.append(r)
+    tflops = statistics.median(v["tflops"] for v in vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(tflops, 6), "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * statistics.median(v["seconds"] for v in vals), 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"{args.config} M={M} N={N} K={K}",
+                                        "dist": args.dist},
+        "cpu_baseline": {"value": round(tflops, 6), "unit": "TFLOP/s", "cores": threads,
+                         "kind": "oracle",
+                         "sample": f"first {vals[0]['rows']} rows of C per step "
+                                   f"(of {M}), full N and K; fp64 i-k-j C triple loop"},
+        "e2e": {"value": round(tflops, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="giga", choices=["giga", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--dist", default="d2", choices=["d1", "d2", "d3"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=60.0,
+                    help="total seconds of oracle work for --impl reference")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import synth
+    from paper_2504_01266_b200 import giga
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            print(f"--gpus {args.gpus} needs torchrun with {args.gpus} processes", file=sys.stderr)
+            return 2
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+        obj = [giga.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        giga.rank_init(rank, world, local, obj[0])
+    else:
+        giga.rank_init(0, 1, local, None)
+
+    M, N, K = CONFIGS[args.config]
+    r0, rows = giga.partition(M, world, rank)
+    A = synth.gen_rows_torch(r0, rows, K, synth.MATRIX_A, args.dist, device=dev)
+    if rank == 0:
+        B = synth.gen_rows_torch(0, K, N, synth.MATRIX_B, args.dist, device=dev)
+    else:
+        B = torch.empty((K, N), dtype=torch.float32, device=dev)
+    C = torch.empty((M, N), dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        giga.matmul_rank(A, B, C, M, N, K, stream=stream)
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device events on the launching stream ----
+    giga.timing_enable(True)
+    giga.timing_reset()
+    clocks = ClockSampler(local).start()
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    kt = giga.timing_read()
+    giga.timing_enable(False)
+    if pg is not None:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    flops = 2.0 * M * N * K
+    tflops = flops / (ms_step * 1e-3) / 1e12
+
+    # ---- roofline of the dominant kernel (the shard GEMM) ----
+    peaks, peak_src = load_peaks()
+    # TF32 dense peak = measured bf16 x (nominal tf32 / bf16 = 1.1 / 2.25 ~ 0.5)
+    tf32_sustained = 0.5 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    tf32_burst = 0.5 * peaks["bf16_tflops"]
+    gemm_ms = kt["gemm_ms"] / max(1, kt["gemm_launches"])
+    # algorithmic tensor flops per launch: 3 TF32 MMAs per logical product (3xTF32)
+    tensor_flops = 3 * 2.0 * rows * N * K
+    achieved = tensor_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tr = json.load(f).get(args.config)
+            traffic = tr
+        except Exception:  # noqa: BLE001
+            traffic = None
+    roof = {"bound": "tensor", "achieved": round(achieved, 2) if achieved else None,
+            "peak": round(tf32_sustained, 1), "unit": "TFLOP/s",
+            "frac": round(achieved / tf32_sustained, 4) if achieved else None,
+            "traffic": traffic,
+            "kernel": "gemm_3xtf32_kernel", "kernel_ms": round(gemm_ms, 4),
+            "kernel_share_of_step": round(gemm_ms / ms_step, 4) if ms_step else None,
+            "peak_note": f"TF32 dense = 0.5 x {peak_src} bf16 sustained "
+                         f"({peaks.get('bf16_tflops_sustained')}); burst-based frac "
+                         f"{round(achieved / tf32_burst, 4) if achieved else None}",
+            "split_ms_per_step": round(kt["split_ms"] / args.steps, 4)}
+
+    # ---- end to end: host buffers through the C ABI ----
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e = measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev, pg)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        r = oracle_sample(M, N, K, args.dist, args.cpu_budget, threads)
+        cpu = {"value": round(r["tflops"], 6), "unit": "TFLOP/s", "cores": threads,
+               "kind": "oracle",
+               "sample": f"first {r['rows']} rows of C (of {M}), full N={N}, K={K}: "
+                         f"{r['seconds']:.1f} s fp64 i-k-j C triple loop"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(tflops, 3), "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (3xTF32 tensor, fp32-accurate)", "data": "synthetic",
+            "config": {"workload": f"{args.config} M={M} N={N} K={K}", "dist": args.dist,
+                       "parallelism": f"row-split x{world}",
+                       "l2": "inputs larger than L2 (A, B, C 1 GiB each at c3)"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(kt["gemm_launches"] + kt["split_launches"]),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    giga.finalize()
+    if pg is not None:
+        pg.destroy_process_group()
+    return 0
+
+
+def measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev, pg):
+    """Same metric with the inputs in pinned HOST memory: every step copies this rank's A
+    rows (and B on rank 0) host->device, runs the hot path and copies this rank's C rows
+    back (N = 1: the single giga_matmul host-pointer call of the C ABI)."""
+    r0, rows = giga.partition(M, world, rank)
+    if world == 1:
+        giga.finalize()
+        giga.init(1)
+        Ah = synth.gen_rows_torch(0, M, K, synth.MATRIX_A, args.dist, device=dev).cpu().pin_memory()
+        Bh = synth.gen_rows_torch(0, K, N, synth.MATRIX_B, args.dist, device=dev).cpu().pin_memory()
+        Ch = torch.empty((M, N), dtype=torch.float32).pin_memory()
+        giga.matmul(Ah, Bh, Ch, M, N, K, 1)  # warm (workspace)
+        ts = []
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            giga.matmul(Ah, Bh, Ch, M, N, K, 1)
+            ts.append(time.perf_counter() - t0)
+        t = statistics.median(ts)
+        h2d = 4 * (M * K + K * N)
+        d2h = 4 * M * N
+        return {"value": round(2.0 * M * N * K / t / 1e12, 3), "unit": "TFLOP/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": round(t * 1e3, 3),
+                "api": "giga_matmul(host pinned A, B, C) blocking, wall clock"}
+    # N > 1: each rank stages its own rows; rank 0 stages B
+    Ah = torch.empty((rows, K), dtype=torch.float32).pin_memory()
+    Ah.copy_(synth.gen_rows_torch(r0, rows, K, synth.MATRIX_A, args.dist, device=dev).cpu())
+    Bh = None
+    if rank == 0:
+        Bh = synth.gen_rows_torch(0, K, N, synth.MATRIX_B, args.dist, device=dev).cpu().pin_memory()
+    Ch = torch.empty((rows, N), dtype=torch.float32).pin_memory()
+    A = torch.empty((rows, K), dtype=torch.float32, device=dev)
+    B = torch.empty((K, N), dtype=torch.float32, device=dev)
+    C = torch.empty((M, N), dtype=torch.float32, device=dev)
+    s = torch.cuda.Stream(device=dev)
+
+    def one():
+        with torch.cuda.stream(s):
+            A.copy_(Ah, non_blocking=True)
+            if Bh is not None:
+                B.copy_(Bh, non_blocking=True)
+            giga.matmul_rank(A, B, C, M, N, K, stream=s)
+            Ch.copy_(C[r0:r0 + rows], non_blocking=True)
+        s.synchronize()
+
+    one()
+    ts = []
+    for _ in range(args.e2e_steps):
+        pg.barrier()
+        t0 = time.perf_counter()
+        one()
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ts.append(float(t.item()))
+    t = statistics.median(ts)
+    return {"value": round(2.0 * M * N * K / t / 1e12, 3), "unit": "TFLOP/s",
+            "h2d_bytes_per_step": 4 * (M * K + K * N), "d2h_bytes_per_step": 4 * M * N,
+            "ms_per_step": round(t * 1e3, 3),
+            "api": "pinned H2D + giga_matmul_rank + D2H per rank, wall clock max over ranks"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,166 @@
+/*
+ * giga.h -- C ABI of the B200-native GigaAPI matrix multiply (arXiv 2504.01266).
+ *
+ * The operation (S4.2.7 "Matrix Multiplication"):
+ *     C[i][j] = sum_k A[i][k] * B[k][j]
+ * "each element in C[i,j] is calculated by taking a dot product of the i-th row of the
+ *  matrix A and the j-th column of matrix B", the sum "reported and assigned at the end"
+ * (PAPER.md:291): C is fully OVERWRITTEN, its prior contents never matter (the paper's
+ * dirty-memory bug, cannot happen).
+ *
+ * Distribution ("we effectively half them ... half the multiplications are
+ * carried out on one GPU ... copy over half the matrices"; generalised to g GPUs per
+ * PAPER.md:311): the rows of A (and C) are split into contiguous blocks, one per GPU; every
+ * GPU receives a full copy of B; the C row blocks are gathered. giga_partition() states the
+ * split rule.
+ *
+ * Layout: every matrix is dense row-major fp32 (SPEC.md:234-236 MatrixF32); A is M x K
+ * (row stride K), B is K x N (row stride N), C is M x N (row stride N). No transposes, no
+ * alpha/beta.
+ *
+ * Precision: fp32 in, fp32 out, fp32-accurate: internally each product is formed as
+ * 3xTF32 (a_lo*b_hi + a_hi*b_lo + a_hi*b_hi on the tcgen05 tensor cores, partial sums
+ * promoted into fp32 registers) so that per element
+ *     |C - C_exact| <= 1e-5 * sum_k |A_ik| |B_kj|          (BASELINE.json north_star)
+ * and integer-valued inputs whose partial sums stay below 2^24 give bit-exact results.
+ * Non-finite inputs: NaN propagates; Inf may turn into NaN (Inf - Inf in the split).
+ *
+ * Errors: every function returns GIGA_OK (0) or a negative giga_status; the message of the
+ * last failure on the calling thread is in giga_last_error(). After a failed call the
+ * device memory in use equals its value before the call (no leaks; the workspace cache is
+ * only grown by successful calls and is released by giga_finalize).
+ *
+ * Ownership: the caller owns every pointer passed in; the library never keeps a caller
+ * pointer after returning. The library owns its streams, events, communicators and
+ * workspace (TF32 low-part buffers, padded copies), freed in giga_finalize().
+ *
+ * Threading: calls are serialised by an internal mutex (one call at a time per process).
+ */
+#ifndef GIGA_H_
+#define GIGA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum giga_status {
+  GIGA_OK = 0,
+  GIGA_ERR_INVALID_ARG = -1,         /* M, N or K < 1; ngpus out of range; NULL pointer;
+                                        C overlapping A or B; misaligned device pointer */
+  GIGA_ERR_NOT_INITIALIZED = -2,     /* call before giga_init / giga_rank_init */
+  GIGA_ERR_ALREADY_INITIALIZED = -3, /* init twice without giga_finalize */
+  GIGA_ERR_NO_DEVICE = -4,           /* no sm_100 GPU, or fewer than requested */
+  GIGA_ERR_OOM = -5,                 /* device (or pinned host) allocation failed */
+  GIGA_ERR_CUDA = -6,                /* any other CUDA runtime/driver failure */
+  GIGA_ERR_COMM = -7,                /* NCCL / peer-transport failure */
+  GIGA_ERR_UNSUPPORTED = -8          /* valid request this build cannot serve */
+};
+
+/* ------------------------------------------------------------------------------------ */
+/* Single-process API: one process drives g GPUs (the paper's GigaGPU object). */
+
+/* Initialise the library on GPUs 0..n-1, n = ngpus_max (ngpus_max <= 0: all visible GPUs).
+ * Creates per-GPU compute and copy streams, events, enables peer access between the GPUs
+ * and resolves the TMA descriptor encoder. Errors: ALREADY_INITIALIZED, NO_DEVICE
+ * (fewer than n sm_100 GPUs), CUDA. */
+int giga_init(int ngpus_max);
+
+/* Number of GPUs the library was initialised with (0 if not initialised). */
+int giga_num_devices(void);
+
+/* Release everything giga_init / giga_rank_init created (streams, events, communicators,
+ * workspace). Safe to call when not initialised (returns GIGA_OK). */
+int giga_finalize(void);
+
+/* The row-block rule (PAPER.md:287 halving generalised; "last device takes
+ * remainder"): rows_g = floor(M / ngpus) for g < ngpus-1, the last GPU takes
+ * M - (ngpus-1)*floor(M/ngpus); row0_g = g*floor(M/ngpus). Shards may be empty when
+ * M < ngpus. Pure host arithmetic; needs no initialisation. Errors: INVALID_ARG. */
+int giga_partition(int64_t M, int ngpus, int g, int64_t *row0, int64_t *rows);
+
+/* C = A * B on GPUs 0..ngpus-1.
+ * A, B, C: either all HOST pointers (pageable or pinned) -- the paper's semantics: the
+ * library copies each A row block and B to the GPUs, computes, and copies each GPU's C row
+ * block straight back into C -- or all DEVICE pointers on GPU 0 (A, B, C as M x K, K x N,
+ * M x N buffers); the result then lands in C on GPU 0. Blocking: returns after C holds the
+ * result. Errors: NOT_INITIALIZED, INVALID_ARG (M,N,K < 1; ngpus not in
+ * [1, giga_num_devices()]; NULL; C overlapping A or B; mixed host/device pointers),
+ * OOM, CUDA, COMM. */
+int giga_matmul(const float *A, const float *B, float *C, int64_t M, int64_t N, int64_t K,
+                int ngpus);
+
+/* Device-resident, pre-sharded hot path (what bench.py times).
+ * A_shard[g]: device pointer on GPU g to the rows_g x K block of A (giga_partition rule).
+ * B_buf[0]:   device pointer on GPU 0 holding B (K x N). B_buf[g>0]: K x N receive buffers
+ *             on GPU g, overwritten with B.
+ * C_full[g]:  device pointer on GPU g to an M x N buffer; on return EVERY GPU holds the full
+ *             C (the row blocks are gathered).
+ * Errors: as giga_matmul. */
+int giga_matmul_sharded(const float *const *A_shard, float *const *B_buf,
+                        float *const *C_full, int64_t M, int64_t N, int64_t K, int ngpus);
+
+/* Message describing the last failure on this thread ("" if none). */
+const char *giga_last_error(void);
+
+/* ------------------------------------------------------------------------------------ */
+/* Multi-process API: one process per GPU (torchrun), a communicator across the processes.
+ * Rank 0 calls giga_comm_unique_id and ships the 128 bytes to the others (any channel,
+ * e.g. torch.distributed); then every rank calls giga_rank_init. */
+
+int giga_comm_unique_id(uint8_t id[128]);
+
+/* rank in [0, world), device = the CUDA ordinal this process drives. Errors:
+ * ALREADY_INITIALIZED, INVALID_ARG, NO_DEVICE, COMM. */
+int giga_rank_init(int rank, int world, int device, const uint8_t id[128]);
+
+/* This rank's share of C = A * B, device pointers on this rank's GPU:
+ * A_shard: rows_r x K block (giga_partition(M, world, rank)); B: K x N (source on rank 0,
+ * receive buffer elsewhere); C_full: M x N, holds the full C on return on every rank.
+ * Work is enqueued on `stream` (a cudaStream_t, NULL = the library's stream) and the call
+ * returns without synchronising the host (stream-ordered). Errors: NOT_INITIALIZED,
+ * INVALID_ARG, CUDA, COMM. */
+int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, int64_t N,
+                     int64_t K, void *stream);
+
+/* ------------------------------------------------------------------------------------ */
+/* Single-device building blocks (device pointers on the current CUDA device; work is
+ * enqueued on `stream`, a cudaStream_t, 0 = legacy default stream; no host sync). They do
+ * not need giga_init. */
+
+/* lo[i] = x[i] - tf32(x[i]) for i < n, where tf32() is the operand conversion the
+ * tcgen05 kind::tf32 tensor core applies to raw fp32 bits (truncation of the low 13
+ * mantissa bits; measured). The difference is exact in fp32. x and lo
+ * 16-byte aligned. Errors: INVALID_ARG, CUDA. */
+int giga_split_lo(const float *x, float *lo, int64_t n, void *stream);
+
+/* C[i*ldc + j] = sum_k A[i*K+k] B[k*N+j] for i < M, j < N, with A_lo / B_lo the low parts
+ * produced by giga_split_lo. Requirements: K % 4 == 0, N % 4 == 0, ldc % 4 == 0, ldc >= N,
+ * all pointers 16-byte aligned (TMA). Errors: INVALID_ARG, CUDA. */
+int giga_gemm_3xtf32(const float *A, const float *A_lo, const float *B, const float *B_lo,
+                     float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, void *stream);
+
+/* As giga_gemm_3xtf32 with the numerics knobs exposed (tests and probes):
+ * terms = 3 (3xTF32) or 1 (plain TF32: a_hi*b_hi only; A_lo/B_lo may be NULL);
+ * promote_kblocks = number of 16-wide k-blocks accumulated in TMEM before the partial sum
+ * is added into the fp32 register sum; 0 = never promote (one TMEM accumulation over K);
+ * -1 = the library default. */
+int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const float *B_lo,
+                        float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, int terms,
+                        int promote_kblocks, void *stream);
+
+/* ------------------------------------------------------------------------------------ */
+/* Kernel timing (bench.py's roofline): when enabled, CUDA events bracket every GEMM and
+ * split launch on the stream it is launched on; giga_timing_read synchronises on the
+ * recorded events and returns the summed device milliseconds and launch counts since the
+ * last reset. */
+int giga_timing_enable(int on);
+int giga_timing_reset(void);
+int giga_timing_read(double *gemm_ms, int64_t *gemm_launches, double *split_ms,
+                     int64_t *split_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GIGA_H_ */

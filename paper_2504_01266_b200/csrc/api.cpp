@@ -1,0 +1,803 @@
+// api.cpp -- the C ABI declared in include/giga.h: library state, the row-block partitioner,
+// the per-GPU workspace cache, and the orchestration of one row-split matrix multiply
+// (PAPER.md:285-291): place A row blocks, distribute B (NCCL broadcast), split to TF32
+// hi/lo, shard GEMM, gather the C row blocks (NCCL all-gather / per-owner broadcast).
+#include "giga.h"
+
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "nccl_loader.h"
+
+namespace giga {
+namespace {
+
+// ---------------------------------------------------------------------------------------
+// errors
+thread_local std::string t_err;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return code;
+}
+
+int fail_cuda(cudaError_t e, const char *what, int line) {
+  cudaGetLastError();  // clear a non-sticky error so the next call starts clean
+  const int code = (e == cudaErrorMemoryAllocation) ? GIGA_ERR_OOM : GIGA_ERR_CUDA;
+  return fail(code, "%s failed at api.cpp:%d: %s (%s)", what, line, cudaGetErrorName(e),
+              cudaGetErrorString(e));
+}
+
+#define CK(x)                                                     \
+  do {                                                            \
+    cudaError_t e_ = (x);                                         \
+    if (e_ != cudaSuccess) return fail_cuda(e_, #x, __LINE__);    \
+  } while (0)
+
+#define TRY(x)                \
+  do {                        \
+    int r_ = (x);             \
+    if (r_ != GIGA_OK) return r_; \
+  } while (0)
+
+// ---------------------------------------------------------------------------------------
+// state
+
+struct Buf {
+  void *p = nullptr;
+  size_t bytes = 0;
+};
+
+struct DevCtx {
+  int dev = -1;
+  cudaStream_t compute = nullptr;  // splits + GEMM (+ H2D/D2H in host mode)
+  cudaStream_t comm = nullptr;     // broadcast of B, gather of C
+  cudaEvent_t ev_b = nullptr;      // B present on this GPU
+  cudaEvent_t ev_c = nullptr;      // this GPU's C rows computed
+  cudaEvent_t ev_start = nullptr;  // caller-stream entry (rank mode)
+  Buf A_lo, B_lo, A_pad, B_pad, C_pad, A_h, B_h, C_h;
+};
+
+struct State {
+  std::mutex mu;
+  int mode = 0;  // 0 none, 1 single-process, 2 rank
+  std::vector<DevCtx> devs;
+  std::map<int, std::vector<ncclComm_t>> comms;  // single-process: ngpus -> comms
+  ncclComm_t rank_comm = nullptr;
+  int rank = 0, world = 1;
+};
+State g;
+
+struct TimeRec {
+  int dev;
+  int kind;  // 0 gemm, 1 split
+  cudaEvent_t a, b;
+};
+std::mutex g_tmu;
+bool g_timing = false;
+std::vector<TimeRec> g_tpending;
+std::vector<std::pair<int, cudaEvent_t>> g_tpool;
+double g_tms[2] = {0, 0};
+int64_t g_tcount[2] = {0, 0};
+
+cudaEvent_t pool_event(int dev) {
+  for (size_t i = 0; i < g_tpool.size(); ++i)
+    if (g_tpool[i].first == dev) {
+      cudaEvent_t e = g_tpool[i].second;
+      g_tpool.erase(g_tpool.begin() + i);
+      return e;
+    }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return e;
+}
+
+// Launch `fn` on `st`, bracketed by timing events when timing is enabled.
+template <class F>
+cudaError_t timed(int kind, cudaStream_t st, F fn) {
+  bool on;
+  {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    on = g_timing;
+  }
+  if (!on) return fn();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaEvent_t a, b;
+  {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    a = pool_event(dev);
+    b = pool_event(dev);
+  }
+  if (a) cudaEventRecord(a, st);
+  cudaError_t e = fn();
+  if (b) cudaEventRecord(b, st);
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (a && b)
+    g_tpending.push_back({dev, kind, a, b});
+  else {
+    if (a) g_tpool.push_back({dev, a});
+    if (b) g_tpool.push_back({dev, b});
+  }
+  return e;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------------------------------
+// workspace: grow-only per-GPU buffers, reserved transactionally so a failed call leaves the
+// device memory footprint exactly as it found it.
+
+int ws_reserve(DevCtx &d, std::initializer_list<std::pair<Buf *, size_t>> req) {
+  std::vector<std::pair<Buf *, void *>> fresh;
+  for (auto &r : req) {
+    if (r.first->bytes >= r.second) continue;
+    bool dup = false;
+    for (auto &f : fresh) dup |= (f.first == r.first);
+    if (dup) continue;
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, r.second);
+    if (e != cudaSuccess) {
+      for (auto &f : fresh) cudaFree(f.second);
+      return fail_cuda(e, "cudaMalloc(workspace)", __LINE__);
+    }
+    fresh.push_back({r.first, p});
+  }
+  for (auto &f : fresh) {
+    size_t want = 0;
+    for (auto &r : req)
+      if (r.first == f.first) want = std::max(want, r.second);
+    if (f.first->p) cudaFree(f.first->p);
+    f.first->p = f.second;
+    f.first->bytes = want;
+  }
+  return GIGA_OK;
+}
+
+void ws_free(DevCtx &d) {
+  for (Buf *b : {&d.A_lo, &d.B_lo, &d.A_pad, &d.B_pad, &d.C_pad, &d.A_h, &d.B_h, &d.C_h}) {
+    if (b->p) cudaFree(b->p);
+    b->p = nullptr;
+    b->bytes = 0;
+  }
+}
+
+float *fptr(Buf &b) { return static_cast<float *>(b.p); }
+
+int ctx_create(DevCtx &d, int dev) {
+  d.dev = dev;
+  CK(cudaSetDevice(dev));
+  CK(cudaStreamCreateWithFlags(&d.compute, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&d.comm, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&d.ev_b, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&d.ev_c, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&d.ev_start, cudaEventDisableTiming));
+  return GIGA_OK;
+}
+
+void ctx_destroy(DevCtx &d) {
+  if (d.dev < 0) return;
+  cudaSetDevice(d.dev);
+  cudaDeviceSynchronize();
+  ws_free(d);
+  if (d.compute) cudaStreamDestroy(d.compute);
+  if (d.comm) cudaStreamDestroy(d.comm);
+  for (cudaEvent_t e : {d.ev_b, d.ev_c, d.ev_start})
+    if (e) cudaEventDestroy(e);
+  d = DevCtx{};
+}
+
+int check_sm100(int dev) {
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10)
+    return fail(GIGA_ERR_NO_DEVICE, "device %d is sm_%d%d, this build is sm_100a only", dev,
+                prop.major, prop.minor);
+  return GIGA_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// one shard on one GPU: split A and B into TF32 hi/lo and run the tensor-core GEMM into
+// C (rows x N, row stride ldc). If `wait_b` is given, B is only touched after it fires (the
+// A split overlaps the distribution of B).
+
+int split(const float *x, float *lo, int64_t n, cudaStream_t st) {
+  CK(timed(1, st, [&] { return launch_split_lo(x, lo, n, st); }));
+  return GIGA_OK;
+}
+
+int gemm(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
+         int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st) {
+  CK(timed(0, st, [&] {
+    return launch_gemm_3xtf32(A, Alo, B, Blo, C, M, N, K, ldc, 3, -1, st);
+  }));
+  return GIGA_OK;
+}
+
+int shard_compute(DevCtx &d, cudaStream_t st, const float *A, int64_t rows, const float *B,
+                  float *C, int64_t ldc, int64_t N, int64_t K, cudaEvent_t wait_b) {
+  if (rows <= 0) {
+    if (wait_b) CK(cudaStreamWaitEvent(st, wait_b, 0));
+    return GIGA_OK;
+  }
+  const bool direct = (K % 4 == 0) && (N % 4 == 0) && (ldc % 4 == 0) && aligned16(A) &&
+                      aligned16(B) && aligned16(C);
+  if (direct) {
+    TRY(ws_reserve(d, {{&d.A_lo, size_t(rows * K) * 4}, {&d.B_lo, size_t(K * N) * 4}}));
+    TRY(split(A, fptr(d.A_lo), rows * K, st));
+    if (wait_b) CK(cudaStreamWaitEvent(st, wait_b, 0));
+    TRY(split(B, fptr(d.B_lo), K * N, st));
+    return gemm(A, fptr(d.A_lo), B, fptr(d.B_lo), C, rows, N, K, ldc, st);
+  }
+  // Unaligned shapes (H6): zero-padded copies with K, N rounded up to multiples of 4. Zero
+  // columns of A / rows of B add nothing to any dot product.
+  const int64_t K4 = (K + 3) / 4 * 4, N4 = (N + 3) / 4 * 4;
+  TRY(ws_reserve(d, {{&d.A_pad, size_t(rows * K4) * 4},
+                     {&d.B_pad, size_t(K4 * N4) * 4},
+                     {&d.C_pad, size_t(rows * N4) * 4},
+                     {&d.A_lo, size_t(rows * K4) * 4},
+                     {&d.B_lo, size_t(K4 * N4) * 4}}));
+  CK(cudaMemsetAsync(d.A_pad.p, 0, size_t(rows * K4) * 4, st));
+  CK(cudaMemcpy2DAsync(d.A_pad.p, K4 * 4, A, K * 4, K * 4, rows, cudaMemcpyDeviceToDevice, st));
+  TRY(split(fptr(d.A_pad), fptr(d.A_lo), rows * K4, st));
+  if (wait_b) CK(cudaStreamWaitEvent(st, wait_b, 0));
+  CK(cudaMemsetAsync(d.B_pad.p, 0, size_t(K4 * N4) * 4, st));
+  CK(cudaMemcpy2DAsync(d.B_pad.p, N4 * 4, B, N * 4, N * 4, K, cudaMemcpyDeviceToDevice, st));
+  TRY(split(fptr(d.B_pad), fptr(d.B_lo), K4 * N4, st));
+  TRY(gemm(fptr(d.A_pad), fptr(d.A_lo), fptr(d.B_pad), fptr(d.B_lo), fptr(d.C_pad), rows, N4,
+           K4, N4, st));
+  CK(cudaMemcpy2DAsync(C, ldc * 4, d.C_pad.p, N4 * 4, N * 4, rows, cudaMemcpyDeviceToDevice,
+                       st));
+  return GIGA_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// NCCL
+
+int nccl_check(ncclResult_t r, const char *what) {
+  if (r == ncclSuccess) return GIGA_OK;
+  const NcclApi *api = nccl_api(nullptr);
+  return fail(GIGA_ERR_COMM, "%s failed: %s", what, api ? api->GetErrorString(r) : "?");
+}
+
+int get_comms(int ngpus, std::vector<ncclComm_t> **out) {
+  auto it = g.comms.find(ngpus);
+  if (it != g.comms.end()) {
+    *out = &it->second;
+    return GIGA_OK;
+  }
+  const char *why = nullptr;
+  const NcclApi *api = nccl_api(&why);
+  if (!api) return fail(GIGA_ERR_COMM, "NCCL unavailable: %s", why ? why : "?");
+  std::vector<int> devs(ngpus);
+  for (int i = 0; i < ngpus; ++i) devs[i] = g.devs[i].dev;
+  std::vector<ncclComm_t> comms(ngpus, nullptr);
+  TRY(nccl_check(api->CommInitAll(comms.data(), ngpus, devs.data()), "ncclCommInitAll"));
+  g.comms[ngpus] = comms;
+  *out = &g.comms[ngpus];
+  return GIGA_OK;
+}
+
+void partition_rows(int64_t M, int ngpus, int gi, int64_t *row0, int64_t *rows) {
+  const int64_t base = M / ngpus;
+  *row0 = int64_t(gi) * base;
+  *rows = (gi == ngpus - 1) ? M - int64_t(ngpus - 1) * base : base;
+}
+
+// Gather the C row blocks so that every rank's C_full holds all of C. Equal blocks: one
+// in-place all-gather; otherwise one broadcast per owner (NCCL all-gather needs equal counts).
+int gather_rows(const NcclApi *api, ncclComm_t comm, cudaStream_t st, float *C_full, int64_t M,
+                int64_t N, int world, int rank) {
+  int64_t r0, rows;
+  partition_rows(M, world, rank, &r0, &rows);
+  if (M % world == 0) {
+    return nccl_check(api->AllGather(C_full + r0 * N, C_full, size_t(rows * N), ncclFloat32,
+                                     comm, st),
+                      "ncclAllGather(C)");
+  }
+  for (int o = 0; o < world; ++o) {
+    int64_t o0, orows;
+    partition_rows(M, world, o, &o0, &orows);
+    if (orows == 0) continue;
+    TRY(nccl_check(api->Broadcast(C_full + o0 * N, C_full + o0 * N, size_t(orows * N),
+                                  ncclFloat32, o, comm, st),
+                   "ncclBroadcast(C block)"));
+  }
+  return GIGA_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// argument checks
+
+bool overlaps(const void *a, size_t abytes, const void *b, size_t bbytes) {
+  const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + bbytes && y < x + abytes;
+}
+
+int check_dims(int64_t M, int64_t N, int64_t K) {
+  if (M < 1 || N < 1 || K < 1)
+    return fail(GIGA_ERR_INVALID_ARG, "M, N, K must be >= 1 (got %lld, %lld, %lld)",
+                (long long)M, (long long)N, (long long)K);
+  const int64_t lim = int64_t(1) << 31;
+  if (M >= lim || N >= lim || K >= lim || M > (int64_t(1) << 62) / N ||
+      K > (int64_t(1) << 62) / N || M > (int64_t(1) << 62) / K)
+    return fail(GIGA_ERR_INVALID_ARG, "matrix dimensions too large");
+  return GIGA_OK;
+}
+
+// pointer kind: 1 = device (dev set), 0 = host
+int pointer_kind(const void *p, int *dev) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (a.type == cudaMemoryTypeDevice) {
+    *dev = a.device;
+    return 1;
+  }
+  return 0;
+}
+
+int sync_all(int ngpus) {
+  for (int i = 0; i < ngpus; ++i) {
+    DevCtx &d = g.devs[i];
+    CK(cudaSetDevice(d.dev));
+    CK(cudaStreamSynchronize(d.compute));
+    CK(cudaStreamSynchronize(d.comm));
+  }
+  return GIGA_OK;
+}
+
+// Device-resident path on GPUs 0..ngpus-1 (B_buf[0] root, C_full[g] all receive full C).
+int sharded_locked(const float *const *A_shard, float *const *B_buf, float *const *C_full,
+                   int64_t M, int64_t N, int64_t K, int ngpus) {
+  if (ngpus == 1) {
+    DevCtx &d = g.devs[0];
+    CK(cudaSetDevice(d.dev));
+    TRY(shard_compute(d, d.compute, A_shard[0], M, B_buf[0], C_full[0], N, N, K, nullptr));
+    return sync_all(1);
+  }
+  std::vector<ncclComm_t> *comms = nullptr;
+  TRY(get_comms(ngpus, &comms));
+  const NcclApi *api = nccl_api(nullptr);
+  // (1) distribute B: broadcast from GPU 0 on the comm streams
+  TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
+  for (int i = 0; i < ngpus; ++i) {
+    DevCtx &d = g.devs[i];
+    CK(cudaSetDevice(d.dev));
+    ncclResult_t r = api->Broadcast(B_buf[0], B_buf[i], size_t(K * N), ncclFloat32, 0,
+                                    (*comms)[i], d.comm);
+    if (r != ncclSuccess) {
+      api->GroupEnd();
+      return nccl_check(r, "ncclBroadcast(B)");
+    }
+  }
+  TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
+  // (2) per GPU: split A (overlaps the broadcast), then B, then the GEMM
+  for (int i = 0; i < ngpus; ++i) {
+    DevCtx &d = g.devs[i];
+    CK(cudaSetDevice(d.dev));
+    CK(cudaEventRecord(d.ev_b, d.comm));
+    int64_t r0, rows;
+    partition_rows(M, ngpus, i, &r0, &rows);
+    TRY(shard_compute(d, d.compute, A_shard[i], rows, B_buf[i], C_full[i] + r0 * N, N, N, K,
+                      d.ev_b));
+    CK(cudaEventRecord(d.ev_c, d.compute));
+    CK(cudaStreamWaitEvent(d.comm, d.ev_c, 0));
+  }
+  // (3) gather the C row blocks on every GPU
+  TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
+  for (int i = 0; i < ngpus; ++i) {
+    DevCtx &d = g.devs[i];
+    CK(cudaSetDevice(d.dev));
+    int rc = gather_rows(api, (*comms)[i], d.comm, C_full[i], M, N, ngpus, i);
+    if (rc != GIGA_OK) {
+      api->GroupEnd();
+      return rc;
+    }
+  }
+  TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
+  TRY(sync_all(ngpus));
+  for (int i = 0; i < ngpus; ++i) {
+    ncclResult_t ar = ncclSuccess;
+    api->CommGetAsyncError((*comms)[i], &ar);
+    TRY(nccl_check(ar, "NCCL async"));
+  }
+  return GIGA_OK;
+}
+
+int matmul_locked(const float *A, const float *B, float *C, int64_t M, int64_t N, int64_t K,
+                  int ngpus) {
+  int da = -1, db = -1, dc = -1;
+  const int ka = pointer_kind(A, &da), kb = pointer_kind(B, &db), kc = pointer_kind(C, &dc);
+  if (ka != kb || kb != kc)
+    return fail(GIGA_ERR_INVALID_ARG, "A, B, C must be all host or all device pointers");
+  const bool device = ka == 1;
+  if (device && (da != g.devs[0].dev || db != g.devs[0].dev || dc != g.devs[0].dev))
+    return fail(GIGA_ERR_INVALID_ARG, "device pointers must all live on GPU %d", g.devs[0].dev);
+
+  if (device && ngpus == 1) {
+    DevCtx &d = g.devs[0];
+    CK(cudaSetDevice(d.dev));
+    TRY(shard_compute(d, d.compute, A, M, B, C, N, N, K, nullptr));
+    return sync_all(1);
+  }
+
+  // Stage: every GPU gets its A row block and a B buffer; GPU 0 gets B.
+  for (int i = 0; i < ngpus; ++i) {
+    DevCtx &d = g.devs[i];
+    CK(cudaSetDevice(d.dev));
+    int64_t r0, rows;
+    partition_rows(M, ngpus, i, &r0, &rows);
+    const bool own_b = !(device && i == 0);
+    TRY(ws_reserve(d, {{&d.A_h, size_t(std::max<int64_t>(rows, 1) * K) * 4},
+                       {&d.B_h, own_b ? size_t(K * N) * 4 : 0},
+                       {&d.C_h, size_t(std::max<int64_t>(rows, 1) * N) * 4}}));
+    if (rows > 0)
+      CK(cudaMemcpyAsync(d.A_h.p, A + r0 * K, size_t(rows * K) * 4,
+                         device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, d.compute));
+    if (i == 0 && !device)
+      CK(cudaMemcpyAsync(d.B_h.p, B, size_t(K * N) * 4, cudaMemcpyHostToDevice, d.compute));
+  }
+  const float *B0 = device ? B : fptr(g.devs[0].B_h);
+  if (ngpus > 1) {
+    std::vector<ncclComm_t> *comms = nullptr;
+    TRY(get_comms(ngpus, &comms));
+    const NcclApi *api = nccl_api(nullptr);
+    // B must be on GPU 0 before the broadcast reads it
+    CK(cudaSetDevice(g.devs[0].dev));
+    CK(cudaEventRecord(g.devs[0].ev_start, g.devs[0].compute));
+    for (int i = 0; i < ngpus; ++i) {
+      CK(cudaSetDevice(g.devs[i].dev));
+      CK(cudaStreamWaitEvent(g.devs[i].comm, g.devs[0].ev_start, 0));
+    }
+    TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
+    for (int i = 0; i < ngpus; ++i) {
+      DevCtx &d = g.devs[i];
+      CK(cudaSetDevice(d.dev));
+      float *dst = (i == 0) ? const_cast<float *>(B0) : fptr(d.B_h);
+      ncclResult_t r =
+          api->Broadcast(B0, dst, size_t(K * N), ncclFloat32, 0, (*comms)[i], d.comm);
+      if (r != ncclSuccess) {
+        api->GroupEnd();
+        return nccl_check(r, "ncclBroadcast(B)");
+      }
+    }
+    TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
+  }
+  for (int i = 0; i < ngpus; ++i) {
+    DevCtx &d = g.devs[i];
+    CK(cudaSetDevice(d.dev));
+    int64_t r0, rows;
+    partition_rows(M, ngpus, i, &r0, &rows);
+    cudaEvent_t wait = nullptr;
+    if (ngpus > 1) {
+      CK(cudaEventRecord(d.ev_b, d.comm));
+      wait = d.ev_b;
+    }
+    const float *Bi = (i == 0) ? B0 : fptr(d.B_h);
+    float *Ci = (device && i == 0) ? C + r0 * N : fptr(d.C_h);
+    TRY(shard_compute(d, d.compute, fptr(d.A_h), rows, Bi, Ci, N, N, K, wait));
+    if (rows > 0 && !(device && i == 0))
+      CK(cudaMemcpyAsync(C + r0 * N, d.C_h.p, size_t(rows * N) * 4,
+                         device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, d.compute));
+  }
+  return sync_all(ngpus);
+}
+
+}  // namespace
+}  // namespace giga
+
+using namespace giga;
+
+// =========================================================================================
+// C ABI
+extern "C" {
+
+const char *giga_last_error(void) { return t_err.c_str(); }
+
+int giga_partition(int64_t M, int ngpus, int gi, int64_t *row0, int64_t *rows) {
+  if (M < 0 || ngpus < 1 || gi < 0 || gi >= ngpus || !row0 || !rows)
+    return fail(GIGA_ERR_INVALID_ARG, "giga_partition: bad arguments");
+  partition_rows(M, ngpus, gi, row0, rows);
+  return GIGA_OK;
+}
+
+int giga_num_devices(void) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  return g.mode == 1 ? int(g.devs.size()) : (g.mode == 2 ? 1 : 0);
+}
+
+int giga_init(int ngpus_max) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.mode != 0) return fail(GIGA_ERR_ALREADY_INITIALIZED, "giga_init: already initialised");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(GIGA_ERR_NO_DEVICE, "no CUDA device visible");
+  }
+  const int n = ngpus_max <= 0 ? count : ngpus_max;
+  if (n > count)
+    return fail(GIGA_ERR_NO_DEVICE, "asked for %d GPUs, %d visible", ngpus_max, count);
+  for (int i = 0; i < n; ++i) TRY(check_sm100(i));
+  if (ensure_tma_encoder() != 0)
+    return fail(GIGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  g.devs.assign(n, DevCtx{});
+  for (int i = 0; i < n; ++i) {
+    int rc = ctx_create(g.devs[i], i);
+    if (rc != GIGA_OK) {
+      for (auto &d : g.devs) ctx_destroy(d);
+      g.devs.clear();
+      return rc;
+    }
+  }
+  // peer access so NCCL / copies can use NVLink directly (best effort)
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      if (i == j) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, i, j);
+      if (can) {
+        cudaSetDevice(i);
+        cudaDeviceEnablePeerAccess(j, 0);
+        cudaGetLastError();
+      }
+    }
+  g.mode = 1;
+  return GIGA_OK;
+}
+
+int giga_finalize(void) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.mode == 0) return GIGA_OK;
+  const NcclApi *api = nccl_api(nullptr);
+  if (api) {
+    for (auto &kv : g.comms)
+      for (ncclComm_t c : kv.second)
+        if (c) api->CommDestroy(c);
+    if (g.rank_comm) api->CommDestroy(g.rank_comm);
+  }
+  g.comms.clear();
+  g.rank_comm = nullptr;
+  for (auto &d : g.devs) ctx_destroy(d);
+  g.devs.clear();
+  {
+    std::lock_guard<std::mutex> tl(g_tmu);
+    for (auto &r : g_tpending) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    g_tpending.clear();
+    for (auto &p : g_tpool) cudaEventDestroy(p.second);
+    g_tpool.clear();
+  }
+  g.mode = 0;
+  return GIGA_OK;
+}
+
+int giga_matmul(const float *A, const float *B, float *C, int64_t M, int64_t N, int64_t K,
+                int ngpus) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.mode != 1) return fail(GIGA_ERR_NOT_INITIALIZED, "giga_matmul: call giga_init first");
+  if (!A || !B || !C) return fail(GIGA_ERR_INVALID_ARG, "giga_matmul: NULL pointer");
+  TRY(check_dims(M, N, K));
+  if (ngpus < 1 || ngpus > int(g.devs.size()))
+    return fail(GIGA_ERR_INVALID_ARG, "ngpus=%d outside [1, %d]", ngpus, int(g.devs.size()));
+  if (overlaps(C, size_t(M * N) * 4, A, size_t(M * K) * 4) ||
+      overlaps(C, size_t(M * N) * 4, B, size_t(K * N) * 4))
+    return fail(GIGA_ERR_INVALID_ARG, "C overlaps A or B");
+  return matmul_locked(A, B, C, M, N, K, ngpus);
+}
+
+int giga_matmul_sharded(const float *const *A_shard, float *const *B_buf, float *const *C_full,
+                        int64_t M, int64_t N, int64_t K, int ngpus) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.mode != 1)
+    return fail(GIGA_ERR_NOT_INITIALIZED, "giga_matmul_sharded: call giga_init first");
+  if (!A_shard || !B_buf || !C_full) return fail(GIGA_ERR_INVALID_ARG, "NULL pointer array");
+  TRY(check_dims(M, N, K));
+  if (ngpus < 1 || ngpus > int(g.devs.size()))
+    return fail(GIGA_ERR_INVALID_ARG, "ngpus=%d outside [1, %d]", ngpus, int(g.devs.size()));
+  for (int i = 0; i < ngpus; ++i) {
+    int64_t r0, rows;
+    partition_rows(M, ngpus, i, &r0, &rows);
+    if ((rows > 0 && !A_shard[i]) || !B_buf[i] || !C_full[i])
+      return fail(GIGA_ERR_INVALID_ARG, "NULL buffer for GPU %d", i);
+    int dv = -1;
+    if (pointer_kind(C_full[i], &dv) != 1 || dv != g.devs[i].dev ||
+        pointer_kind(B_buf[i], &dv) != 1 || dv != g.devs[i].dev ||
+        (rows > 0 && (pointer_kind(A_shard[i], &dv) != 1 || dv != g.devs[i].dev)))
+      return fail(GIGA_ERR_INVALID_ARG, "buffers for GPU %d must be device memory on it", i);
+    if (overlaps(C_full[i], size_t(M * N) * 4, B_buf[i], size_t(K * N) * 4) ||
+        (rows > 0 && overlaps(C_full[i], size_t(M * N) * 4, A_shard[i], size_t(rows * K) * 4)))
+      return fail(GIGA_ERR_INVALID_ARG, "C_full[%d] overlaps A or B", i);
+  }
+  return sharded_locked(A_shard, B_buf, C_full, M, N, K, ngpus);
+}
+
+// ---- multi-process (one process per GPU) ------------------------------------------------
+
+int giga_comm_unique_id(uint8_t id[128]) {
+  if (!id) return fail(GIGA_ERR_INVALID_ARG, "NULL id");
+  const char *why = nullptr;
+  const NcclApi *api = nccl_api(&why);
+  if (!api) return fail(GIGA_ERR_COMM, "NCCL unavailable: %s", why ? why : "?");
+  ncclUniqueId u;
+  TRY(nccl_check(api->GetUniqueId(&u), "ncclGetUniqueId"));
+  memcpy(id, u.internal, 128);
+  return GIGA_OK;
+}
+
+int giga_rank_init(int rank, int world, int device, const uint8_t id[128]) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.mode != 0)
+    return fail(GIGA_ERR_ALREADY_INITIALIZED, "giga_rank_init: already initialised");
+  if (world < 1 || rank < 0 || rank >= world || device < 0 || (world > 1 && !id))
+    return fail(GIGA_ERR_INVALID_ARG, "giga_rank_init: bad rank/world/device/id");
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || device >= count) {
+    cudaGetLastError();
+    return fail(GIGA_ERR_NO_DEVICE, "device %d not visible", device);
+  }
+  TRY(check_sm100(device));
+  if (ensure_tma_encoder() != 0)
+    return fail(GIGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  g.devs.assign(1, DevCtx{});
+  int rc = ctx_create(g.devs[0], device);
+  if (rc != GIGA_OK) {
+    ctx_destroy(g.devs[0]);
+    g.devs.clear();
+    return rc;
+  }
+  if (world > 1) {
+    const char *why = nullptr;
+    const NcclApi *api = nccl_api(&why);
+    if (!api) {
+      ctx_destroy(g.devs[0]);
+      g.devs.clear();
+      return fail(GIGA_ERR_COMM, "NCCL unavailable: %s", why ? why : "?");
+    }
+    ncclUniqueId u;
+    memcpy(u.internal, id, 128);
+    cudaSetDevice(device);
+    rc = nccl_check(api->CommInitRank(&g.rank_comm, world, u, rank), "ncclCommInitRank");
+    if (rc != GIGA_OK) {
+      ctx_destroy(g.devs[0]);
+      g.devs.clear();
+      return rc;
+    }
+  }
+  g.rank = rank;
+  g.world = world;
+  g.mode = 2;
+  return GIGA_OK;
+}
+
+int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, int64_t N,
+                     int64_t K, void *stream) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.mode != 2) return fail(GIGA_ERR_NOT_INITIALIZED, "giga_matmul_rank: not initialised");
+  TRY(check_dims(M, N, K));
+  int64_t r0, rows;
+  partition_rows(M, g.world, g.rank, &r0, &rows);
+  if ((rows > 0 && !A_shard) || !B || !C_full)
+    return fail(GIGA_ERR_INVALID_ARG, "giga_matmul_rank: NULL pointer");
+  DevCtx &d = g.devs[0];
+  CK(cudaSetDevice(d.dev));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.compute;
+  if (g.world == 1)
+    return shard_compute(d, st, A_shard, rows, B, C_full + r0 * N, N, N, K, nullptr);
+  const NcclApi *api = nccl_api(nullptr);
+  // comm stream joins the caller's stream, broadcasts B, and later gathers C
+  CK(cudaEventRecord(d.ev_start, st));
+  CK(cudaStreamWaitEvent(d.comm, d.ev_start, 0));
+  TRY(nccl_check(api->Broadcast(B, B, size_t(K * N), ncclFloat32, 0, g.rank_comm, d.comm),
+                 "ncclBroadcast(B)"));
+  CK(cudaEventRecord(d.ev_b, d.comm));
+  TRY(shard_compute(d, st, A_shard, rows, B, C_full + r0 * N, N, N, K, d.ev_b));
+  CK(cudaEventRecord(d.ev_c, st));
+  CK(cudaStreamWaitEvent(d.comm, d.ev_c, 0));
+  TRY(gather_rows(api, g.rank_comm, d.comm, C_full, M, N, g.world, g.rank));
+  // the caller's stream resumes after the gather
+  CK(cudaEventRecord(d.ev_c, d.comm));
+  CK(cudaStreamWaitEvent(st, d.ev_c, 0));
+  return GIGA_OK;
+}
+
+// ---- building blocks ---------------------------------------------------------------------
+
+int giga_split_lo(const float *x, float *lo, int64_t n, void *stream) {
+  if (!x || !lo || n < 0 || !aligned16(x) || !aligned16(lo))
+    return fail(GIGA_ERR_INVALID_ARG, "giga_split_lo: bad arguments");
+  return split(x, lo, n, static_cast<cudaStream_t>(stream));
+}
+
+int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const float *B_lo,
+                        float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, int terms,
+                        int promote_kblocks, void *stream) {
+  if (!A || !B || !C || (terms == 3 && (!A_lo || !B_lo)) || (terms != 1 && terms != 3))
+    return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_3xtf32: bad pointers/terms");
+  TRY(check_dims(M, N, K));
+  if ((K & 3) || (N & 3) || (ldc & 3) || ldc < N || !aligned16(A) || !aligned16(B) ||
+      !aligned16(C) || (A_lo && !aligned16(A_lo)) || (B_lo && !aligned16(B_lo)))
+    return fail(GIGA_ERR_INVALID_ARG,
+                "giga_gemm_3xtf32: needs K%%4 == N%%4 == ldc%%4 == 0, ldc >= N, 16B-aligned");
+  if (ensure_tma_encoder() != 0) return fail(GIGA_ERR_CUDA, "TMA encoder unavailable");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(timed(0, st, [&] {
+    return launch_gemm_3xtf32(A, A_lo, B, B_lo, C, M, N, K, ldc, terms, promote_kblocks, st);
+  }));
+  return GIGA_OK;
+}
+
+int giga_gemm_3xtf32(const float *A, const float *A_lo, const float *B, const float *B_lo,
+                     float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, void *stream) {
+  return giga_gemm_3xtf32_ex(A, A_lo, B, B_lo, C, M, N, K, ldc, 3, -1, stream);
+}
+
+// ---- timing ------------------------------------------------------------------------------
+
+int giga_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_timing = on != 0;
+  return GIGA_OK;
+}
+
+int giga_timing_reset(void) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  for (auto &r : g_tpending) {
+    cudaEventSynchronize(r.b);
+    g_tpool.push_back({r.dev, r.a});
+    g_tpool.push_back({r.dev, r.b});
+  }
+  g_tpending.clear();
+  g_tms[0] = g_tms[1] = 0;
+  g_tcount[0] = g_tcount[1] = 0;
+  return GIGA_OK;
+}
+
+int giga_timing_read(double *gemm_ms, int64_t *gemm_launches, double *split_ms,
+                     int64_t *split_launches) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  for (auto &r : g_tpending) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    float ms = 0;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+    } else {
+      g_tms[r.kind] += ms;
+      g_tcount[r.kind] += 1;
+    }
+    g_tpool.push_back({r.dev, r.a});
+    g_tpool.push_back({r.dev, r.b});
+  }
+  g_tpending.clear();
+  if (gemm_ms) *gemm_ms = g_tms[0];
+  if (gemm_launches) *gemm_launches = g_tcount[0];
+  if (split_ms) *split_ms = g_tms[1];
+  if (split_launches) *split_launches = g_tcount[1];
+  return GIGA_OK;
+}
+
+}  // extern "C"

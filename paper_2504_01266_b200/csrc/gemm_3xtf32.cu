@@ -1,0 +1,428 @@
+// gemm_3xtf32.cu -- the shard GEMM of GigaAPI's row-split matrix multiply, sm_100a.
+//
+// What it computes (S4.2.7): C[i][j] = sum_k A[i][k] * B[k][j] for the
+// rows of one shard, every element assigned once at the end ("the total sum being reported
+// and assigned at the end of the loop"). The paper's kernel is one scalar thread per C
+// element on sm_75 (16x16 blocks PAPER.md:194); this is a B200 design:
+//
+//   * fp32 accuracy from TF32 tensor cores (BASELINE.json north_star (3)): x = hi + lo with
+//     hi = the tensor core's own TF32 reading of the raw fp32 bits and lo = x - hi (exact),
+//     produced by split_lo_kernel. Per 8-wide k step three tcgen05.mma.kind::tf32 are issued
+//     into one TMEM accumulator, small terms first: a_lo*b_hi, a_hi*b_lo, a_hi*b_hi
+//     (a_lo*b_lo, ~2^-20 relative, is dropped). hi is never materialised: the MMA is fed
+//     the raw fp32 tile and reads only its TF32 part.
+//   * Accumulator promotion: the tensor core's fp32 accumulation is not round-to-nearest
+//     (measured), so every `p_kb` k-blocks the MMA warp switches to the other of
+//     two TMEM accumulators and the epilogue warps add the finished partial into an fp32
+//     register sum with round-to-nearest adds.
+//   * Warp specialisation, persistent CTAs (one per SM, 1 CTA/SM by smem):
+//       warp 0 lane 0  TMA producer: A, A_lo tiles (K-major, 64B swizzle) and B, B_lo tiles
+//                      (N-major, 128B swizzle) into a 4-stage smem ring (mbarrier full/empty)
+//       warp 1 lane 0  MMA issuer: 3 UMMAs per k8, tcgen05.commit frees smem stages and
+//                      publishes finished accumulators
+//       warps 2..9     epilogue: tcgen05.ld TMEM -> registers, RN fp32 promotion adds,
+//                      16-byte vector stores into the shard's rows of C.
+//
+// Tile: 128 (M) x 256 (N) per CTA, k-block 16 (two k8 UMMA steps), TMEM 2 x 256 columns.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+#include <mutex>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace giga {
+
+namespace cfg {
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 16;
+constexpr int STAGES = 4;
+constexpr int NUM_EPI_WARPS = 8;
+constexpr int NUM_THREADS = 64 + NUM_EPI_WARPS * 32;
+constexpr uint32_t A_BYTES = BM * BK * 4;          // 8 KiB: 128 rows x 64 B
+constexpr uint32_t B_BYTES = BK * BN * 4;          // 16 KiB: 8 chunks x (16 rows x 128 B)
+constexpr uint32_t B_CHUNK_BYTES = BK * 32 * 4;    // 2 KiB: one 32-column chunk of B
+constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 48 KiB
+constexpr uint32_t ACC_COLS = BN;                  // fp32 accumulator: 1 TMEM column per n
+constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;       // two accumulators (promotion ping-pong)
+constexpr int GROUP_M = 16;                        // L2 raster: 16 M-tiles per group
+constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
+}  // namespace cfg
+
+struct GemmParams {
+  int M, N, K, ldc;
+  int terms;      // 3 = 3xTF32, 1 = TF32 (hi*hi only)
+  int p_kb;       // k-blocks per TMEM accumulation interval (>= 1)
+  int n_kb;       // k-blocks per tile
+  int m_tiles, n_tiles, num_tiles;
+};
+
+// ---- UMMA descriptors -------------------------------------------------------------------
+// Shared-memory matrix descriptor (sm100, "version 1"):
+//   [0,14) start address >> 4   [16,30) leading byte offset >> 4   [32,46) stride byte
+//   offset >> 4   [46,48) version = 1   [49,52) base offset = 0   [52] lbo mode = 0
+//   [61,64) layout: 2 = SWIZZLE_128B, 4 = SWIZZLE_64B
+// A (K-major, SW64): rows of 64 B (16 fp32 of K), 8-row atoms of 512 B -> SBO = 512; LBO is
+//   unused for swizzled K-major (1). The k8 step j starts 32 B further into the row.
+// B (N-major, SW128): rows of 128 B = 32 n, one row per k; 8-row atoms (1 KiB) -> SBO = 1024
+//   between k-groups; 32-column chunks 2 KiB apart -> LBO = 2048. The k8 step j starts
+//   j * 1024 B further.
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                               uint32_t layout) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(layout & 7) << 61;
+  return d;
+}
+// Instruction descriptor, kind::tf32: [4,6) D fmt = 1 (F32); [7,10) A fmt = 2 (TF32);
+// [10,13) B fmt = 2 (TF32); [15] A major = 0 (K); [16] B major = 1 (MN); [17,23) N >> 3;
+// [24,29) M >> 4.
+__host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+         (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void tile_coords(int t, const GemmParams &p, int &mb, int &nb) {
+  const int group_size = cfg::GROUP_M * p.n_tiles;
+  const int g = t / group_size;
+  const int first_m = g * cfg::GROUP_M;
+  const int gm = min(cfg::GROUP_M, p.m_tiles - first_m);
+  const int local = t - g * group_size;
+  mb = first_m + local % gm;
+  nb = local / gm;
+}
+
+__global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
+    gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmA,
+                       const __grid_constant__ CUtensorMap tmAlo,
+                       const __grid_constant__ CUtensorMap tmB,
+                       const __grid_constant__ CUtensorMap tmBlo, float *__restrict__ C,
+                       const GemmParams p) {
+  using namespace cfg;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    if (p.terms == 3) {
+      ptx::prefetch_tmap(&tmAlo);
+      ptx::prefetch_tmap(&tmBlo);
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], NUM_EPI_WARPS);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int n_int = (p.n_kb + p.p_kb - 1) / p.p_kb;
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      const uint32_t tx = p.terms == 3 ? STAGE_BYTES : (A_BYTES + B_BYTES);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, p, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < p.n_kb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *sA = smem + stage * STAGE_BYTES;
+          uint8_t *sAlo = sA + A_BYTES;
+          uint8_t *sB = sA + 2 * A_BYTES;
+          uint8_t *sBlo = sB + B_BYTES;
+          const int k0 = kb * BK;
+          ptx::mbar_expect_tx(&full[stage], tx);
+          ptx::tma_load_2d(sA, &tmA, &full[stage], k0, m0);
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c)
+            ptx::tma_load_2d(sB + c * B_CHUNK_BYTES, &tmB, &full[stage], n0 + 32 * c, k0);
+          if (p.terms == 3) {
+            ptx::tma_load_2d(sAlo, &tmAlo, &full[stage], k0, m0);
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c)
+              ptx::tma_load_2d(sBlo + c * B_CHUNK_BYTES, &tmBlo, &full[stage], n0 + 32 * c, k0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t acc_iter = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int kb = 0;
+        for (int it = 0; it < n_int; ++it, ++acc_iter) {
+          const uint32_t buf = acc_iter & 1, use = acc_iter >> 1;
+          ptx::mbar_wait(&tempty[buf], (use & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t d_tmem = tmem_base + buf * ACC_COLS;
+          const int kb_end = min(kb + p.p_kb, p.n_kb);
+          uint32_t acc = 0;
+          for (; kb < kb_end; ++kb) {
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            const uint32_t sA = ptx::smem_u32(smem + stage * STAGE_BYTES);
+            const uint32_t sAlo = sA + A_BYTES;
+            const uint32_t sB = sA + 2 * A_BYTES;
+            const uint32_t sBlo = sB + B_BYTES;
+#pragma unroll
+            for (int k8 = 0; k8 < BK / 8; ++k8) {
+              const uint64_t dA = make_sdesc(sA + 32 * k8, 16, 512, 4);
+              const uint64_t dB = make_sdesc(sB + 1024 * k8, B_CHUNK_BYTES, 1024, 2);
+              if (p.terms == 3) {
+                const uint64_t dAlo = make_sdesc(sAlo + 32 * k8, 16, 512, 4);
+                const uint64_t dBlo = make_sdesc(sBlo + 1024 * k8, B_CHUNK_BYTES, 1024, 2);
+                ptx::mma_tf32(d_tmem, dAlo, dB, idesc, acc);
+                ptx::mma_tf32(d_tmem, dA, dBlo, idesc, 1u);
+                acc = 1;
+              }
+              ptx::mma_tf32(d_tmem, dA, dB, idesc, acc);
+              acc = 1;
+            }
+            ptx::mma_commit(&empty[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          ptx::mma_commit(&tfull[buf]);
+        }
+      }
+    }
+  } else {
+    // ======================= epilogue (8 warps) =======================
+    const int e = warp - 2;
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const int half = e >> 2;    // column half of the 256-wide tile
+    const int row_in_tile = quad * 32 + lane;
+    uint32_t acc_iter = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, p, mb, nb);
+      float sum[128];  // fp32 running sum of the promoted partials (0 + p == p exactly)
+#pragma unroll
+      for (int j = 0; j < 128; ++j) sum[j] = 0.0f;
+      for (int it = 0; it < n_int; ++it, ++acc_iter) {
+        const uint32_t buf = acc_iter & 1, use = acc_iter >> 1;
+        ptx::mbar_wait(&tfull[buf], use & 1);
+        ptx::tc_fence_after();
+        const uint32_t taddr =
+            tmem_base + (uint32_t(quad * 32) << 16) + buf * ACC_COLS + half * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float v[16];
+          ptx::tmem_ld16_wait(taddr + c * 16, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) sum[c * 16 + j] = __fadd_rn(sum[c * 16 + j], v[j]);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+      }
+      // store this thread's row segment: 128 consecutive fp32 = 32 x 16 B
+      const int row = mb * BM + row_in_tile;
+      if (row < p.M) {
+        const int col0 = nb * BN + half * 128;
+        float *crow = C + int64_t(row) * p.ldc + col0;
+        if (col0 + 128 <= p.N) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            reinterpret_cast<float4 *>(crow)[j] =
+                make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + 4 * j < p.N)  // N % 4 == 0: a float4 is all-in or all-out
+              reinterpret_cast<float4 *>(crow)[j] =
+                  make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ---- split: lo = x - tf32(x) ------------------------------------------------------------
+// tf32(x) is what kind::tf32 reads from raw fp32 bits: the top 19 bits (sign, exponent,
+// 10 mantissa bits), i.e. truncation toward zero of the low 13 mantissa bits (measured on
+// B200 by tests/test_gpu_probe.py). x - tf32(x) is exact in fp32 (same sign, the 13 low
+// bits of x's significand).
+__device__ __forceinline__ float tf32_lo(float x) {
+  const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  return __fsub_rn(x, hi);
+}
+
+__global__ void __launch_bounds__(256) split_lo_kernel(const float *__restrict__ x,
+                                                       float *__restrict__ lo, int64_t n) {
+  const int64_t n4 = n >> 2;
+  const float4 *x4 = reinterpret_cast<const float4 *>(x);
+  float4 *lo4 = reinterpret_cast<float4 *>(lo);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  // 4 independent 16-byte loads in flight per thread
+  for (; i + 3 * stride < n4; i += 4 * stride) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(x4 + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      __stcs(lo4 + i + u * stride,
+             make_float4(tf32_lo(v[u].x), tf32_lo(v[u].y), tf32_lo(v[u].z), tf32_lo(v[u].w)));
+  }
+  for (; i < n4; i += stride) {
+    const float4 v = __ldcs(x4 + i);
+    __stcs(lo4 + i, make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w)));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const int64_t j = (n4 << 2) + threadIdx.x;
+    lo[j] = tf32_lo(x[j]);
+  }
+}
+
+// ---- host side ----------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+int ensure_tma_encoder() {
+  std::call_once(g_encode_once, [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode ? 0 : -1;
+}
+
+// 2-D fp32 map over a row-major (rows x cols, row stride ld elements) matrix.
+static bool make_map(CUtensorMap *m, const float *ptr, uint64_t cols, uint64_t rows,
+                     uint64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle sw) {
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * sizeof(float)};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int num_sms_current() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t n4 = (n + 3) / 4;
+  int64_t blocks = (n4 + 255) / 256;
+  const int64_t cap = int64_t(num_sms_current()) * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  split_lo_kernel<<<unsigned(blocks), 256, 0, st>>>(x, lo, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
+                               const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,
+                               int64_t ldc, int terms, int promote_kblocks, cudaStream_t st) {
+  using namespace cfg;
+  if (M < 1 || N < 1 || K < 1 || (K & 3) || (N & 3) || (ldc & 3) || ldc < N)
+    return cudaErrorInvalidValue;
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || ldc > INT32_MAX)
+    return cudaErrorInvalidValue;
+  if (terms != 1 && terms != 3) return cudaErrorInvalidValue;
+  if (terms == 3 && (!A_lo || !B_lo)) return cudaErrorInvalidValue;
+  if (ensure_tma_encoder() != 0) return cudaErrorNotSupported;
+
+  CUtensorMap tA, tAlo, tB, tBlo;
+  if (!make_map(&tA, A, K, M, K, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !make_map(&tB, B, N, K, N, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  if (terms == 3) {
+    if (!make_map(&tAlo, A_lo, K, M, K, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !make_map(&tBlo, B_lo, N, K, N, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+  } else {
+    tAlo = tA;
+    tBlo = tB;
+  }
+
+  GemmParams p;
+  p.M = int(M);
+  p.N = int(N);
+  p.K = int(K);
+  p.ldc = int(ldc);
+  p.terms = terms;
+  p.n_kb = int((K + BK - 1) / BK);
+  int pk = promote_kblocks < 0 ? kDefaultPromoteKBlocks : promote_kblocks;
+  p.p_kb = (pk == 0 || pk > p.n_kb) ? p.n_kb : pk;
+  p.m_tiles = int((M + BM - 1) / BM);
+  p.n_tiles = int((N + BN - 1) / BN);
+  p.num_tiles = p.m_tiles * p.n_tiles;
+
+  // the smem opt-in is a per-device function attribute
+  static std::mutex attr_mu;
+  static uint64_t attr_done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(attr_mu);
+    if (!(attr_done >> (dev & 63) & 1)) {
+      cudaError_t e = cudaFuncSetAttribute(
+          gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+      if (e != cudaSuccess) return e;
+      attr_done |= uint64_t(1) << (dev & 63);
+    }
+  }
+
+  const int grid = p.num_tiles < num_sms_current() ? p.num_tiles : num_sms_current();
+  gemm_3xtf32_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(tA, tAlo, tB, tBlo, C, p);
+  return cudaGetLastError();
+}
+
+}  // namespace giga

@@ -1,0 +1,26 @@
+// kernels.h -- host-side launchers of the sm_100a kernels (internal to libgiga).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace giga {
+
+// Default number of 16-wide k-blocks accumulated in TMEM before promotion into the fp32
+// register sum. 16 k-blocks = K 256 = 32 k8 steps.
+constexpr int kDefaultPromoteKBlocks = 16;
+
+// lo = x - tf32(x) over n elements (HBM-bound elementwise split).
+cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t st);
+
+// C[M x N, row stride ldc] = A[M x K] * B[K x N] by 3xTF32 (terms = 3) or 1xTF32 (terms = 1)
+// on the tcgen05 tensor cores. Requires K % 4 == 0, N % 4 == 0, ldc % 4 == 0, 16B-aligned
+// pointers. promote_kblocks: 0 = never, -1 = default. Returns cudaErrorInvalidValue for bad
+// shapes, or the launch error.
+cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
+                               const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,
+                               int64_t ldc, int terms, int promote_kblocks, cudaStream_t st);
+
+// Resolves cuTensorMapEncodeTiled through the runtime (no libcuda link). 0 on success.
+int ensure_tma_encoder();
+
+}  // namespace giga

@@ -1,0 +1,27 @@
+// nccl_loader.h -- NCCL entry points resolved at run time (dlopen), so libgiga has no
+// link-time dependency on a particular libnccl and single-GPU use never touches NCCL.
+// Types come from the NCCL 2.28 header shipped with the torch wheel.
+#pragma once
+#include <nccl.h>
+
+namespace giga {
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t *, int, const int *) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+  ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+// Returns nullptr (and fills *why) if libnccl.so.2 cannot be loaded.
+const NcclApi *nccl_api(const char **why);
+
+}  // namespace giga

@@ -1,0 +1,198 @@
+"""Thin ctypes binding of libgiga.so (include/giga.h). Argument marshalling only.
+
+Every step of the matrix multiply runs inside libgiga's CUDA kernels and NCCL calls; this
+module converts numpy arrays / torch tensors to raw pointers and status codes to
+exceptions. There is no fallback: if libgiga.so is missing or cannot load, importing this
+module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgiga.so")
+
+GIGA_OK = 0
+STATUS = {
+    0: "GIGA_OK", -1: "GIGA_ERR_INVALID_ARG", -2: "GIGA_ERR_NOT_INITIALIZED",
+    -3: "GIGA_ERR_ALREADY_INITIALIZED", -4: "GIGA_ERR_NO_DEVICE", -5: "GIGA_ERR_OOM",
+    -6: "GIGA_ERR_CUDA", -7: "GIGA_ERR_COMM", -8: "GIGA_ERR_UNSUPPORTED",
+}
+EXPORTS = (
+    "giga_init", "giga_num_devices", "giga_finalize", "giga_partition", "giga_matmul",
+    "giga_matmul_sharded", "giga_last_error", "giga_comm_unique_id", "giga_rank_init",
+    "giga_matmul_rank", "giga_split_lo", "giga_gemm_3xtf32", "giga_gemm_3xtf32_ex",
+    "giga_timing_enable", "giga_timing_reset", "giga_timing_read",
+)
+
+
+class GigaError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (there is no CPU fallback)")
+    # NCCL is dlopen'ed lazily by libgiga; make the torch wheel's copy resolvable first.
+    try:
+        import torch  # noqa: F401  (loads libnccl.so.2 into the process)
+    except Exception:
+        pass
+    lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    i64, i32, p = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+    P64 = ctypes.POINTER(ctypes.c_int64)
+    sig = {
+        "giga_init": ([i32], i32),
+        "giga_num_devices": ([], i32),
+        "giga_finalize": ([], i32),
+        "giga_partition": ([i64, i32, i32, P64, P64], i32),
+        "giga_matmul": ([p, p, p, i64, i64, i64, i32], i32),
+        "giga_matmul_sharded": ([p, p, p, i64, i64, i64, i32], i32),
+        "giga_last_error": ([], ctypes.c_char_p),
+        "giga_comm_unique_id": ([p], i32),
+        "giga_rank_init": ([i32, i32, i32, p], i32),
+        "giga_matmul_rank": ([p, p, p, i64, i64, i64, p], i32),
+        "giga_split_lo": ([p, p, i64, p], i32),
+        "giga_gemm_3xtf32": ([p, p, p, p, p, i64, i64, i64, i64, p], i32),
+        "giga_gemm_3xtf32_ex": ([p, p, p, p, p, i64, i64, i64, i64, i32, i32, p], i32),
+        "giga_timing_enable": ([i32], i32),
+        "giga_timing_reset": ([], i32),
+        "giga_timing_read": ([ctypes.POINTER(ctypes.c_double), P64,
+                              ctypes.POINTER(ctypes.c_double), P64], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+lib = _load()
+
+
+def last_error() -> str:
+    return lib.giga_last_error().decode()
+
+
+def _check(rc: int):
+    if rc != GIGA_OK:
+        raise GigaError(rc, last_error())
+
+
+def _ptr(x):
+    """Raw address of a numpy array / torch tensor (contiguous fp32) or an int."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if isinstance(x, np.ndarray):
+        if not x.flags.c_contiguous:
+            raise ValueError("arrays must be C-contiguous")
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+        return x.data_ptr()
+    raise TypeError(f"cannot take the address of {type(x)}")
+
+
+def _stream(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream  # torch.cuda.Stream
+
+
+# ---- single-process API -----------------------------------------------------------------
+
+def init(ngpus_max: int = 0):
+    _check(lib.giga_init(ngpus_max))
+
+
+def num_devices() -> int:
+    return lib.giga_num_devices()
+
+
+def finalize():
+    _check(lib.giga_finalize())
+
+
+def partition(M: int, ngpus: int, g: int):
+    r0, rows = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.giga_partition(M, ngpus, g, ctypes.byref(r0), ctypes.byref(rows)))
+    return r0.value, rows.value
+
+
+def matmul(A, B, C, M: int, N: int, K: int, ngpus: int = 1):
+    """giga_matmul: A, B, C all host (numpy / pinned torch) or all device (GPU 0)."""
+    _check(lib.giga_matmul(_ptr(A), _ptr(B), _ptr(C), M, N, K, ngpus))
+
+
+def matmul_sharded(A_shards, B_bufs, C_fulls, M: int, N: int, K: int):
+    n = len(C_fulls)
+    arr = ctypes.c_void_p * n
+    a = arr(*[_ptr(x) if x is not None else None for x in A_shards])
+    b = arr(*[_ptr(x) for x in B_bufs])
+    c = arr(*[_ptr(x) for x in C_fulls])
+    _check(lib.giga_matmul_sharded(ctypes.cast(a, ctypes.c_void_p), ctypes.cast(b, ctypes.c_void_p),
+                                   ctypes.cast(c, ctypes.c_void_p), M, N, K, n))
+
+
+# ---- multi-process API ------------------------------------------------------------------
+
+def comm_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib.giga_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return bytes(buf)
+
+
+def rank_init(rank: int, world: int, device: int, uid: bytes | None):
+    buf = (ctypes.c_uint8 * 128)(*uid) if uid is not None else None
+    _check(lib.giga_rank_init(rank, world, device,
+                              ctypes.cast(buf, ctypes.c_void_p) if buf is not None else None))
+
+
+def matmul_rank(A_shard, B, C_full, M: int, N: int, K: int, stream=None):
+    _check(lib.giga_matmul_rank(_ptr(A_shard), _ptr(B), _ptr(C_full), M, N, K, _stream(stream)))
+
+
+# ---- building blocks --------------------------------------------------------------------
+
+def split_lo(x, lo, n: int | None = None, stream=None):
+    n = x.numel() if n is None else n
+    _check(lib.giga_split_lo(_ptr(x), _ptr(lo), n, _stream(stream)))
+
+
+def gemm_3xtf32(A, A_lo, B, B_lo, C, M, N, K, ldc=None, terms=3, promote_kblocks=-1,
+                stream=None):
+    _check(lib.giga_gemm_3xtf32_ex(_ptr(A), _ptr(A_lo), _ptr(B), _ptr(B_lo), _ptr(C), M, N, K,
+                                   N if ldc is None else ldc, terms, promote_kblocks,
+                                   _stream(stream)))
+
+
+# ---- timing -----------------------------------------------------------------------------
+
+def timing_enable(on: bool = True):
+    _check(lib.giga_timing_enable(1 if on else 0))
+
+
+def timing_reset():
+    _check(lib.giga_timing_reset())
+
+
+def timing_read():
+    gm, sm = ctypes.c_double(), ctypes.c_double()
+    gn, sn = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.giga_timing_read(ctypes.byref(gm), ctypes.byref(gn), ctypes.byref(sm),
+                                ctypes.byref(sn)))
+    return {"gemm_ms": gm.value, "gemm_launches": gn.value, "split_ms": sm.value,
+            "split_launches": sn.value}

@@ -1,0 +1,328 @@
+"""GPU parity tests: libgiga (through its C ABI) vs the CPU fp64 oracle, element by element.
+
+Bars (BASELINE.json north_star; R5/R8):
+* integer-valued inputs (synth "d3"): bit-exact;
+* real-valued inputs: |C_gpu - C_ref| <= 1e-5 * sum_k |A_ik||B_kj| per element;
+* C is prefilled with NaN sentinels, so an unwritten element fails.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.check import check_close, check_exact
+import synth
+from golden_io import load
+
+pytestmark = pytest.mark.gpu
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (run with -m 'not gpu' on CPU)"
+    return torch
+
+
+@pytest.fixture(scope="module")
+def giga(torch_cuda):
+    from paper_2504_01266_b200 import build
+    build.build()
+    from paper_2504_01266_b200 import giga as g
+    g.finalize()
+    g.init(1)
+    yield g
+    g.finalize()
+
+
+def _dev(torch, x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def run_host(giga, A, B):
+    """giga_matmul with host pointers (the paper's call)."""
+    M, K = A.shape
+    N = B.shape[1]
+    C = np.full((M, N), np.nan, np.float32)
+    giga.matmul(np.ascontiguousarray(A), np.ascontiguousarray(B), C, M, N, K, 1)
+    return C
+
+
+def run_device(giga, torch, A, B):
+    """giga_matmul with device pointers on GPU 0, C prefilled with NaN."""
+    M, K = A.shape
+    N = B.shape[1]
+    dA, dB = _dev(torch, A), _dev(torch, B)
+    dC = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    giga.matmul(dA, dB, dC, M, N, K, 1)
+    return dC.cpu().numpy()
+
+
+# ---- numerics probes (what the kernel design rests on) ----------------------------------
+
+def test_probe_tf32_operand_conversion_is_truncation(giga, torch_cuda):
+    """kind::tf32 reads raw fp32 operands by dropping the low 13 mantissa bits (RZ).
+
+    The split kernel's lo = x - tf32(x) relies on this. One nonzero product per output,
+    K = 8, plain TF32 (terms=1): C[i,0] = tf32(x_i) * 1 exactly."""
+    torch = torch_cuda
+    M, N, K = 128, 256, 8
+    low = np.array([0x0001, 0x0FFF, 0x1000, 0x1001, 0x1FFF, 0x0800, 0x17FF, 0x0000],
+                   dtype=np.uint32)
+    base = np.array([0x3F800000, 0xBF800000, 0x40490000, 0x3E000000], dtype=np.uint32)
+    xs = (base[:, None] | low[None, :]).reshape(-1)
+    xs = np.resize(xs, M).view(np.float32)
+    A = np.zeros((M, K), np.float32)
+    A[:, 0] = xs
+    B = np.zeros((K, N), np.float32)
+    B[0, :] = 1.0
+    dA, dB = _dev(torch, A), _dev(torch, B)
+    dC = torch.full((M, N), float("nan"), device="cuda")
+    giga.gemm_3xtf32(dA, None, dB, None, dC, M, N, K, terms=1)
+    torch.cuda.synchronize()
+    got = dC.cpu().numpy()[:, 0]
+    rz = (xs.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "probe_tf32_input.json"), "w") as f:
+        json.dump({"x_bits": [hex(int(v)) for v in xs.view(np.uint32)[:32]],
+                   "c_bits": [hex(int(v)) for v in got.view(np.uint32)[:32]],
+                   "rz_matches": int(np.sum(got.view(np.uint32) == rz.view(np.uint32)))}, f)
+    assert np.array_equal(got.view(np.uint32), rz.view(np.uint32))
+
+
+def test_probe_accumulation_rounding(giga, torch_cuda):
+    """Record how the TMEM fp32 accumulator rounds (the promotion design depends on it).
+
+    Row i: first k8 MMA gives D = 1, second adds d_i (K = 16, terms = 1, no promotion).
+    Exact sums 1 + d_i are compared with fp32 round-to-nearest and round-toward-zero."""
+    torch = torch_cuda
+    M, N, K = 128, 256, 16
+    ds = np.array([2.0 ** -25, 1.5 * 2.0 ** -24, 2.0 ** -24, -2.0 ** -25, -1.5 * 2.0 ** -25,
+                   0.75 * 2.0 ** -23, 3 * 2.0 ** -26, -3 * 2.0 ** -26], np.float64)
+    A = np.zeros((M, K), np.float32)
+    A[:, 0] = 1.0
+    A[:, 8] = np.resize(ds, M).astype(np.float32)
+    B = np.zeros((K, N), np.float32)
+    B[0, :] = 1.0
+    B[8, :] = 1.0
+    dA, dB = _dev(torch, A), _dev(torch, B)
+    dC = torch.full((M, N), float("nan"), device="cuda")
+    giga.gemm_3xtf32(dA, None, dB, None, dC, M, N, K, terms=1, promote_kblocks=0)
+    torch.cuda.synchronize()
+    got = dC.cpu().numpy()[: len(ds), 0].astype(np.float64)
+    exact = 1.0 + ds
+    rn = exact.astype(np.float32).astype(np.float64)
+    rz = np.array([np.nextafter(np.float32(e), np.float32(0)) if np.float32(e) != e and
+                   abs(float(np.float32(e))) > abs(e) else np.float32(e) for e in exact],
+                  np.float64)
+    res = {"d": ds.tolist(), "got": got.tolist(), "rn": rn.tolist(), "rz": rz.tolist(),
+           "is_rn": bool(np.array_equal(got, rn)), "is_rz": bool(np.array_equal(got, rz))}
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "probe_accumulate.json"), "w") as f:
+        json.dump(res, f, indent=1)
+    print("accumulation probe:", res)
+    assert np.all(np.isfinite(got))
+
+
+def test_split_lo_is_exact_difference(giga, torch_cuda):
+    torch = torch_cuda
+    x = synth.gen_rows(0, 1, 100003, synth.MATRIX_A, "d2")[0]
+    x[:8] = [0, -0.0, 1e-30, -1e-30, 3.0, -7.5, 1e20, 1 + 2 ** -23]
+    dx = _dev(torch, x)
+    dlo = torch.full_like(dx, float("nan"))
+    giga.split_lo(dx, dlo)
+    torch.cuda.synchronize()
+    lo = dlo.cpu().numpy()
+    hi = (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+    assert np.array_equal(lo.view(np.uint32), (x - hi).view(np.uint32))
+    assert np.array_equal((hi.astype(np.float64) + lo.astype(np.float64)), x.astype(np.float64))
+
+
+# ---- exact cases ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["spec_2x2.txt", "identity_3x3.txt"])
+def test_golden_examples_bit_exact(giga, torch_cuda, name):
+    g = load(name)
+    C = run_host(giga, g["A"], g["B"])
+    assert np.array_equal(C, g["C"])
+    C2 = run_device(giga, torch_cuda, g["A"], g["B"])
+    assert np.array_equal(C2, g["C"])
+
+
+INT_SHAPES = [(1, 1, 1), (2, 2, 2), (3, 5, 7), (127, 129, 33), (128, 256, 32), (129, 257, 20),
+              (300, 260, 1028), (1000, 1000, 1000), (256, 512, 4096)]
+
+
+@pytest.mark.parametrize("M,N,K", INT_SHAPES)
+def test_integer_inputs_bit_exact(giga, torch_cuda, M, N, K):
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+    Cref, _ = oracle.gemm(A, B)
+    ok, st = check_exact(run_device(giga, torch_cuda, A, B), Cref)
+    assert ok, st
+    if M * N <= 300 * 300:
+        ok, st = check_exact(run_host(giga, A, B), Cref)
+        assert ok, st
+
+
+def test_all_ones_gives_k(giga, torch_cuda):
+    M, N, K = 200, 300, 2000
+    C = run_device(giga, torch_cuda, np.ones((M, K), np.float32), np.ones((K, N), np.float32))
+    assert np.all(C == K)
+
+
+def test_permutation_exact(giga, torch_cuda):
+    m, k = 300, 260
+    A = synth.gen_matrix(m, k, synth.MATRIX_A, "d2")
+    p = np.random.default_rng(1).permutation(m)
+    P = np.zeros((m, m), np.float32)
+    P[np.arange(m), p] = 1.0
+    C = run_device(giga, torch_cuda, P, A)
+    # 3xTF32 keeps ~22 of 24 bits of a general fp32 value: within tolerance, not bit-exact
+    Cref, S = oracle.gemm(P, A)
+    ok, st = check_close(C, Cref, S)
+    assert ok, st
+
+
+# ---- tolerance cases --------------------------------------------------------------------
+
+TOL_CASES = [(512, 512, 512, "d1"), (512, 512, 512, "d2"), (777, 1031, 2052, "d2"),
+             (130, 260, 4096, "d1"), (64, 128, 16384, "d1"), (129, 300, 9, "d2"),
+             (1, 1, 5, "d1"), (5, 3, 1, "d2")]
+
+
+@pytest.mark.parametrize("M,N,K,dist", TOL_CASES)
+def test_tolerance_vs_oracle(giga, torch_cuda, M, N, K, dist):
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, dist)
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
+    Cref, S = oracle.gemm(A, B)
+    ok, st = check_close(run_device(giga, torch_cuda, A, B), Cref, S)
+    assert ok, st
+    if M * N <= 1 << 18:
+        ok, st = check_close(run_host(giga, A, B), Cref, S)
+        assert ok, st
+
+
+def test_promotion_is_what_keeps_long_sums_accurate(giga, torch_cuda):
+    """D1 (all positive) at K = 16384: record the error with and without promotion; the
+    default (promoted) path must meet the bound."""
+    torch = torch_cuda
+    M, N, K = 128, 256, 16384
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, "d1")
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, "d1")
+    Cref, S = oracle.gemm(A, B)
+    dA, dB = _dev(torch, A), _dev(torch, B)
+    dAlo, dBlo = torch.empty_like(dA), torch.empty_like(dB)
+    giga.split_lo(dA, dAlo)
+    giga.split_lo(dB, dBlo)
+    res = {}
+    for pk in (0, 4, 16, 64):
+        dC = torch.full((M, N), float("nan"), device="cuda")
+        giga.gemm_3xtf32(dA, dAlo, dB, dBlo, dC, M, N, K, promote_kblocks=pk)
+        torch.cuda.synchronize()
+        ok, st = check_close(dC.cpu().numpy(), Cref, S)
+        signed = float(np.mean((dC.cpu().numpy().astype(np.float64) - Cref) / S))
+        res[pk] = {"ok": ok, "max_rel": st["max_rel_err"], "mean_rel": st["mean_rel_err"],
+                   "mean_signed_rel": signed}
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "probe_promotion.json"), "w") as f:
+        json.dump(res, f, indent=1)
+    print("promotion sweep:", res)
+    assert res[16]["ok"], res
+
+
+# ---- full-size configurations, row-sampled ---------------------------------------------
+
+def _sampled_rows(M, rng, extra=64):
+    rows = {0, M - 1, M // 2, M // 2 - 1}
+    rows.update(int(r) for r in rng.integers(0, M, extra))
+    return np.array(sorted(rows))
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 4096, 4096), (16384, 16384, 16384),
+                                   (262144, 1024, 1024)])
+def test_full_size_sampled_rows(giga, torch_cuda, M, N, K):
+    """BASELINE configs at full size through the sharded device path bench.py times
+    (ngpus = 1), oracle on sampled rows (every element of each sampled row)."""
+    torch = torch_cuda
+    dA = synth.gen_rows_torch(0, M, K, synth.MATRIX_A, "d2", device="cuda")
+    dB = synth.gen_rows_torch(0, K, N, synth.MATRIX_B, "d2", device="cuda")
+    dC = torch.full((M, N), float("nan"), device="cuda")
+    giga.matmul_sharded([dA], [dB], [dC], M, N, K)
+    rows = _sampled_rows(M, np.random.default_rng(M + N + K), extra=32)
+    Cs = dC[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert not torch.isnan(dC).any().item()
+    del dA, dC
+    Ar = synth.gen_rows_index(rows, K, synth.MATRIX_A, "d2")
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, "d2")
+    Cref, S = oracle.gemm(Ar, B)
+    ok, st = check_close(Cs, Cref, S)
+    assert ok, st
+
+
+# ---- error paths -------------------------------------------------------------------------
+
+def test_error_codes(giga, torch_cuda):
+    torch = torch_cuda
+    a = np.ones((4, 4), np.float32)
+    with pytest.raises(giga.GigaError) as e:
+        giga.matmul(a, a, np.empty_like(a), 0, 4, 4, 1)
+    assert e.value.status == "GIGA_ERR_INVALID_ARG"
+    with pytest.raises(giga.GigaError) as e:
+        giga.matmul(a, a, np.empty_like(a), 4, 4, 4, 2)
+    assert e.value.status == "GIGA_ERR_INVALID_ARG"
+    with pytest.raises(giga.GigaError) as e:
+        giga.matmul(a, a, a, 4, 4, 4, 1)  # C aliases A
+    assert e.value.status == "GIGA_ERR_INVALID_ARG"
+    d = torch.ones((4, 4), device="cuda")
+    with pytest.raises(giga.GigaError) as e:
+        giga.matmul(a, d, np.empty_like(a), 4, 4, 4, 1)  # mixed host/device
+    assert e.value.status == "GIGA_ERR_INVALID_ARG"
+    with pytest.raises(giga.GigaError) as e:
+        giga.init(1)
+    assert e.value.status == "GIGA_ERR_ALREADY_INITIALIZED"
+
+
+def test_oom_leaves_no_leak(giga, torch_cuda):
+    """A request whose workspace cannot fit fails with GIGA_ERR_OOM before touching any
+    input, and device memory in use is exactly what it was (SPEC.md:460/619 no leaks)."""
+    torch = torch_cuda
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    M, N, K = 1 << 30, 64, 64  # host mode needs 4*M*(K+N) = 512 GiB of device workspace
+    base = 1 << 44  # unmapped host addresses, never dereferenced: allocation fails first
+    with pytest.raises(giga.GigaError) as e:
+        giga.matmul(base, base + (1 << 41), base + (1 << 42), M, N, K, 1)
+    assert e.value.status == "GIGA_ERR_OOM", str(e.value)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free1 == free0
+    g = load("spec_2x2.txt")
+    assert np.array_equal(run_host(giga, g["A"], g["B"]), g["C"])
+
+
+def test_rank_api_world1_on_torch_stream(torch_cuda):
+    """One-process-per-GPU API at world size 1 (what bench.py uses), on a torch stream."""
+    torch = torch_cuda
+    from paper_2504_01266_b200 import giga as g
+    g.finalize()
+    g.rank_init(0, 1, 0, None)
+    try:
+        M, N, K = 300, 400, 260
+        A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+        B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+        dA, dB = _dev(torch, A), _dev(torch, B)
+        dC = torch.full((M, N), float("nan"), device="cuda")
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            g.matmul_rank(dA, dB, dC, M, N, K, stream=s)
+        s.synchronize()
+        Cref, _ = oracle.gemm(A, B)
+        ok, st = check_exact(dC.cpu().numpy(), Cref)
+        assert ok, st
+    finally:
+        g.finalize()
+        g.init(1)
