@@ -13,12 +13,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgiga.so")
+DEBUG_LIB = os.path.join(HERE, "libgiga_debug.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["gemm_3xtf32.cu"]
 CPP_SOURCES = ["api.cpp", "nccl_loader.cpp"]
-HEADERS = ["ptx.cuh", "kernels.h", "nccl_loader.h"]
+HEADERS = ["ptx.cuh", "kernels.h", "nccl_loader.h", "debug_kernels.cu"]
 
 
 def nccl_paths():
@@ -67,6 +68,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
                            "-ldl", "-lpthread"])
     os.replace(tmp, LIB)
+    # bring-up probes (not the product path): debug kernels + the TMA encoder helper
+    dsrc = os.path.join(CSRC, "debug_kernels.cu")
+    do = os.path.join(objdir, "debug_kernels.cu.o")
+    subprocess.check_call([NVCC, *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", *common, "-c",
+                           dsrc, "-o", do])
+    tmp = DEBUG_LIB + f".tmp{os.getpid()}"
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, do,
+                           os.path.join(objdir, "gemm_3xtf32.cu.o"), "-ldl", "-lpthread"])
+    os.replace(tmp, DEBUG_LIB)
     return LIB
 
 

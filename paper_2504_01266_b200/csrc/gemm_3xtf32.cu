@@ -17,7 +17,7 @@
 //     register sum with round-to-nearest adds.
 //   * Warp specialisation, persistent CTAs (one per SM, 1 CTA/SM by smem):
 //       warp 0 lane 0  TMA producer: A, A_lo tiles (K-major, 64B swizzle) and B, B_lo tiles
-//                      (N-major, 128B swizzle) into a 4-stage smem ring (mbarrier full/empty)
+//                      (N-major, 128B/32B-atom swizzle) into a 4-stage smem ring (mbarriers)
 //       warp 1 lane 0  MMA issuer: 3 UMMAs per k8, tcgen05.commit frees smem stages and
 //                      publishes finished accumulators
 //       warps 2..9     epilogue: tcgen05.ld TMEM -> registers, RN fp32 promotion adds,
@@ -65,12 +65,14 @@ struct GemmParams {
 // Shared-memory matrix descriptor (sm100, "version 1"):
 //   [0,14) start address >> 4   [16,30) leading byte offset >> 4   [32,46) stride byte
 //   offset >> 4   [46,48) version = 1   [49,52) base offset = 0   [52] lbo mode = 0
-//   [61,64) layout: 2 = SWIZZLE_128B, 4 = SWIZZLE_64B
+//   [61,64) layout: 1 = SWIZZLE_128B_BASE32B, 2 = SWIZZLE_128B, 4 = SWIZZLE_64B
 // A (K-major, SW64): rows of 64 B (16 fp32 of K), 8-row atoms of 512 B -> SBO = 512; LBO is
 //   unused for swizzled K-major (1). The k8 step j starts 32 B further into the row.
-// B (N-major, SW128): rows of 128 B = 32 n, one row per k; 8-row atoms (1 KiB) -> SBO = 1024
-//   between k-groups; 32-column chunks 2 KiB apart -> LBO = 2048. The k8 step j starts
-//   j * 1024 B further.
+// B (N-major): for 32-bit MN-major operands the only UMMA layout is SWIZZLE_128B_BASE32B
+//   (32-byte granules XOR-swizzled inside 128-byte rows with a 4-row period; TMA mode
+//   128B_ATOM_32B). Rows of 128 B = 32 n, one row per k; 4-row k-groups 512 B apart -> SBO;
+//   32-column chunks 2 KiB apart -> LBO = 2048. The k8 step j starts j * 1024 B further.
+//   (Measured on B200 with scripts/debug_umma.py: plain SWIZZLE_128B N-major tf32 yields 0.)
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
                                                uint32_t layout) {
   uint64_t d = 0;
@@ -203,10 +205,10 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
 #pragma unroll
             for (int k8 = 0; k8 < BK / 8; ++k8) {
               const uint64_t dA = make_sdesc(sA + 32 * k8, 16, 512, 4);
-              const uint64_t dB = make_sdesc(sB + 1024 * k8, B_CHUNK_BYTES, 1024, 2);
+              const uint64_t dB = make_sdesc(sB + 1024 * k8, B_CHUNK_BYTES, 512, 1);
               if (p.terms == 3) {
                 const uint64_t dAlo = make_sdesc(sAlo + 32 * k8, 16, 512, 4);
-                const uint64_t dBlo = make_sdesc(sBlo + 1024 * k8, B_CHUNK_BYTES, 1024, 2);
+                const uint64_t dBlo = make_sdesc(sBlo + 1024 * k8, B_CHUNK_BYTES, 512, 1);
                 ptx::mma_tf32(d_tmem, dAlo, dB, idesc, acc);
                 ptx::mma_tf32(d_tmem, dA, dBlo, idesc, 1u);
                 acc = 1;
@@ -381,11 +383,11 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
 
   CUtensorMap tA, tAlo, tB, tBlo;
   if (!make_map(&tA, A, K, M, K, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
-      !make_map(&tB, B, N, K, N, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B))
+      !make_map(&tB, B, N, K, N, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return cudaErrorInvalidValue;
   if (terms == 3) {
     if (!make_map(&tAlo, A_lo, K, M, K, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
-        !make_map(&tBlo, B_lo, N, K, N, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B))
+        !make_map(&tBlo, B_lo, N, K, N, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
       return cudaErrorInvalidValue;
   } else {
     tAlo = tA;
