@@ -210,6 +210,7 @@ def main():
         B = torch.empty((K, N), dtype=torch.float32, device=dev)
     C = torch.empty((M, N), dtype=torch.float32, device=dev)
     stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))  # inputs are produced on torch's stream
 
     def step():
         giga.matmul_rank(A, B, C, M, N, K, stream=stream)
@@ -348,6 +349,7 @@ def measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev, pg):
     B = torch.empty((K, N), dtype=torch.float32, device=dev)
     C = torch.empty((M, N), dtype=torch.float32, device=dev)
     s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
 
     def one():
         with torch.cuda.stream(s):

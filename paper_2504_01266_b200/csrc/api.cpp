@@ -357,6 +357,17 @@ int pointer_kind(const void *p, int *dev) {
   return 0;
 }
 
+// The single-process calls are blocking ("synchronize and copy back"): they
+// start after everything already queued on the participating devices (e.g. the producer of
+// A or B on another stream) and return after their own work is done.
+int quiesce(int ngpus) {
+  for (int i = 0; i < ngpus; ++i) {
+    CK(cudaSetDevice(g.devs[i].dev));
+    CK(cudaDeviceSynchronize());
+  }
+  return GIGA_OK;
+}
+
 int sync_all(int ngpus) {
   for (int i = 0; i < ngpus; ++i) {
     DevCtx &d = g.devs[i];
@@ -606,6 +617,7 @@ int giga_matmul(const float *A, const float *B, float *C, int64_t M, int64_t N, 
   if (overlaps(C, size_t(M * N) * 4, A, size_t(M * K) * 4) ||
       overlaps(C, size_t(M * N) * 4, B, size_t(K * N) * 4))
     return fail(GIGA_ERR_INVALID_ARG, "C overlaps A or B");
+  TRY(quiesce(ngpus));
   return matmul_locked(A, B, C, M, N, K, ngpus);
 }
 
@@ -632,6 +644,7 @@ int giga_matmul_sharded(const float *const *A_shard, float *const *B_buf, float 
         (rows > 0 && overlaps(C_full[i], size_t(M * N) * 4, A_shard[i], size_t(rows * K) * 4)))
       return fail(GIGA_ERR_INVALID_ARG, "C_full[%d] overlaps A or B", i);
   }
+  TRY(quiesce(ngpus));
   return sharded_locked(A_shard, B_buf, C_full, M, N, K, ngpus);
 }
 

@@ -29,6 +29,8 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "kernels.h"
@@ -323,6 +325,20 @@ __global__ void __launch_bounds__(256) split_lo_kernel(const float *__restrict__
 }
 
 // ---- host side ----------------------------------------------------------------------------
+// Promotion interval: kDefaultPromoteKBlocks, overridable once per process with the
+// GIGA_PROMOTE_KBLOCKS environment variable (0 = never promote; tests / sweeps only).
+int default_promote_kblocks() {
+  static int v = [] {
+    const char *e = getenv("GIGA_PROMOTE_KBLOCKS");
+    if (e && *e) {
+      const int x = atoi(e);
+      if (x >= 0) return x;
+    }
+    return kDefaultPromoteKBlocks;
+  }();
+  return v;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static std::once_flag g_encode_once;
 
@@ -401,7 +417,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.ldc = int(ldc);
   p.terms = terms;
   p.n_kb = int((K + BK - 1) / BK);
-  int pk = promote_kblocks < 0 ? kDefaultPromoteKBlocks : promote_kblocks;
+  int pk = promote_kblocks < 0 ? default_promote_kblocks() : promote_kblocks;
   p.p_kb = (pk == 0 || pk > p.n_kb) ? p.n_kb : pk;
   p.m_tiles = int((M + BM - 1) / BM);
   p.n_tiles = int((N + BN - 1) / BN);

@@ -9,6 +9,9 @@ namespace giga {
 // register sum. 16 k-blocks = K 256 = 32 k8 steps.
 constexpr int kDefaultPromoteKBlocks = 16;
 
+// The promotion interval in effect (kDefaultPromoteKBlocks or $GIGA_PROMOTE_KBLOCKS).
+int default_promote_kblocks();
+
 // lo = x - tf32(x) over n elements (HBM-bound elementwise split).
 cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t st);
 

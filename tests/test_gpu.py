@@ -317,6 +317,7 @@ def test_rank_api_world1_on_torch_stream(torch_cuda):
         dA, dB = _dev(torch, A), _dev(torch, B)
         dC = torch.full((M, N), float("nan"), device="cuda")
         s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())  # stream-ordered API: inputs first
         with torch.cuda.stream(s):
             g.matmul_rank(dA, dB, dC, M, N, K, stream=s)
         s.synchronize()
