@@ -141,14 +141,16 @@ int giga_split_lo(const float *x, float *lo, int64_t n, void *stream);
 int giga_gemm_3xtf32(const float *A, const float *A_lo, const float *B, const float *B_lo,
                      float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, void *stream);
 
-/* As giga_gemm_3xtf32 with the numerics knobs exposed (tests and probes):
+/* As giga_gemm_3xtf32 with the numerics and tiling knobs exposed (tests and probes):
  * terms = 3 (3xTF32) or 1 (plain TF32: a_hi*b_hi only; A_lo/B_lo may be NULL);
  * promote_kblocks = number of 16-wide k-blocks accumulated in TMEM before the partial sum
  * is added into the fp32 register sum; 0 = never promote (one TMEM accumulation over K);
- * -1 = the library default. */
+ * -1 = the library default;
+ * cta_group = 1 (one CTA per 128 x 256 tile), 2 (a CTA pair per 256 x 256 tile, UMMA
+ * cta_group::2), 0 = chosen from the shape. */
 int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const float *B_lo,
                         float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, int terms,
-                        int promote_kblocks, void *stream);
+                        int promote_kblocks, int cta_group, void *stream);
 
 /* ------------------------------------------------------------------------------------ */
 /* Kernel timing (bench.py's roofline): when enabled, CUDA events bracket every GEMM and

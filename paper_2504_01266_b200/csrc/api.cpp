@@ -747,7 +747,9 @@ int giga_split_lo(const float *x, float *lo, int64_t n, void *stream) {
 
 int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const float *B_lo,
                         float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, int terms,
-                        int promote_kblocks, void *stream) {
+                        int promote_kblocks, int cta_group, void *stream) {
+  if (cta_group < 0 || cta_group > 2)
+    return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_3xtf32_ex: cta_group must be 0, 1 or 2");
   if (!A || !B || !C || (terms == 3 && (!A_lo || !B_lo)) || (terms != 1 && terms != 3))
     return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_3xtf32: bad pointers/terms");
   TRY(check_dims(M, N, K));
@@ -758,14 +760,15 @@ int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const
   if (ensure_tma_encoder() != 0) return fail(GIGA_ERR_CUDA, "TMA encoder unavailable");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CK(timed(0, st, [&] {
-    return launch_gemm_3xtf32(A, A_lo, B, B_lo, C, M, N, K, ldc, terms, promote_kblocks, st);
+    return launch_gemm_3xtf32(A, A_lo, B, B_lo, C, M, N, K, ldc, terms, promote_kblocks, st,
+                              cta_group);
   }));
   return GIGA_OK;
 }
 
 int giga_gemm_3xtf32(const float *A, const float *A_lo, const float *B, const float *B_lo,
                      float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, void *stream) {
-  return giga_gemm_3xtf32_ex(A, A_lo, B, B_lo, C, M, N, K, ldc, 3, -1, stream);
+  return giga_gemm_3xtf32_ex(A, A_lo, B, B_lo, C, M, N, K, ldc, 3, -1, 0, stream);
 }
 
 // ---- timing ------------------------------------------------------------------------------

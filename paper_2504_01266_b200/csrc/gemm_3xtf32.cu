@@ -6,29 +6,31 @@
 // element on sm_75 (16x16 blocks PAPER.md:194); this is a B200 design:
 //
 //   * fp32 accuracy from TF32 tensor cores (BASELINE.json north_star (3)): x = hi + lo with
-//     hi = the tensor core's own TF32 reading of the raw fp32 bits and lo = x - hi (exact),
-//     produced by split_lo_kernel. Per 8-wide k step three tcgen05.mma.kind::tf32 are issued
-//     into one TMEM accumulator, small terms first: a_lo*b_hi, a_hi*b_lo, a_hi*b_hi
-//     (a_lo*b_lo, ~2^-20 relative, is dropped). hi is never materialised: the MMA is fed
-//     the raw fp32 tile and reads only its TF32 part.
-//   * Accumulator promotion: the tensor core's fp32 accumulation is not round-to-nearest
-//     (measured), so every `p_kb` k-blocks the MMA warp switches to the other of
-//     two TMEM accumulators and the epilogue warps add the finished partial into an fp32
-//     register sum with round-to-nearest adds.
-//   * Warp specialisation, persistent CTAs (one per SM, 1 CTA/SM by smem):
+//     hi = the tensor core's own TF32 reading of the raw fp32 bits (truncation, measured)
+//     and lo = x - hi (exact), produced by split_lo_kernel. Per 8-wide k step three
+//     tcgen05.mma.kind::tf32 are issued into one TMEM accumulator, small terms first:
+//     a_lo*b_hi, a_hi*b_lo, a_hi*b_hi (a_lo*b_lo, ~2^-20 relative, is dropped). hi is never
+//     materialised: the MMA is fed the raw fp32 tile and reads only its TF32 part.
+//   * Accumulator promotion: the tensor core's fp32 accumulation truncates (measured,
+//     tests/test_gpu.py::test_probe_accumulation_rounding), so every `p_kb` k-blocks the
+//     MMA issuer switches to the other of two TMEM accumulators and the epilogue warps add
+//     the finished partial into an fp32 register sum with round-to-nearest adds.
+//   * CTA pairs (CG = 2, cta_group::2): a cluster of two CTAs on one TPC computes a
+//     256 x 256 tile; each CTA stages its own 128 rows of A and half (128 columns) of B, the
+//     leader issues M=256 UMMAs that read both CTAs' shared memory and write both CTAs'
+//     TMEM. Per SM this halves the B operand traffic (smem and L2) of the 1-CTA tile.
+//     CG = 1 (128 x 256 per CTA) serves small problems.
+//   * Warp specialisation, persistent clusters (one CTA per SM, 1 CTA/SM by smem):
 //       warp 0 lane 0  TMA producer: A, A_lo tiles (K-major, 64B swizzle) and B, B_lo tiles
-//                      (N-major, 128B/32B-atom swizzle) into a 4-stage smem ring (mbarriers)
-//       warp 1 lane 0  MMA issuer: 3 UMMAs per k8, tcgen05.commit frees smem stages and
-//                      publishes finished accumulators
+//                      (N-major, 128B/32B-atom swizzle) into a smem ring (mbarriers)
+//       warp 1 lane 0  MMA issuer (leader CTA): 3 UMMAs per k8; tcgen05.commit frees smem
+//                      stages in both CTAs and publishes finished accumulators
 //       warps 2..9     epilogue: tcgen05.ld TMEM -> registers, RN fp32 promotion adds,
 //                      16-byte vector stores into the shard's rows of C.
-//
-// Tile: 128 (M) x 256 (N) per CTA, k-block 16 (two k8 UMMA steps), TMEM 2 x 256 columns.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
-
 #include <stdlib.h>
 
 #include <mutex>
@@ -39,21 +41,28 @@
 namespace giga {
 
 namespace cfg {
-constexpr int BM = 128;
-constexpr int BN = 256;
-constexpr int BK = 16;
-constexpr int STAGES = 4;
+constexpr int BM = 128;  // rows of A per CTA (UMMA M per CTA)
+constexpr int BN = 256;  // UMMA N: columns of the tile (a CTA pair stages 128 each)
+constexpr int BK = 16;   // k-block: two k8 UMMA steps
 constexpr int NUM_EPI_WARPS = 8;
 constexpr int NUM_THREADS = 64 + NUM_EPI_WARPS * 32;
-constexpr uint32_t A_BYTES = BM * BK * 4;          // 8 KiB: 128 rows x 64 B
-constexpr uint32_t B_BYTES = BK * BN * 4;          // 16 KiB: 8 chunks x (16 rows x 128 B)
-constexpr uint32_t B_CHUNK_BYTES = BK * 32 * 4;    // 2 KiB: one 32-column chunk of B
-constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 48 KiB
-constexpr uint32_t ACC_COLS = BN;                  // fp32 accumulator: 1 TMEM column per n
-constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;       // two accumulators (promotion ping-pong)
-constexpr int GROUP_M = 16;                        // L2 raster: 16 M-tiles per group
-constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t A_BYTES = BM * BK * 4;        // 8 KiB: 128 rows x 64 B
+constexpr uint32_t B_CHUNK_BYTES = BK * 32 * 4;  // 2 KiB: one 32-column chunk of B
+constexpr uint32_t ACC_COLS = BN;                // fp32 accumulator: 1 TMEM column per n
+constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;     // two accumulators (promotion ping-pong)
+constexpr int GROUP_M = 16;                      // L2 raster: 16 M-tiles per group
+constexpr size_t SMEM_RING = 192 * 1024;         // operand ring per CTA
 }  // namespace cfg
+
+template <int CG>
+struct Tile {
+  static constexpr int TILE_M = cfg::BM * CG;                    // rows per cluster tile
+  static constexpr int B_COLS = cfg::BN / CG;                    // B columns this CTA stages
+  static constexpr uint32_t B_BYTES = cfg::BK * B_COLS * 4;      // per operand per CTA
+  static constexpr uint32_t STAGE_BYTES = 2 * cfg::A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = int(cfg::SMEM_RING / STAGE_BYTES);  // 4 (CG=1), 6 (CG=2)
+  static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
+};
 
 struct GemmParams {
   int M, N, K, ldc;
@@ -103,6 +112,7 @@ __device__ __forceinline__ void tile_coords(int t, const GemmParams &p, int &mb,
   nb = local / gm;
 }
 
+template <int CG>
 __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmAlo,
@@ -110,10 +120,12 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
                        const __grid_constant__ CUtensorMap tmBlo, float *__restrict__ C,
                        const GemmParams p) {
   using namespace cfg;
+  using T = Tile<CG>;
+  constexpr int STAGES = T::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * T::STAGE_BYTES);
   uint64_t *empty = full + STAGES;
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
@@ -121,6 +133,10 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;  // rank in the CTA pair
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / CG;
+  const int num_clusters = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -135,44 +151,70 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], NUM_EPI_WARPS);
+      ptx::mbar_init(&tempty[b], NUM_EPI_WARPS * CG);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) {
+    if (CG == 2)
+      ptx::tmem_alloc_cg2(tmem_slot, TMEM_COLS);
+    else
+      ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    ptx::cluster_sync();  // peer barriers initialised before any remote arrive / TMA
+  else
+    __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int n_int = (p.n_kb + p.p_kb - 1) / p.p_kb;
 
   if (warp == 0) {
-    // ======================= TMA producer =======================
+    // ======================= TMA producer (both CTAs) =======================
     if (lane == 0) {
-      const uint32_t tx = p.terms == 3 ? STAGE_BYTES : (A_BYTES + B_BYTES);
+      const uint32_t tx_cta = p.terms == 3 ? T::STAGE_BYTES : (A_BYTES + T::B_BYTES);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
         int mb, nb;
         tile_coords(t, p, mb, nb);
-        const int m0 = mb * BM, n0 = nb * BN;
+        const int m0 = mb * T::TILE_M + int(rank) * BM;
+        const int n0 = nb * BN + int(rank) * T::B_COLS;
         for (int kb = 0; kb < p.n_kb; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t *sA = smem + stage * STAGE_BYTES;
+          uint8_t *sA = smem + stage * T::STAGE_BYTES;
           uint8_t *sAlo = sA + A_BYTES;
           uint8_t *sB = sA + 2 * A_BYTES;
-          uint8_t *sBlo = sB + B_BYTES;
+          uint8_t *sBlo = sB + T::B_BYTES;
           const int k0 = kb * BK;
-          ptx::mbar_expect_tx(&full[stage], tx);
-          ptx::tma_load_2d(sA, &tmA, &full[stage], k0, m0);
+          if (CG == 1) {
+            ptx::mbar_expect_tx(&full[stage], tx_cta);
+            ptx::tma_load_2d(sA, &tmA, &full[stage], k0, m0);
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c)
-            ptx::tma_load_2d(sB + c * B_CHUNK_BYTES, &tmB, &full[stage], n0 + 32 * c, k0);
-          if (p.terms == 3) {
-            ptx::tma_load_2d(sAlo, &tmAlo, &full[stage], k0, m0);
+            for (int c = 0; c < T::B_COLS / 32; ++c)
+              ptx::tma_load_2d(sB + c * B_CHUNK_BYTES, &tmB, &full[stage], n0 + 32 * c, k0);
+            if (p.terms == 3) {
+              ptx::tma_load_2d(sAlo, &tmAlo, &full[stage], k0, m0);
 #pragma unroll
-            for (int c = 0; c < BN / 32; ++c)
-              ptx::tma_load_2d(sBlo + c * B_CHUNK_BYTES, &tmBlo, &full[stage], n0 + 32 * c, k0);
+              for (int c = 0; c < T::B_COLS / 32; ++c)
+                ptx::tma_load_2d(sBlo + c * B_CHUNK_BYTES, &tmBlo, &full[stage], n0 + 32 * c,
+                                 k0);
+            }
+          } else {
+            // both CTAs' bytes are counted on the leader's full barrier
+            if (leader) ptx::mbar_expect_tx(&full[stage], 2 * tx_cta);
+            const uint32_t bar = ptx::smem_u32(&full[stage]) & ptx::kPeerBitMask;
+            ptx::tma_load_2d_cg2(sA, &tmA, bar, k0, m0);
+#pragma unroll
+            for (int c = 0; c < T::B_COLS / 32; ++c)
+              ptx::tma_load_2d_cg2(sB + c * B_CHUNK_BYTES, &tmB, bar, n0 + 32 * c, k0);
+            if (p.terms == 3) {
+              ptx::tma_load_2d_cg2(sAlo, &tmAlo, bar, k0, m0);
+#pragma unroll
+              for (int c = 0; c < T::B_COLS / 32; ++c)
+                ptx::tma_load_2d_cg2(sBlo + c * B_CHUNK_BYTES, &tmBlo, bar, n0 + 32 * c, k0);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -182,13 +224,13 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ======================= MMA issuer =======================
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(BM, BN);
+    // ======================= MMA issuer (leader CTA) =======================
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = make_idesc(BM * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
         int kb = 0;
         for (int it = 0; it < n_int; ++it, ++acc_iter) {
           const uint32_t buf = acc_iter & 1, use = acc_iter >> 1;
@@ -200,42 +242,59 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
           for (; kb < kb_end; ++kb) {
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
-            const uint32_t sA = ptx::smem_u32(smem + stage * STAGE_BYTES);
+            const uint32_t sA = ptx::smem_u32(smem + stage * T::STAGE_BYTES);
             const uint32_t sAlo = sA + A_BYTES;
             const uint32_t sB = sA + 2 * A_BYTES;
-            const uint32_t sBlo = sB + B_BYTES;
+            const uint32_t sBlo = sB + T::B_BYTES;
 #pragma unroll
             for (int k8 = 0; k8 < BK / 8; ++k8) {
               const uint64_t dA = make_sdesc(sA + 32 * k8, 16, 512, 4);
               const uint64_t dB = make_sdesc(sB + 1024 * k8, B_CHUNK_BYTES, 512, 1);
-              if (p.terms == 3) {
-                const uint64_t dAlo = make_sdesc(sAlo + 32 * k8, 16, 512, 4);
-                const uint64_t dBlo = make_sdesc(sBlo + 1024 * k8, B_CHUNK_BYTES, 512, 1);
-                ptx::mma_tf32(d_tmem, dAlo, dB, idesc, acc);
-                ptx::mma_tf32(d_tmem, dA, dBlo, idesc, 1u);
-                acc = 1;
+              const uint64_t dAlo = make_sdesc(sAlo + 32 * k8, 16, 512, 4);
+              const uint64_t dBlo = make_sdesc(sBlo + 1024 * k8, B_CHUNK_BYTES, 512, 1);
+              if (CG == 1) {
+                if (p.terms == 3) {
+                  ptx::mma_tf32(d_tmem, dAlo, dB, idesc, acc);
+                  ptx::mma_tf32(d_tmem, dA, dBlo, idesc, 1u);
+                  acc = 1;
+                }
+                ptx::mma_tf32(d_tmem, dA, dB, idesc, acc);
+              } else {
+                if (p.terms == 3) {
+                  ptx::mma_tf32_cg2(d_tmem, dAlo, dB, idesc, acc);
+                  ptx::mma_tf32_cg2(d_tmem, dA, dBlo, idesc, 1u);
+                  acc = 1;
+                }
+                ptx::mma_tf32_cg2(d_tmem, dA, dB, idesc, acc);
               }
-              ptx::mma_tf32(d_tmem, dA, dB, idesc, acc);
               acc = 1;
             }
-            ptx::mma_commit(&empty[stage]);
+            if (CG == 1)
+              ptx::mma_commit(&empty[stage]);
+            else
+              ptx::mma_commit_cg2(&empty[stage], 0x3);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
-          ptx::mma_commit(&tfull[buf]);
+          if (CG == 1)
+            ptx::mma_commit(&tfull[buf]);
+          else
+            ptx::mma_commit_cg2(&tfull[buf], 0x3);
         }
       }
     }
   } else {
-    // ======================= epilogue (8 warps) =======================
+    // ======================= epilogue (8 warps per CTA) =======================
     const int e = warp - 2;
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int half = e >> 2;    // column half of the 256-wide tile
-    const int row_in_tile = quad * 32 + lane;
+    const int row_in_tile = int(rank) * BM + quad * 32 + lane;
+    const uint32_t tempty_leader0 = ptx::smem_u32(&tempty[0]) & ptx::kPeerBitMask;
+    const uint32_t tempty_leader1 = ptx::smem_u32(&tempty[1]) & ptx::kPeerBitMask;
     uint32_t acc_iter = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
       int mb, nb;
       tile_coords(t, p, mb, nb);
       float sum[128];  // fp32 running sum of the promoted partials (0 + p == p exactly)
@@ -256,10 +315,15 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+        if (lane == 0) {
+          if (CG == 1)
+            ptx::mbar_arrive(&tempty[buf]);
+          else
+            ptx::mbar_arrive_cluster(buf ? tempty_leader1 : tempty_leader0);
+        }
       }
       // store this thread's row segment: 128 consecutive fp32 = 32 x 16 B
-      const int row = mb * BM + row_in_tile;
+      const int row = mb * T::TILE_M + row_in_tile;
       if (row < p.M) {
         const int col0 = nb * BN + half * 128;
         float *crow = C + int64_t(row) * p.ldc + col0;
@@ -280,18 +344,24 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
   }
   __syncwarp();
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    ptx::cluster_sync();  // no CTA leaves while its peer may still signal its barriers
+  else
+    __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    if (CG == 2)
+      ptx::tmem_dealloc_cg2(tmem_base, TMEM_COLS);
+    else
+      ptx::tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
 // ---- split: lo = x - tf32(x) ------------------------------------------------------------
 // tf32(x) is what kind::tf32 reads from raw fp32 bits: the top 19 bits (sign, exponent,
 // 10 mantissa bits), i.e. truncation toward zero of the low 13 mantissa bits (measured on
-// B200 by tests/test_gpu_probe.py). x - tf32(x) is exact in fp32 (same sign, the 13 low
-// bits of x's significand).
+// B200 by tests/test_gpu.py::test_probe_tf32_operand_conversion_is_truncation). x - tf32(x)
+// is exact in fp32 (same sign, the 13 low bits of x's significand).
 __device__ __forceinline__ float tf32_lo(float x) {
   const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
   return __fsub_rn(x, hi);
@@ -337,6 +407,18 @@ int default_promote_kblocks() {
     return kDefaultPromoteKBlocks;
   }();
   return v;
+}
+
+// CTA-group size: 2 (CTA pairs) unless the problem has fewer 256-row tiles than SM pairs,
+// or $GIGA_CTA_GROUP forces 1 or 2.
+int choose_cta_group(int64_t M, int64_t N, int num_sms) {
+  static int forced = [] {
+    const char *e = getenv("GIGA_CTA_GROUP");
+    return (e && (*e == '1' || *e == '2')) ? (*e - '0') : 0;
+  }();
+  if (forced) return forced;
+  const int64_t tiles2 = ((M + 255) / 256) * ((N + 255) / 256);
+  return tiles2 >= num_sms / 2 ? 2 : 1;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -385,9 +467,26 @@ cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t s
   return cudaGetLastError();
 }
 
+// the smem opt-in is a per-device function attribute
+template <int CG>
+static cudaError_t ensure_smem_attr() {
+  static std::mutex mu;
+  static uint64_t done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done >> (dev & 63) & 1) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(gemm_3xtf32_kernel<CG>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(Tile<CG>::SMEM_BYTES));
+  if (e == cudaSuccess) done |= uint64_t(1) << (dev & 63);
+  return e;
+}
+
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
                                const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,
-                               int64_t ldc, int terms, int promote_kblocks, cudaStream_t st) {
+                               int64_t ldc, int terms, int promote_kblocks, cudaStream_t st,
+                               int cta_group) {
   using namespace cfg;
   if (M < 1 || N < 1 || K < 1 || (K & 3) || (N & 3) || (ldc & 3) || ldc < N)
     return cudaErrorInvalidValue;
@@ -397,6 +496,8 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   if (terms == 3 && (!A_lo || !B_lo)) return cudaErrorInvalidValue;
   if (ensure_tma_encoder() != 0) return cudaErrorNotSupported;
 
+  const int num_sms = num_sms_current();
+  const int cg = (cta_group == 1 || cta_group == 2) ? cta_group : choose_cta_group(M, N, num_sms);
   CUtensorMap tA, tAlo, tB, tBlo;
   if (!make_map(&tA, A, K, M, K, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
       !make_map(&tB, B, N, K, N, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
@@ -419,28 +520,36 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.n_kb = int((K + BK - 1) / BK);
   int pk = promote_kblocks < 0 ? default_promote_kblocks() : promote_kblocks;
   p.p_kb = (pk == 0 || pk > p.n_kb) ? p.n_kb : pk;
-  p.m_tiles = int((M + BM - 1) / BM);
+  const int tile_m = BM * cg;
+  p.m_tiles = int((M + tile_m - 1) / tile_m);
   p.n_tiles = int((N + BN - 1) / BN);
   p.num_tiles = p.m_tiles * p.n_tiles;
 
-  // the smem opt-in is a per-device function attribute
-  static std::mutex attr_mu;
-  static uint64_t attr_done = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  {
-    std::lock_guard<std::mutex> lk(attr_mu);
-    if (!(attr_done >> (dev & 63) & 1)) {
-      cudaError_t e = cudaFuncSetAttribute(
-          gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-      if (e != cudaSuccess) return e;
-      attr_done |= uint64_t(1) << (dev & 63);
-    }
+  if (cg == 1) {
+    cudaError_t e = ensure_smem_attr<1>();
+    if (e != cudaSuccess) return e;
+    const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
+    gemm_3xtf32_kernel<1><<<grid, NUM_THREADS, Tile<1>::SMEM_BYTES, st>>>(tA, tAlo, tB, tBlo,
+                                                                          C, p);
+    return cudaGetLastError();
   }
-
-  const int grid = p.num_tiles < num_sms_current() ? p.num_tiles : num_sms_current();
-  gemm_3xtf32_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(tA, tAlo, tB, tBlo, C, p);
-  return cudaGetLastError();
+  cudaError_t e = ensure_smem_attr<2>();
+  if (e != cudaSuccess) return e;
+  const int pairs = num_sms / 2;
+  const int clusters = p.num_tiles < pairs ? p.num_tiles : pairs;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(unsigned(2 * clusters));
+  lc.blockDim = dim3(NUM_THREADS);
+  lc.dynamicSmemBytes = Tile<2>::SMEM_BYTES;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, gemm_3xtf32_kernel<2>, tA, tAlo, tB, tBlo, C, p);
 }
 
 }  // namespace giga

@@ -6,8 +6,8 @@
 namespace giga {
 
 // Default number of 16-wide k-blocks accumulated in TMEM before promotion into the fp32
-// register sum. 16 k-blocks = K 256 = 32 k8 steps.
-constexpr int kDefaultPromoteKBlocks = 16;
+// register sum. 8 k-blocks = K 128 = 16 k8 steps.
+constexpr int kDefaultPromoteKBlocks = 8;
 
 // The promotion interval in effect (kDefaultPromoteKBlocks or $GIGA_PROMOTE_KBLOCKS).
 int default_promote_kblocks();
@@ -17,13 +17,18 @@ cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t s
 
 // C[M x N, row stride ldc] = A[M x K] * B[K x N] by 3xTF32 (terms = 3) or 1xTF32 (terms = 1)
 // on the tcgen05 tensor cores. Requires K % 4 == 0, N % 4 == 0, ldc % 4 == 0, 16B-aligned
-// pointers. promote_kblocks: 0 = never, -1 = default. Returns cudaErrorInvalidValue for bad
+// pointers. promote_kblocks: 0 = never, -1 = default. cta_group: 1 (128x256 tile per CTA),
+// 2 (256x256 tile per CTA pair), 0 = chosen by shape. Returns cudaErrorInvalidValue for bad
 // shapes, or the launch error.
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
                                const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,
-                               int64_t ldc, int terms, int promote_kblocks, cudaStream_t st);
+                               int64_t ldc, int terms, int promote_kblocks, cudaStream_t st,
+                               int cta_group = 0);
 
 // Resolves cuTensorMapEncodeTiled through the runtime (no libcuda link). 0 on success.
 int ensure_tma_encoder();
+
+// CTA-group size the GEMM launch will use for an M x N shard (1 or 2; $GIGA_CTA_GROUP).
+int choose_cta_group(int64_t M, int64_t N, int num_sms);
 
 }  // namespace giga

@@ -62,7 +62,7 @@ def _load():
         "giga_matmul_rank": ([p, p, p, i64, i64, i64, p], i32),
         "giga_split_lo": ([p, p, i64, p], i32),
         "giga_gemm_3xtf32": ([p, p, p, p, p, i64, i64, i64, i64, p], i32),
-        "giga_gemm_3xtf32_ex": ([p, p, p, p, p, i64, i64, i64, i64, i32, i32, p], i32),
+        "giga_gemm_3xtf32_ex": ([p, p, p, p, p, i64, i64, i64, i64, i32, i32, i32, p], i32),
         "giga_timing_enable": ([i32], i32),
         "giga_timing_reset": ([], i32),
         "giga_timing_read": ([ctypes.POINTER(ctypes.c_double), P64,
@@ -173,10 +173,10 @@ def split_lo(x, lo, n: int | None = None, stream=None):
 
 
 def gemm_3xtf32(A, A_lo, B, B_lo, C, M, N, K, ldc=None, terms=3, promote_kblocks=-1,
-                stream=None):
+                cta_group=0, stream=None):
     _check(lib.giga_gemm_3xtf32_ex(_ptr(A), _ptr(A_lo), _ptr(B), _ptr(B_lo), _ptr(C), M, N, K,
                                    N if ldc is None else ldc, terms, promote_kblocks,
-                                   _stream(stream)))
+                                   cta_group, _stream(stream)))
 
 
 # ---- timing -----------------------------------------------------------------------------

@@ -168,6 +168,48 @@ def test_integer_inputs_bit_exact(giga, torch_cuda, M, N, K):
         assert ok, st
 
 
+CG_SHAPES = [(1, 4, 4), (130, 260, 20), (255, 256, 16), (257, 512, 36), (600, 1000, 1028),
+             (2048, 2048, 512)]
+
+
+@pytest.mark.parametrize("cta_group", [1, 2])
+@pytest.mark.parametrize("M,N,K", CG_SHAPES)
+def test_cta_group_variants_bit_exact(giga, torch_cuda, M, N, K, cta_group):
+    """Both tile variants (1 CTA per 128x256 tile; CTA pair per 256x256 tile with
+    cta_group::2 UMMAs) on ragged shapes, integer inputs, NaN-prefilled C."""
+    torch = torch_cuda
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+    dA, dB = _dev(torch, A), _dev(torch, B)
+    dAlo, dBlo = torch.empty_like(dA), torch.empty_like(dB)
+    giga.split_lo(dA, dAlo)
+    giga.split_lo(dB, dBlo)
+    dC = torch.full((M, N), float("nan"), device="cuda")
+    giga.gemm_3xtf32(dA, dAlo, dB, dBlo, dC, M, N, K, cta_group=cta_group)
+    torch.cuda.synchronize()
+    Cref, _ = oracle.gemm(A, B)
+    ok, st = check_exact(dC.cpu().numpy(), Cref)
+    assert ok, st
+
+
+@pytest.mark.parametrize("cta_group", [1, 2])
+def test_cta_group_variants_tolerance(giga, torch_cuda, cta_group):
+    torch = torch_cuda
+    M, N, K = 700, 900, 3000
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, "d1")
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, "d1")
+    dA, dB = _dev(torch, A), _dev(torch, B)
+    dAlo, dBlo = torch.empty_like(dA), torch.empty_like(dB)
+    giga.split_lo(dA, dAlo)
+    giga.split_lo(dB, dBlo)
+    dC = torch.full((M, N), float("nan"), device="cuda")
+    giga.gemm_3xtf32(dA, dAlo, dB, dBlo, dC, M, N, K, cta_group=cta_group)
+    torch.cuda.synchronize()
+    Cref, S = oracle.gemm(A, B)
+    ok, st = check_close(dC.cpu().numpy(), Cref, S)
+    assert ok, st
+
+
 def test_all_ones_gives_k(giga, torch_cuda):
     M, N, K = 200, 300, 2000
     C = run_device(giga, torch_cuda, np.ones((M, K), np.float32), np.ones((K, N), np.float32))
