@@ -50,7 +50,7 @@ constexpr uint32_t A_BYTES = BM * BK * 4;        // 8 KiB: 128 rows x 64 B
 constexpr uint32_t B_CHUNK_BYTES = BK * 32 * 4;  // 2 KiB: one 32-column chunk of B
 constexpr uint32_t ACC_COLS = BN;                // fp32 accumulator: 1 TMEM column per n
 constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;     // two accumulators (promotion ping-pong)
-constexpr int GROUP_M = 16;                      // L2 raster: 16 M-tiles per group
+constexpr int GROUP_M = 8;                       // L2 raster: default M-tiles per group
 constexpr size_t SMEM_RING = 192 * 1024;         // operand ring per CTA
 }  // namespace cfg
 
@@ -70,6 +70,7 @@ struct GemmParams {
   int p_kb;       // k-blocks per TMEM accumulation interval (>= 1)
   int n_kb;       // k-blocks per tile
   int m_tiles, n_tiles, num_tiles;
+  int group_m;    // L2 raster: consecutive tiles walk group_m M-tiles before the next N-tile
 };
 
 // ---- UMMA descriptors -------------------------------------------------------------------
@@ -103,10 +104,10 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
 }
 
 __device__ __forceinline__ void tile_coords(int t, const GemmParams &p, int &mb, int &nb) {
-  const int group_size = cfg::GROUP_M * p.n_tiles;
+  const int group_size = p.group_m * p.n_tiles;
   const int g = t / group_size;
-  const int first_m = g * cfg::GROUP_M;
-  const int gm = min(cfg::GROUP_M, p.m_tiles - first_m);
+  const int first_m = g * p.group_m;
+  const int gm = min(p.group_m, p.m_tiles - first_m);
   const int local = t - g * group_size;
   mb = first_m + local % gm;
   nb = local / gm;
@@ -524,6 +525,11 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.m_tiles = int((M + tile_m - 1) / tile_m);
   p.n_tiles = int((N + BN - 1) / BN);
   p.num_tiles = p.m_tiles * p.n_tiles;
+  static int group_env = [] {
+    const char *e = getenv("GIGA_GROUP_M");
+    return (e && atoi(e) > 0) ? atoi(e) : 0;
+  }();
+  p.group_m = group_env ? group_env : GROUP_M;
 
   if (cg == 1) {
     cudaError_t e = ensure_smem_attr<1>();
