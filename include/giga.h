@@ -124,6 +124,18 @@ int giga_rank_init(int rank, int world, int device, const uint8_t id[128]);
 int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, int64_t N,
                      int64_t K, void *stream);
 
+/* The N > 1 pipeline's chunk plan (pure host arithmetic, identical on every rank; the
+ * orchestration of giga_matmul_sharded / giga_matmul_rank uses exactly these functions).
+ * B is broadcast from rank 0 in *kchunks K-row chunks [kbounds[c], kbounds[c+1]) (kbounds
+ * needs room for 17 entries), the shard GEMM accumulates chunk by chunk, and the C row
+ * blocks are gathered in *rchunks rounds; in round q owner o broadcasts the rows returned
+ * by giga_plan_block(M, world, rchunks, o, q). Knobs: $GIGA_BCAST_CHUNKS,
+ * $GIGA_GATHER_CHUNKS (default 4 each). Errors: INVALID_ARG. */
+int giga_pipeline_plan(int64_t M, int64_t N, int64_t K, int world, int *kchunks,
+                       int64_t *kbounds, int *rchunks);
+int giga_plan_block(int64_t M, int world, int rchunks, int owner, int q, int64_t *row0,
+                    int64_t *rows);
+
 /* ------------------------------------------------------------------------------------ */
 /* Single-device building blocks (device pointers on the current CUDA device; work is
  * enqueued on `stream`, a cudaStream_t, 0 = legacy default stream; no host sync). They do

@@ -62,6 +62,8 @@ struct Buf {
   size_t bytes = 0;
 };
 
+constexpr int kMaxChunks = 16;  // pipeline chunks per phase (B K-chunks, C row-chunks)
+
 struct DevCtx {
   int dev = -1;
   cudaStream_t compute = nullptr;  // splits + GEMM (+ H2D/D2H in host mode)
@@ -69,6 +71,8 @@ struct DevCtx {
   cudaEvent_t ev_b = nullptr;      // B present on this GPU
   cudaEvent_t ev_c = nullptr;      // this GPU's C rows computed
   cudaEvent_t ev_start = nullptr;  // caller-stream entry (rank mode)
+  std::vector<cudaEvent_t> ev_kchunk;  // pipeline: B K-chunk c present
+  std::vector<cudaEvent_t> ev_rchunk;  // pipeline: C row-chunk q computed
   Buf A_lo, B_lo, A_pad, B_pad, C_pad, A_h, B_h, C_h;
 };
 
@@ -189,6 +193,10 @@ int ctx_create(DevCtx &d, int dev) {
   CK(cudaEventCreateWithFlags(&d.ev_b, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d.ev_c, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d.ev_start, cudaEventDisableTiming));
+  for (auto *v : {&d.ev_kchunk, &d.ev_rchunk}) {
+    v->assign(kMaxChunks, nullptr);
+    for (auto &e : *v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   return GIGA_OK;
 }
 
@@ -201,6 +209,9 @@ void ctx_destroy(DevCtx &d) {
   if (d.comm) cudaStreamDestroy(d.comm);
   for (cudaEvent_t e : {d.ev_b, d.ev_c, d.ev_start})
     if (e) cudaEventDestroy(e);
+  for (auto *v : {&d.ev_kchunk, &d.ev_rchunk})
+    for (cudaEvent_t e : *v)
+      if (e) cudaEventDestroy(e);
   d = DevCtx{};
 }
 
@@ -378,10 +389,214 @@ int sync_all(int ngpus) {
   return GIGA_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// The multi-GPU pipeline (SURVEY.md 8(a) a3-a7 with 8(e) overlap). Per participant (one per
+// GPU in single-process mode; this process's GPU in rank mode):
+//   compute stream: split A -> A_lo (overlaps the first broadcast chunk);
+//                   for each K-chunk c: wait B chunk c, split it, GEMM over that K range
+//                   accumulating into the shard's rows of C (c > 0: C += A_c B_c, an fp32
+//                   RN add like the in-kernel promotion); the last K-chunk's GEMM is split
+//                   into row chunks q, each publishing an event;
+//   comm stream:    NCCL broadcast of B chunk by chunk from rank 0 (contiguous K-row
+//                   ranges), then per row chunk q one grouped broadcast per owner of its rows
+//                   of C (an all-gather of non-contiguous blocks), overlapping the GEMM of
+//                   the next row chunks.
+// The persistent GEMM leaves $GIGA_COMM_SMS SMs (default 8) free so NCCL's kernels run
+// beside it. Every collective is issued in the same order on every rank (the chunk bounds
+// are functions of M, N, K, world only).
+
+// The chunk plan: B is broadcast in pb K-chunks [kb[c], kb[c+1]) (multiples of 16, at least
+// 512 deep); the last K-chunk's GEMM and the C gather run in pc row chunks; chunk q of owner
+// o is rows [o0 + orows*q/pc, o0 + orows*(q+1)/pc) of its shard (plan_block). Knobs:
+// $GIGA_BCAST_CHUNKS (4), $GIGA_GATHER_CHUNKS (4); unaligned shapes use one chunk of each.
+struct Plan {
+  int pb = 1, pc = 1;
+  int64_t kb[kMaxChunks + 1] = {0};
+};
+
+int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
+Plan make_plan(int64_t M, int64_t K, int world, bool aligned) {
+  Plan pl;
+  int64_t rows_max = 0;
+  for (int r = 0; r < world; ++r) {
+    int64_t r0, rows;
+    partition_rows(M, world, r, &r0, &rows);
+    rows_max = std::max(rows_max, rows);
+  }
+  if (aligned) {
+    pl.pb = std::min(std::max(env_int("GIGA_BCAST_CHUNKS", 4), 1), kMaxChunks);
+    pl.pb = int(std::min<int64_t>(pl.pb, std::max<int64_t>(1, K / 512)));
+    pl.pc = std::min(std::max(env_int("GIGA_GATHER_CHUNKS", 4), 1), kMaxChunks);
+    pl.pc = int(std::min<int64_t>(pl.pc, std::max<int64_t>(1, rows_max / 256)));
+  }
+  for (int c = 0; c < pl.pb; ++c) pl.kb[c] = (K * c / pl.pb) / 16 * 16;
+  pl.kb[pl.pb] = K;
+  return pl;
+}
+
+void plan_block(int64_t M, int world, int pc, int owner, int q, int64_t *row0, int64_t *rows) {
+  int64_t o0, orows;
+  partition_rows(M, world, owner, &o0, &orows);
+  const int64_t q0 = orows * q / pc, q1 = orows * (q + 1) / pc;
+  *row0 = o0 + q0;
+  *rows = q1 - q0;
+}
+
+struct Part {
+  DevCtx *d;
+  ncclComm_t comm;
+  int rank;
+  const float *A;   // rows_r x K shard
+  float *B;         // K x N: source on rank 0, receive buffer elsewhere
+  float *C;         // M x N: every rank ends with all of C
+  cudaStream_t st;  // compute stream
+};
+
+bool force_comm() { return env_int("GIGA_FORCE_COMM", 0) != 0; }
+
+int gemm_chunk(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
+               int64_t rows, int64_t N, int64_t Kc, const GemmExtra &ex, cudaStream_t st) {
+  CK(timed(0, st, [&] {
+    return launch_gemm_3xtf32(A, Alo, B, Blo, C, rows, N, Kc, N, 3, -1, st, 0, &ex);
+  }));
+  return GIGA_OK;
+}
+
+int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int64_t K) {
+  const char *why = nullptr;
+  const NcclApi *api = nccl_api(&why);
+  if (!api) return fail(GIGA_ERR_COMM, "NCCL unavailable: %s", why ? why : "?");
+  bool aligned = (K % 4 == 0) && (N % 4 == 0);
+  for (auto &p : parts) aligned = aligned && aligned16(p.A) && aligned16(p.B) && aligned16(p.C);
+  const Plan plan = make_plan(M, K, world, aligned);
+  const int pb = plan.pb, pc = plan.pc;
+  const int64_t *kb = plan.kb;
+  GemmExtra ex;
+  ex.lda = K;
+  ex.ldb = N;
+  {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, parts[0].d->dev);
+    ex.max_ctas = std::max(2, nsm - std::max(0, env_int("GIGA_COMM_SMS", 8)));
+  }
+
+  // 0. join the caller's stream, workspace, split A
+  for (auto &p : parts) {
+    CK(cudaSetDevice(p.d->dev));
+    CK(cudaEventRecord(p.d->ev_start, p.st));
+    CK(cudaStreamWaitEvent(p.d->comm, p.d->ev_start, 0));
+    int64_t r0, rows;
+    partition_rows(M, world, p.rank, &r0, &rows);
+    if (aligned) {
+      TRY(ws_reserve(*p.d, {{&p.d->A_lo, size_t(std::max<int64_t>(rows, 1) * K) * 4},
+                            {&p.d->B_lo, size_t(K * N) * 4}}));
+      if (rows > 0) TRY(split(p.A, fptr(p.d->A_lo), rows * K, p.st));
+    }
+  }
+  // 1. broadcast B from rank 0, K-chunk by K-chunk
+  for (int c = 0; c < pb; ++c) {
+    TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
+    for (auto &p : parts) {
+      CK(cudaSetDevice(p.d->dev));
+      float *src = p.B + kb[c] * N;
+      ncclResult_t r = api->Broadcast(src, src, size_t((kb[c + 1] - kb[c]) * N), ncclFloat32, 0,
+                                      p.comm, p.d->comm);
+      if (r != ncclSuccess) {
+        api->GroupEnd();
+        return nccl_check(r, "ncclBroadcast(B chunk)");
+      }
+    }
+    TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
+    for (auto &p : parts) {
+      CK(cudaSetDevice(p.d->dev));
+      CK(cudaEventRecord(p.d->ev_kchunk[c], p.d->comm));
+    }
+  }
+  // 2. compute: K-chunks accumulate into C; the last one in row chunks
+  for (auto &p : parts) {
+    CK(cudaSetDevice(p.d->dev));
+    int64_t r0, rows;
+    partition_rows(M, world, p.rank, &r0, &rows);
+    float *Cs = p.C + r0 * N;
+    if (!aligned) {  // padded single-chunk path (odd shapes / unaligned pointers)
+      TRY(shard_compute(*p.d, p.st, p.A, rows, p.B, Cs, N, N, K, p.d->ev_kchunk[0]));
+      CK(cudaEventRecord(p.d->ev_rchunk[0], p.st));
+      continue;
+    }
+    const float *Alo = fptr(p.d->A_lo);
+    float *Blo = fptr(p.d->B_lo);
+    for (int c = 0; c < pb; ++c) {
+      const int64_t Kc = kb[c + 1] - kb[c];
+      CK(cudaStreamWaitEvent(p.st, p.d->ev_kchunk[c], 0));
+      TRY(split(p.B + kb[c] * N, Blo + kb[c] * N, Kc * N, p.st));
+      GemmExtra e = ex;
+      e.accumulate = c > 0;
+      const float *Bc = p.B + kb[c] * N, *Bloc = Blo + kb[c] * N;
+      if (c < pb - 1) {
+        if (rows > 0)
+          TRY(gemm_chunk(p.A + kb[c], Alo + kb[c], Bc, Bloc, Cs, rows, N, Kc, e, p.st));
+        continue;
+      }
+      for (int q = 0; q < pc; ++q) {
+        int64_t b0, brows;
+        plan_block(M, world, pc, p.rank, q, &b0, &brows);
+        const int64_t q0 = b0 - r0;  // offset inside this rank's shard
+        if (brows > 0)
+          TRY(gemm_chunk(p.A + q0 * K + kb[c], Alo + q0 * K + kb[c], Bc, Bloc, Cs + q0 * N,
+                         brows, N, Kc, e, p.st));
+        CK(cudaEventRecord(p.d->ev_rchunk[q], p.st));
+      }
+    }
+  }
+  // 3. gather C row chunk by row chunk: one broadcast per owner, grouped
+  for (int q = 0; q < pc; ++q) {
+    for (auto &p : parts) {
+      CK(cudaSetDevice(p.d->dev));
+      CK(cudaStreamWaitEvent(p.d->comm, p.d->ev_rchunk[q], 0));
+    }
+    TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
+    for (auto &p : parts) {
+      CK(cudaSetDevice(p.d->dev));
+      if (pc == 1) {  // whole blocks: in-place all-gather when equal, else per-owner bcast
+        const int rc = gather_rows(api, p.comm, p.d->comm, p.C, M, N, world, p.rank);
+        if (rc != GIGA_OK) {
+          api->GroupEnd();
+          return rc;
+        }
+        continue;
+      }
+      for (int o = 0; o < world; ++o) {
+        int64_t b0, brows;
+        plan_block(M, world, pc, o, q, &b0, &brows);
+        if (brows <= 0) continue;
+        float *blk = p.C + b0 * N;
+        ncclResult_t r =
+            api->Broadcast(blk, blk, size_t(brows * N), ncclFloat32, o, p.comm, p.d->comm);
+        if (r != ncclSuccess) {
+          api->GroupEnd();
+          return nccl_check(r, "ncclBroadcast(C chunk)");
+        }
+      }
+    }
+    TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
+  }
+  // 4. the caller's stream resumes after the gather
+  for (auto &p : parts) {
+    CK(cudaSetDevice(p.d->dev));
+    CK(cudaEventRecord(p.d->ev_c, p.d->comm));
+    CK(cudaStreamWaitEvent(p.st, p.d->ev_c, 0));
+  }
+  return GIGA_OK;
+}
+
 // Device-resident path on GPUs 0..ngpus-1 (B_buf[0] root, C_full[g] all receive full C).
 int sharded_locked(const float *const *A_shard, float *const *B_buf, float *const *C_full,
                    int64_t M, int64_t N, int64_t K, int ngpus) {
-  if (ngpus == 1) {
+  if (ngpus == 1 && !force_comm()) {
     DevCtx &d = g.devs[0];
     CK(cudaSetDevice(d.dev));
     TRY(shard_compute(d, d.compute, A_shard[0], M, B_buf[0], C_full[0], N, N, K, nullptr));
@@ -390,43 +605,14 @@ int sharded_locked(const float *const *A_shard, float *const *B_buf, float *cons
   std::vector<ncclComm_t> *comms = nullptr;
   TRY(get_comms(ngpus, &comms));
   const NcclApi *api = nccl_api(nullptr);
-  // (1) distribute B: broadcast from GPU 0 on the comm streams
-  TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
+  std::vector<Part> parts;
   for (int i = 0; i < ngpus; ++i) {
-    DevCtx &d = g.devs[i];
-    CK(cudaSetDevice(d.dev));
-    ncclResult_t r = api->Broadcast(B_buf[0], B_buf[i], size_t(K * N), ncclFloat32, 0,
-                                    (*comms)[i], d.comm);
-    if (r != ncclSuccess) {
-      api->GroupEnd();
-      return nccl_check(r, "ncclBroadcast(B)");
-    }
-  }
-  TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
-  // (2) per GPU: split A (overlaps the broadcast), then B, then the GEMM
-  for (int i = 0; i < ngpus; ++i) {
-    DevCtx &d = g.devs[i];
-    CK(cudaSetDevice(d.dev));
-    CK(cudaEventRecord(d.ev_b, d.comm));
     int64_t r0, rows;
     partition_rows(M, ngpus, i, &r0, &rows);
-    TRY(shard_compute(d, d.compute, A_shard[i], rows, B_buf[i], C_full[i] + r0 * N, N, N, K,
-                      d.ev_b));
-    CK(cudaEventRecord(d.ev_c, d.compute));
-    CK(cudaStreamWaitEvent(d.comm, d.ev_c, 0));
+    parts.push_back({&g.devs[i], (*comms)[i], i, A_shard[i], B_buf[i], C_full[i],
+                     g.devs[i].compute});
   }
-  // (3) gather the C row blocks on every GPU
-  TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
-  for (int i = 0; i < ngpus; ++i) {
-    DevCtx &d = g.devs[i];
-    CK(cudaSetDevice(d.dev));
-    int rc = gather_rows(api, (*comms)[i], d.comm, C_full[i], M, N, ngpus, i);
-    if (rc != GIGA_OK) {
-      api->GroupEnd();
-      return rc;
-    }
-  }
-  TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
+  TRY(run_pipeline(parts, ngpus, M, N, K));
   TRY(sync_all(ngpus));
   for (int i = 0; i < ngpus; ++i) {
     ncclResult_t ar = ncclSuccess;
@@ -682,7 +868,7 @@ int giga_rank_init(int rank, int world, int device, const uint8_t id[128]) {
     g.devs.clear();
     return rc;
   }
-  if (world > 1) {
+  if (world > 1 || force_comm()) {  // GIGA_FORCE_COMM: the N>1 pipeline at world size 1
     const char *why = nullptr;
     const NcclApi *api = nccl_api(&why);
     if (!api) {
@@ -691,7 +877,13 @@ int giga_rank_init(int rank, int world, int device, const uint8_t id[128]) {
       return fail(GIGA_ERR_COMM, "NCCL unavailable: %s", why ? why : "?");
     }
     ncclUniqueId u;
-    memcpy(u.internal, id, 128);
+    if (id)
+      memcpy(u.internal, id, 128);
+    else if ((rc = nccl_check(api->GetUniqueId(&u), "ncclGetUniqueId")) != GIGA_OK) {
+      ctx_destroy(g.devs[0]);
+      g.devs.clear();
+      return rc;
+    }
     cudaSetDevice(device);
     rc = nccl_check(api->CommInitRank(&g.rank_comm, world, u, rank), "ncclCommInitRank");
     if (rc != GIGA_OK) {
@@ -718,22 +910,31 @@ int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, i
   DevCtx &d = g.devs[0];
   CK(cudaSetDevice(d.dev));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.compute;
-  if (g.world == 1)
+  if (!g.rank_comm)
     return shard_compute(d, st, A_shard, rows, B, C_full + r0 * N, N, N, K, nullptr);
-  const NcclApi *api = nccl_api(nullptr);
-  // comm stream joins the caller's stream, broadcasts B, and later gathers C
-  CK(cudaEventRecord(d.ev_start, st));
-  CK(cudaStreamWaitEvent(d.comm, d.ev_start, 0));
-  TRY(nccl_check(api->Broadcast(B, B, size_t(K * N), ncclFloat32, 0, g.rank_comm, d.comm),
-                 "ncclBroadcast(B)"));
-  CK(cudaEventRecord(d.ev_b, d.comm));
-  TRY(shard_compute(d, st, A_shard, rows, B, C_full + r0 * N, N, N, K, d.ev_b));
-  CK(cudaEventRecord(d.ev_c, st));
-  CK(cudaStreamWaitEvent(d.comm, d.ev_c, 0));
-  TRY(gather_rows(api, g.rank_comm, d.comm, C_full, M, N, g.world, g.rank));
-  // the caller's stream resumes after the gather
-  CK(cudaEventRecord(d.ev_c, d.comm));
-  CK(cudaStreamWaitEvent(st, d.ev_c, 0));
+  std::vector<Part> parts{{&d, g.rank_comm, g.rank, A_shard, B, C_full, st}};
+  return run_pipeline(parts, g.world, M, N, K);
+}
+
+// ---- pipeline plan (host arithmetic) -----------------------------------------------------
+
+int giga_pipeline_plan(int64_t M, int64_t N, int64_t K, int world, int *kchunks,
+                       int64_t *kbounds, int *rchunks) {
+  if (M < 1 || N < 1 || K < 1 || world < 1 || !kchunks || !kbounds || !rchunks)
+    return fail(GIGA_ERR_INVALID_ARG, "giga_pipeline_plan: bad arguments");
+  const Plan pl = make_plan(M, K, world, (K % 4 == 0) && (N % 4 == 0));
+  *kchunks = pl.pb;
+  *rchunks = pl.pc;
+  for (int c = 0; c <= pl.pb; ++c) kbounds[c] = pl.kb[c];
+  return GIGA_OK;
+}
+
+int giga_plan_block(int64_t M, int world, int rchunks, int owner, int q, int64_t *row0,
+                    int64_t *rows) {
+  if (M < 0 || world < 1 || rchunks < 1 || owner < 0 || owner >= world || q < 0 ||
+      q >= rchunks || !row0 || !rows)
+    return fail(GIGA_ERR_INVALID_ARG, "giga_plan_block: bad arguments");
+  plan_block(M, world, rchunks, owner, q, row0, rows);
   return GIGA_OK;
 }
 

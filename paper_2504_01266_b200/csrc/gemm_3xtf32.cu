@@ -66,6 +66,7 @@ struct Tile {
 
 struct GemmParams {
   int M, N, K, ldc;
+  int accumulate; // 1: C += A*B (K-chunked pipelines), 0: C = A*B
   int terms;      // 3 = 3xTF32, 1 = TF32 (hi*hi only)
   int p_kb;       // k-blocks per TMEM accumulation interval (>= 1)
   int n_kb;       // k-blocks per tile
@@ -327,18 +328,19 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       const int row = mb * T::TILE_M + row_in_tile;
       if (row < p.M) {
         const int col0 = nb * BN + half * 128;
-        float *crow = C + int64_t(row) * p.ldc + col0;
-        if (col0 + 128 <= p.N) {
+        float4 *crow = reinterpret_cast<float4 *>(C + int64_t(row) * p.ldc + col0);
+        const bool all_cols = col0 + 128 <= p.N;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            reinterpret_cast<float4 *>(crow)[j] =
-                make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col0 + 4 * j < p.N)  // N % 4 == 0: a float4 is all-in or all-out
-              reinterpret_cast<float4 *>(crow)[j] =
-                  make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+        for (int j = 0; j < 32; ++j) {
+          if (all_cols || col0 + 4 * j < p.N) {  // N % 4 == 0: a float4 is all-in or all-out
+            float4 v = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
+            if (p.accumulate) {  // C += this K-chunk's sum: one more RN promotion add
+              const float4 o = crow[j];
+              v = make_float4(__fadd_rn(o.x, v.x), __fadd_rn(o.y, v.y), __fadd_rn(o.z, v.z),
+                              __fadd_rn(o.w, v.w));
+            }
+            crow[j] = v;
+          }
         }
       }
     }
@@ -487,9 +489,13 @@ static cudaError_t ensure_smem_attr() {
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
                                const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,
                                int64_t ldc, int terms, int promote_kblocks, cudaStream_t st,
-                               int cta_group) {
+                               int cta_group, const GemmExtra *ex) {
   using namespace cfg;
-  if (M < 1 || N < 1 || K < 1 || (K & 3) || (N & 3) || (ldc & 3) || ldc < N)
+  GemmExtra dflt;
+  if (!ex) ex = &dflt;
+  const int64_t lda = ex->lda ? ex->lda : K, ldb = ex->ldb ? ex->ldb : N;
+  if (M < 1 || N < 1 || K < 1 || (lda & 3) || (ldb & 3) || (ldc & 3) || ldc < N || lda < K ||
+      ldb < N)
     return cudaErrorInvalidValue;
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || ldc > INT32_MAX)
     return cudaErrorInvalidValue;
@@ -497,15 +503,17 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   if (terms == 3 && (!A_lo || !B_lo)) return cudaErrorInvalidValue;
   if (ensure_tma_encoder() != 0) return cudaErrorNotSupported;
 
-  const int num_sms = num_sms_current();
+  int num_sms = num_sms_current();
+  if (ex->max_ctas > 0 && ex->max_ctas < num_sms) num_sms = ex->max_ctas & ~1;
+  if (num_sms < 2) num_sms = 2;
   const int cg = (cta_group == 1 || cta_group == 2) ? cta_group : choose_cta_group(M, N, num_sms);
   CUtensorMap tA, tAlo, tB, tBlo;
-  if (!make_map(&tA, A, K, M, K, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
-      !make_map(&tB, B, N, K, N, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+  if (!make_map(&tA, A, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !make_map(&tB, B, N, K, ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return cudaErrorInvalidValue;
   if (terms == 3) {
-    if (!make_map(&tAlo, A_lo, K, M, K, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
-        !make_map(&tBlo, B_lo, N, K, N, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    if (!make_map(&tAlo, A_lo, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !make_map(&tBlo, B_lo, N, K, ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
       return cudaErrorInvalidValue;
   } else {
     tAlo = tA;
@@ -517,6 +525,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.N = int(N);
   p.K = int(K);
   p.ldc = int(ldc);
+  p.accumulate = ex->accumulate ? 1 : 0;
   p.terms = terms;
   p.n_kb = int((K + BK - 1) / BK);
   int pk = promote_kblocks < 0 ? default_promote_kblocks() : promote_kblocks;

@@ -20,10 +20,19 @@ cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t s
 // pointers. promote_kblocks: 0 = never, -1 = default. cta_group: 1 (128x256 tile per CTA),
 // 2 (256x256 tile per CTA pair), 0 = chosen by shape. Returns cudaErrorInvalidValue for bad
 // shapes, or the launch error.
+// Extra operand/launch options: lda / ldb = row strides of A and B in elements (0 = K and
+// N, i.e. dense; K-chunked pipelines pass A + k0 with lda = the full K); accumulate = 1 adds
+// into C (C += A*B, fp32 RN) instead of overwriting; max_ctas caps the persistent grid (SMs
+// left free for concurrent communication kernels; 0 = all SMs).
+struct GemmExtra {
+  int64_t lda = 0, ldb = 0;
+  int accumulate = 0;
+  int max_ctas = 0;
+};
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
                                const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,
                                int64_t ldc, int terms, int promote_kblocks, cudaStream_t st,
-                               int cta_group = 0);
+                               int cta_group = 0, const GemmExtra *ex = nullptr);
 
 // Resolves cuTensorMapEncodeTiled through the runtime (no libcuda link). 0 on success.
 int ensure_tma_encoder();

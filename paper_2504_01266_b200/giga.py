@@ -25,7 +25,8 @@ EXPORTS = (
     "giga_init", "giga_num_devices", "giga_finalize", "giga_partition", "giga_matmul",
     "giga_matmul_sharded", "giga_last_error", "giga_comm_unique_id", "giga_rank_init",
     "giga_matmul_rank", "giga_split_lo", "giga_gemm_3xtf32", "giga_gemm_3xtf32_ex",
-    "giga_timing_enable", "giga_timing_reset", "giga_timing_read",
+    "giga_timing_enable", "giga_timing_reset", "giga_timing_read", "giga_pipeline_plan",
+    "giga_plan_block",
 )
 
 
@@ -67,6 +68,9 @@ def _load():
         "giga_timing_reset": ([], i32),
         "giga_timing_read": ([ctypes.POINTER(ctypes.c_double), P64,
                               ctypes.POINTER(ctypes.c_double), P64], i32),
+        "giga_pipeline_plan": ([i64, i64, i64, i32, ctypes.POINTER(i32), P64,
+                                ctypes.POINTER(i32)], i32),
+        "giga_plan_block": ([i64, i32, i32, i32, i32, P64, P64], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -163,6 +167,20 @@ def rank_init(rank: int, world: int, device: int, uid: bytes | None):
 
 def matmul_rank(A_shard, B, C_full, M: int, N: int, K: int, stream=None):
     _check(lib.giga_matmul_rank(_ptr(A_shard), _ptr(B), _ptr(C_full), M, N, K, _stream(stream)))
+
+
+def pipeline_plan(M: int, N: int, K: int, world: int):
+    """(kbounds, rchunks): B K-chunk bounds and the number of C gather rounds."""
+    kc, rc = ctypes.c_int(), ctypes.c_int()
+    kb = (ctypes.c_int64 * 17)()
+    _check(lib.giga_pipeline_plan(M, N, K, world, ctypes.byref(kc), kb, ctypes.byref(rc)))
+    return [kb[i] for i in range(kc.value + 1)], rc.value
+
+
+def plan_block(M: int, world: int, rchunks: int, owner: int, q: int):
+    r0, rows = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.giga_plan_block(M, world, rchunks, owner, q, ctypes.byref(r0), ctypes.byref(rows)))
+    return r0.value, rows.value
 
 
 # ---- building blocks --------------------------------------------------------------------
