@@ -67,7 +67,8 @@ constexpr int kMaxChunks = 16;  // pipeline chunks per phase (B K-chunks, C row-
 struct DevCtx {
   int dev = -1;
   cudaStream_t compute = nullptr;  // splits + GEMM (+ H2D/D2H in host mode)
-  cudaStream_t comm = nullptr;     // broadcast of B, gather of C
+  cudaStream_t comm = nullptr;     // broadcast of B, gather of C (host mode: H2D copies)
+  cudaStream_t d2h = nullptr;      // host mode: device-to-host copies of finished C rows
   cudaEvent_t ev_b = nullptr;      // B present on this GPU
   cudaEvent_t ev_c = nullptr;      // this GPU's C rows computed
   cudaEvent_t ev_start = nullptr;  // caller-stream entry (rank mode)
@@ -190,6 +191,7 @@ int ctx_create(DevCtx &d, int dev) {
   CK(cudaSetDevice(dev));
   CK(cudaStreamCreateWithFlags(&d.compute, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&d.comm, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&d.d2h, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&d.ev_b, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d.ev_c, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d.ev_start, cudaEventDisableTiming));
@@ -207,6 +209,7 @@ void ctx_destroy(DevCtx &d) {
   ws_free(d);
   if (d.compute) cudaStreamDestroy(d.compute);
   if (d.comm) cudaStreamDestroy(d.comm);
+  if (d.d2h) cudaStreamDestroy(d.d2h);
   for (cudaEvent_t e : {d.ev_b, d.ev_c, d.ev_start})
     if (e) cudaEventDestroy(e);
   for (auto *v : {&d.ev_kchunk, &d.ev_rchunk})
@@ -622,6 +625,54 @@ int sharded_locked(const float *const *A_shard, float *const *B_buf, float *cons
   return GIGA_OK;
 }
 
+// Host buffers on one GPU (the paper's call): a row-block pipeline over three
+// engines -- host-to-device copies on the comm stream, splits + GEMMs on the compute stream,
+// device-to-host copies on the d2h stream. B goes first; then A row block q is copied while
+// block q-1 computes, and block q's C rows are copied back while block q+1 computes. With
+// pinned host memory the PCIe transfers overlap the tensor-core work. $GIGA_HOST_CHUNKS
+// (default 8) row blocks.
+int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M, int64_t N,
+                  int64_t K) {
+  CK(cudaSetDevice(d.dev));
+  int Q = std::min(std::max(env_int("GIGA_HOST_CHUNKS", 8), 1), kMaxChunks);
+  Q = int(std::min<int64_t>(Q, std::max<int64_t>(1, M / 256)));
+  TRY(ws_reserve(d, {{&d.A_h, size_t(M * K) * 4},
+                     {&d.B_h, size_t(K * N) * 4},
+                     {&d.C_h, size_t(M * N) * 4},
+                     {&d.A_lo, size_t(M * K) * 4},
+                     {&d.B_lo, size_t(K * N) * 4}}));
+  float *Ad = fptr(d.A_h), *Bd = fptr(d.B_h), *Cd = fptr(d.C_h);
+  CK(cudaMemcpyAsync(Bd, B, size_t(K * N) * 4, cudaMemcpyHostToDevice, d.comm));
+  CK(cudaEventRecord(d.ev_b, d.comm));
+  for (int q = 0; q < Q; ++q) {
+    const int64_t q0 = M * q / Q, q1 = M * (q + 1) / Q;
+    if (q1 > q0)
+      CK(cudaMemcpyAsync(Ad + q0 * K, A + q0 * K, size_t((q1 - q0) * K) * 4,
+                         cudaMemcpyHostToDevice, d.comm));
+    CK(cudaEventRecord(d.ev_kchunk[q], d.comm));
+  }
+  CK(cudaStreamWaitEvent(d.compute, d.ev_b, 0));
+  TRY(split(Bd, fptr(d.B_lo), K * N, d.compute));
+  for (int q = 0; q < Q; ++q) {
+    const int64_t q0 = M * q / Q, q1 = M * (q + 1) / Q;
+    CK(cudaStreamWaitEvent(d.compute, d.ev_kchunk[q], 0));
+    if (q1 > q0) {
+      TRY(split(Ad + q0 * K, fptr(d.A_lo) + q0 * K, (q1 - q0) * K, d.compute));
+      TRY(gemm(Ad + q0 * K, fptr(d.A_lo) + q0 * K, Bd, fptr(d.B_lo), Cd + q0 * N, q1 - q0, N, K,
+               N, d.compute));
+    }
+    CK(cudaEventRecord(d.ev_rchunk[q], d.compute));
+    CK(cudaStreamWaitEvent(d.d2h, d.ev_rchunk[q], 0));
+    if (q1 > q0)
+      CK(cudaMemcpyAsync(C + q0 * N, Cd + q0 * N, size_t((q1 - q0) * N) * 4,
+                         cudaMemcpyDeviceToHost, d.d2h));
+  }
+  CK(cudaStreamSynchronize(d.d2h));
+  CK(cudaStreamSynchronize(d.compute));
+  CK(cudaStreamSynchronize(d.comm));
+  return GIGA_OK;
+}
+
 int matmul_locked(const float *A, const float *B, float *C, int64_t M, int64_t N, int64_t K,
                   int ngpus) {
   int da = -1, db = -1, dc = -1;
@@ -638,6 +689,7 @@ int matmul_locked(const float *A, const float *B, float *C, int64_t M, int64_t N
     TRY(shard_compute(d, d.compute, A, M, B, C, N, N, K, nullptr));
     return sync_all(1);
   }
+  if (!device && ngpus == 1 && K % 4 == 0 && N % 4 == 0) return host_pipeline(g.devs[0], A, B, C, M, N, K);
 
   // Stage: every GPU gets its A row block and a B buffer; GPU 0 gets B.
   for (int i = 0; i < ngpus; ++i) {

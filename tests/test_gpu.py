@@ -261,6 +261,25 @@ def test_pipeline_forced_comm_rank_api(torch_cuda, monkeypatch):
         g.init(1)
 
 
+@pytest.mark.parametrize("M,N,K,pinned", [(2000, 520, 1028, True), (4096, 256, 512, False),
+                                          (300, 64, 40, True)])
+def test_host_pipeline_row_blocks(giga, torch_cuda, M, N, K, pinned):
+    """giga_matmul with host buffers: row-block H2D / GEMM / D2H pipeline, bit-exact."""
+    torch = torch_cuda
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+    if pinned:
+        tA, tB = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
+        tC = torch.full((M, N), float("nan")).pin_memory()
+        giga.matmul(tA, tB, tC, M, N, K, 1)
+        C = tC.numpy()
+    else:
+        C = run_host(giga, A, B)
+    Cref, _ = oracle.gemm(A, B)
+    ok, st = check_exact(C, Cref)
+    assert ok, st
+
+
 def test_all_ones_gives_k(giga, torch_cuda):
     M, N, K = 200, 300, 2000
     C = run_device(giga, torch_cuda, np.ones((M, K), np.float32), np.ones((K, N), np.float32))
