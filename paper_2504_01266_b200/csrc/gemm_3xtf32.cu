@@ -26,7 +26,8 @@
 //       warp 1 lane 0  MMA issuer (leader CTA): 3 UMMAs per k8; tcgen05.commit frees smem
 //                      stages in both CTAs and publishes finished accumulators
 //       warps 2..9     epilogue: tcgen05.ld TMEM -> registers, RN fp32 promotion adds,
-//                      16-byte vector stores into the shard's rows of C.
+//                      swizzled smem staging -> TMA bulk stores (reduce-add when a K-chunked
+//                      pipeline accumulates) into the shard's rows of C.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -52,6 +53,8 @@ constexpr uint32_t ACC_COLS = BN;                // fp32 accumulator: 1 TMEM col
 constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;     // two accumulators (promotion ping-pong)
 constexpr int GROUP_M = 8;                       // L2 raster: default M-tiles per group
 constexpr size_t SMEM_RING = 192 * 1024;         // operand ring per CTA
+constexpr uint32_t EPI_STAGE_BYTES = 32 * 32 * 4;  // per epilogue warp: 32 rows x 32 fp32
+constexpr uint32_t EPI_BYTES = NUM_EPI_WARPS * EPI_STAGE_BYTES;  // 32 KiB C staging
 }  // namespace cfg
 
 template <int CG>
@@ -61,7 +64,8 @@ struct Tile {
   static constexpr uint32_t B_BYTES = cfg::BK * B_COLS * 4;      // per operand per CTA
   static constexpr uint32_t STAGE_BYTES = 2 * cfg::A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = int(cfg::SMEM_RING / STAGE_BYTES);  // 4 (CG=1), 6 (CG=2)
-  static constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
+  static constexpr size_t SMEM_BYTES =
+      size_t(STAGES) * STAGE_BYTES + cfg::EPI_BYTES + 1024 + 256;
 };
 
 struct GemmParams {
@@ -119,15 +123,16 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmAlo,
                        const __grid_constant__ CUtensorMap tmB,
-                       const __grid_constant__ CUtensorMap tmBlo, float *__restrict__ C,
-                       const GemmParams p) {
+                       const __grid_constant__ CUtensorMap tmBlo,
+                       const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
   using namespace cfg;
   using T = Tile<CG>;
   constexpr int STAGES = T::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * T::STAGE_BYTES);
+  uint8_t *epi_stage = smem + STAGES * T::STAGE_BYTES;  // C staging for the TMA stores
+  uint64_t *full = reinterpret_cast<uint64_t *>(epi_stage + EPI_BYTES);
   uint64_t *empty = full + STAGES;
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
@@ -147,6 +152,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       ptx::prefetch_tmap(&tmAlo);
       ptx::prefetch_tmap(&tmBlo);
     }
+    ptx::prefetch_tmap(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -292,7 +298,6 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     const int e = warp - 2;
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int half = e >> 2;    // column half of the 256-wide tile
-    const int row_in_tile = int(rank) * BM + quad * 32 + lane;
     const uint32_t tempty_leader0 = ptx::smem_u32(&tempty[0]) & ptx::kPeerBitMask;
     const uint32_t tempty_leader1 = ptx::smem_u32(&tempty[1]) & ptx::kPeerBitMask;
     uint32_t acc_iter = 0;
@@ -324,26 +329,36 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
             ptx::mbar_arrive_cluster(buf ? tempty_leader1 : tempty_leader0);
         }
       }
-      // store this thread's row segment: 128 consecutive fp32 = 32 x 16 B
-      const int row = mb * T::TILE_M + row_in_tile;
-      if (row < p.M) {
-        const int col0 = nb * BN + half * 128;
-        float4 *crow = reinterpret_cast<float4 *>(C + int64_t(row) * p.ldc + col0);
-        const bool all_cols = col0 + 128 <= p.N;
+      // C: this warp's 32 rows x 128 columns go out as four 32 x 32 TMA bulk stores through
+      // its 4 KiB staging tile (128B-swizzled rows: 16-byte chunk j of row r sits at chunk
+      // j ^ (r & 7), so each 8-lane phase of a v4 store covers all 32 banks). The TMA unit
+      // writes whole 128-byte row segments and clips rows >= M / columns >= N. Accumulate
+      // mode (K-chunked pipelines) uses the TMA reduce-add: C += partial in fp32.
+      const uint32_t stg = ptx::smem_u32(epi_stage + e * EPI_STAGE_BYTES);
+      const int crow0 = mb * T::TILE_M + int(rank) * BM + quad * 32;
+      const int ccol0 = nb * BN + half * 128;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (all_cols || col0 + 4 * j < p.N) {  // N % 4 == 0: a float4 is all-in or all-out
-            float4 v = make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]);
-            if (p.accumulate) {  // C += this K-chunk's sum: one more RN promotion add
-              const float4 o = crow[j];
-              v = make_float4(__fadd_rn(o.x, v.x), __fadd_rn(o.y, v.y), __fadd_rn(o.z, v.z),
-                              __fadd_rn(o.w, v.w));
-            }
-            crow[j] = v;
-          }
+      for (int c = 0; c < 4; ++c) {
+        if (lane == 0) ptx::bulk_wait_read<0>();  // previous store has left the staging tile
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t off = uint32_t(lane) * 128 + uint32_t((j ^ (lane & 7)) * 16);
+          ptx::st_shared_v4(stg + off, sum[c * 32 + 4 * j], sum[c * 32 + 4 * j + 1],
+                            sum[c * 32 + 4 * j + 2], sum[c * 32 + 4 * j + 3]);
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (p.accumulate)
+            ptx::tma_store_add_2d(&tmC, epi_stage + e * EPI_STAGE_BYTES, ccol0 + 32 * c, crow0);
+          else
+            ptx::tma_store_2d(&tmC, epi_stage + e * EPI_STAGE_BYTES, ccol0 + 32 * c, crow0);
+          ptx::bulk_commit();
         }
       }
     }
+    if (lane == 0) ptx::bulk_wait<0>();  // all C writes complete before the CTA retires
   }
   __syncwarp();
   ptx::tc_fence_before();
@@ -515,9 +530,10 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   if (ex->max_ctas > 0 && ex->max_ctas < num_sms) num_sms = ex->max_ctas & ~1;
   if (num_sms < 2) num_sms = 2;
   const int cg = (cta_group == 1 || cta_group == 2) ? cta_group : choose_cta_group(M, N, num_sms);
-  CUtensorMap tA, tAlo, tB, tBlo;
+  CUtensorMap tA, tAlo, tB, tBlo, tC;
   if (!make_map(&tA, A, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
-      !make_map(&tB, B, N, K, ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+      !make_map(&tB, B, N, K, ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+      !make_map(&tC, C, N, M, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   if (terms == 3) {
     if (!make_map(&tAlo, A_lo, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
@@ -553,7 +569,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
     if (e != cudaSuccess) return e;
     const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
     gemm_3xtf32_kernel<1><<<grid, NUM_THREADS, Tile<1>::SMEM_BYTES, st>>>(tA, tAlo, tB, tBlo,
-                                                                          C, p);
+                                                                          tC, p);
     return cudaGetLastError();
   }
   cudaError_t e = ensure_smem_attr<2>();
@@ -572,7 +588,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  return cudaLaunchKernelEx(&lc, gemm_3xtf32_kernel<2>, tA, tAlo, tB, tBlo, C, p);
+  return cudaLaunchKernelEx(&lc, gemm_3xtf32_kernel<2>, tA, tAlo, tB, tBlo, tC, p);
 }
 
 }  // namespace giga

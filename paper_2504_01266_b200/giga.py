@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgiga.so")
+LIB_PATH = os.environ.get("GIGA_LIB_PATH") or os.path.join(_HERE, "libgiga.so")  # A/B runs
 
 GIGA_OK = 0
 STATUS = {

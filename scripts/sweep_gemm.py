@@ -6,6 +6,8 @@ import synth
 from paper_2504_01266_b200 import giga
 
 M = N = K = int(os.environ.get("SIZE", "16384"))
+if os.environ.get("MNK"):
+    M, N, K = (int(x) for x in os.environ["MNK"].split(","))
 dev = torch.device("cuda", 0)
 A = synth.gen_rows_torch(0, M, K, 1, "d2", device=dev)
 B = synth.gen_rows_torch(0, K, N, 2, "d2", device=dev)
