@@ -280,6 +280,19 @@ def main():
                          f"{round(achieved / tf32_burst, 4) if achieved else None}",
             "split_ms_per_step": round(kt["split_ms"] / args.steps, 4)}
 
+    # ---- the north_star's whole-step roofline: T_roof / t with
+    #      T_roof = max(2 r_max N K / (P_tf32 / 3), 4 (K N [g > 1] + (M - r_min) N) / BW_nvlink)
+    rows_all = [giga.partition(M, world, g)[1] for g in range(world)]
+    bw_nv = 770e9  # measured NVLink peer-copy GB/s per direction (B200_PROFILING.md)
+    t_comp = 2.0 * max(rows_all) * N * K / (tf32_sustained * 1e12 / 3)
+    t_comm = 4.0 * ((K * N if world > 1 else 0) + (M - min(rows_all)) * N) / bw_nv
+    t_roof = max(t_comp, t_comm)
+    step_roof = {"definition": "T_roof / t, T_roof = max(2 r_max N K / (P_tf32/3), "
+                               "4 (KN[g>1] + (M - r_min) N) / 770 GB/s)",
+                 "t_comp_ms": round(t_comp * 1e3, 4), "t_comm_ms": round(t_comm * 1e3, 4),
+                 "bound": "tensor" if t_comp >= t_comm else "nvlink",
+                 "frac": round(t_roof / (ms_step * 1e-3), 4)}
+
     # ---- end to end: host buffers through the C ABI ----
     e2e = None
     if args.e2e_steps > 0:
@@ -303,7 +316,7 @@ def main():
             "config": {"workload": f"{args.config} M={M} N={N} K={K}", "dist": args.dist,
                        "parallelism": f"row-split x{world}",
                        "l2": "inputs larger than L2 (A, B, C 1 GiB each at c3)"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "roofline_step": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(kt["gemm_launches"] + kt["split_launches"]),
             "clocks": clk,
         }
