@@ -76,6 +76,7 @@ struct GemmParams {
   int n_kb;       // k-blocks per tile
   int m_tiles, n_tiles, num_tiles;
   int group_m;    // L2 raster: consecutive tiles walk group_m M-tiles before the next N-tile
+  unsigned *wave_sync;  // non-null: zeroed counter for the producers' per-wave barrier
 };
 
 // ---- UMMA descriptors -------------------------------------------------------------------
@@ -184,7 +185,25 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       const uint32_t tx_cta = p.terms == 3 ? T::STAGE_BYTES : (A_BYTES + T::B_BYTES);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+      int wave = 0;
+      uint32_t wave_target = 0;
+      for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++wave) {
+        if (p.wave_sync && wave > 0) {
+          // Wave barrier among the producers: start loading wave w only when every CTA that
+          // has a tile in wave w has issued all loads of wave w-1, so the clusters sharing
+          // A / B panels stay within one tile of each other and hit in L2 (unsynchronised,
+          // persistent clusters drift apart over the waves and re-fetch panels from HBM:
+          // 147 -> 35 GB of DRAM reads at 16384^3). A locality hint only, never needed for
+          // correctness: the wait gives up after 2 ms, so CTAs kept off the GPU by another
+          // kernel cannot deadlock it.
+          const int active = min(num_clusters, p.num_tiles - wave * num_clusters);
+          wave_target += uint32_t(active * CG);
+          atomicAdd(p.wave_sync, 1u);
+          const uint64_t t_start = ptx::globaltimer_ns();
+          while (ptx::ld_acquire_gpu(p.wave_sync) < wave_target &&
+                 ptx::globaltimer_ns() - t_start < 2000000ull)
+            __nanosleep(64);
+        }
         int mb, nb;
         tile_coords(t, p, mb, nb);
         const int m0 = mb * T::TILE_M + int(rank) * BM;
@@ -563,6 +582,26 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
     return (e && atoi(e) > 0) ? atoi(e) : 0;
   }();
   p.group_m = group_env ? group_env : GROUP_M;
+  p.wave_sync = nullptr;
+  static const bool wave_env = [] {  // producers' per-wave barrier; $GIGA_WAVE_SYNC=0 disables
+    const char *e = getenv("GIGA_WAVE_SYNC");
+    return !(e && *e == '0');
+  }();
+  if (wave_env && p.num_tiles > (cg == 2 ? num_sms / 2 : num_sms)) {
+    // one counter per device, zeroed on the launch stream before each launch
+    static std::mutex wmu;
+    static unsigned *wbuf[64] = {nullptr};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(wmu);
+    if (!wbuf[dev & 63]) {
+      cudaError_t e = cudaMalloc(&wbuf[dev & 63], sizeof(unsigned));
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaMemsetAsync(wbuf[dev & 63], 0, sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    p.wave_sync = wbuf[dev & 63];
+  }
 
   if (cg == 1) {
     cudaError_t e = ensure_smem_attr<1>();
