@@ -10,6 +10,8 @@ only builds/loads that library and marshals numpy arrays. It computes the plain 
     C[i, j] = sum_k A[i, k] * B[k, j]        (S4.2.7 Matrix Multiplication)
     S[i, j] = sum_k |A[i, k]| * |B[k, j]|    (scale of the north_star bound 1e-5 * S)
 
+Vector ops (dot, l2norm) follow PAPER.md:294-303 in oracle_dot.c; pins in tests/test_oracle_vec.py.
+
 Pins (tests/test_oracle.py): identity, permutation, all-ones = K, integer rank-1 closed
 form, the SPEC.md:282 worked 2x2 example (tests/golden/), exact rational brute force on
 tiny shapes, exact integer products vs numpy int64, transpose identity, row independence,
@@ -26,7 +28,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRC = os.path.join(_HERE, "oracle_gemm.c")
+_SRCS = [os.path.join(_HERE, "oracle_gemm.c"), os.path.join(_HERE, "oracle_dot.c")]
 _LIB_PATH = os.path.join(_HERE, "liboracle_gemm.so")
 _lib = None
 _lock = threading.Lock()
@@ -36,11 +38,11 @@ CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-shared", "-fPIC", "-pt
 
 def build(force: bool = False) -> str:
     """Compile oracle_gemm.c with gcc (no GPU involved). Returns the .so path."""
-    if force or not os.path.exists(_LIB_PATH) or (
-        os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC)
+    if force or not os.path.exists(_LIB_PATH) or any(
+        os.path.getmtime(_LIB_PATH) < os.path.getmtime(s) for s in _SRCS
     ):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, *_SRCS, "-lm"])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
@@ -56,6 +58,10 @@ def _load():
             lib.oracle_gemm_rows_f64.restype = ctypes.c_int
             lib.oracle_gemm_f64.argtypes = [p, p, i64, i64, i64, p, p, ctypes.c_int]
             lib.oracle_gemm_f64.restype = ctypes.c_int
+            lib.oracle_dot_f64.argtypes = [p, p, i64, p, p]
+            lib.oracle_dot_f64.restype = ctypes.c_int
+            lib.oracle_l2norm_f64.argtypes = [p, i64, p]
+            lib.oracle_l2norm_f64.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -112,3 +118,27 @@ def gemm_row_index(A, B, rows, nthreads: int | None = None, want_s: bool = True)
     if rc != 0:
         raise RuntimeError(f"oracle_gemm_rows_f64 failed rc={rc}")
     return C, S
+
+
+# ---- vector operations (S4.2.8) ------------------------
+
+def dot(x, y):
+    """(dot, sabs): sum_i x_i y_i and sum_i |x_i y_i| in fp64, ascending i (oracle_dot.c)."""
+    x, y = _f32c(x).reshape(-1), _f32c(y).reshape(-1)
+    if x.size != y.size:
+        raise ValueError(f"length mismatch {x.size} vs {y.size}")
+    d, s = ctypes.c_double(), ctypes.c_double()
+    rc = _load().oracle_dot_f64(x.ctypes.data, y.ctypes.data, x.size, ctypes.addressof(d),
+                                ctypes.addressof(s))
+    if rc != 0:
+        raise RuntimeError("oracle_dot_f64 failed")
+    return d.value, s.value
+
+
+def l2norm(x):
+    """sqrt(dot(x, x)), the square root taken once at the end."""
+    x = _f32c(x).reshape(-1)
+    r = ctypes.c_double()
+    if _load().oracle_l2norm_f64(x.ctypes.data, x.size, ctypes.addressof(r)) != 0:
+        raise RuntimeError("oracle_l2norm_f64 failed")
+    return r.value

@@ -27,11 +27,18 @@ import numpy as np
 SEED = 250401266
 MATRIX_A = 1
 MATRIX_B = 2
+VECTOR_X = 3  # dot / L2 norm operands
+VECTOR_Y = 4
 
 _GOLDEN = 0x9E3779B97F4A7C15
 _MIX1 = 0xBF58476D1CE4E5B9
 _MIX2 = 0x94D049BB133111EB
-DISTS = ("d1", "d2", "d3")
+DISTS = ("d1", "d2", "d3", "d4")
+
+
+def gen_vector(n: int, vec_id: int, dist: str = "d4", seed: int = SEED) -> np.ndarray:
+    """A length-n fp32 vector (one row of the counter-based generator)."""
+    return gen_rows(0, 1, n, vec_id, dist, seed)[0]
 
 
 def _splitmix64_np(x: np.ndarray) -> np.ndarray:
@@ -42,6 +49,9 @@ def _splitmix64_np(x: np.ndarray) -> np.ndarray:
 
 
 def _to_dist_np(v: np.ndarray, dist: str) -> np.ndarray:
+    if dist == "d4":  # uniform [-10, 10): the paper's vector benchmark values
+        return ((v.astype(np.int64) - (1 << 23)).astype(np.float64) * (10 * 2.0 ** -23)
+                ).astype(np.float32)
     if dist == "d1":
         return ((v + 1).astype(np.float64) * 2.0 ** -24).astype(np.float32)
     if dist == "d2":
@@ -115,7 +125,9 @@ def gen_rows_torch(row0: int, nrows: int, cols: int, matrix_id: int, dist: str =
         z = (z ^ _lsr(z, 27)) * _i64(_MIX2)
         z = z ^ _lsr(z, 31)
         v = _lsr(z, 40)
-        if dist == "d1":
+        if dist == "d4":
+            vals = (v - (1 << 23)).to(torch.float64) * (10 * 2.0 ** -23)
+        elif dist == "d1":
             vals = (v + 1).to(torch.float64) * 2.0 ** -24
         elif dist == "d2":
             vals = (v - (1 << 23)).to(torch.float64) * 2.0 ** -23

@@ -24,6 +24,8 @@ def test_ranges(dist):
         assert x.min() > 0 and x.max() <= 1
     elif dist == "d2":
         assert x.min() >= -1 and x.max() < 1 and abs(float(x.mean())) < 0.01
+    elif dist == "d4":
+        assert x.min() >= -10 and x.max() <= 10 and abs(float(x.mean())) < 0.1
     else:
         assert np.array_equal(x, np.round(x)) and x.min() == -8 and x.max() == 8
 
