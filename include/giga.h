@@ -124,6 +124,29 @@ int giga_rank_init(int rank, int world, int device, const uint8_t id[128]);
 int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, int64_t N,
                      int64_t K, void *stream);
 
+/* ------------------------------------------------------------------------------------ */
+/* Vector operations, the paper's second data-parallel workload (S4.2.8;
+ * SPEC.md:284-301): the index range [0, n) is split with giga_partition's rule ("halving,
+ * with remainder going on one"), every GPU reduces its range, the partials are summed.
+ * Each product of two fp32 values is formed exactly in fp64 and summed in fp64, so
+ * |result - exact| <= 2 n 2^-53 sum_i |x_i y_i|; integer-valued inputs give the exact sum.
+ * Deterministic for a given device and n. */
+
+/* *result = sum_i x[i] * y[i] on GPUs 0..ngpus-1. x, y: both HOST pointers (copied per GPU)
+ * or both DEVICE pointers on GPU 0 (ranges copied to the other GPUs over NVLink). The host
+ * sums the per-GPU partials in device order. Blocking. Errors: NOT_INITIALIZED,
+ * INVALID_ARG (NULL, n < 1, ngpus out of range, mixed pointer kinds), OOM, CUDA. */
+int giga_dot(const float *x, const float *y, int64_t n, int ngpus, double *result);
+
+/* *result = sqrt(giga_dot(x, x)): the square root once, on the host, at the end. */
+int giga_l2norm(const float *x, int64_t n, int ngpus, double *result);
+
+/* Rank API: this rank's range of x and y (device pointers, giga_partition(n, world, rank)
+ * elements); the partials are all-reduced (NCCL, fp64 sum) so every rank's *result (host)
+ * holds the full dot. Enqueued on `stream`, then synchronised. Errors as giga_matmul_rank. */
+int giga_dot_rank(const float *x_shard, const float *y_shard, int64_t n, double *result,
+                  void *stream);
+
 /* The N > 1 pipeline's chunk plan (pure host arithmetic, identical on every rank; the
  * orchestration of giga_matmul_sharded / giga_matmul_rank uses exactly these functions).
  * B is broadcast from rank 0 in *kchunks K-row chunks [kbounds[c], kbounds[c+1]) (kbounds

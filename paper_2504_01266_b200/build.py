@@ -17,7 +17,7 @@ DEBUG_LIB = os.path.join(HERE, "libgiga_debug.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["gemm_3xtf32.cu"]
+CU_SOURCES = ["gemm_3xtf32.cu", "vecops.cu"]
 CPP_SOURCES = ["api.cpp", "nccl_loader.cpp"]
 HEADERS = ["ptx.cuh", "kernels.h", "nccl_loader.h", "debug_kernels.cu"]
 

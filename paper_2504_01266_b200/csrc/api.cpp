@@ -5,6 +5,7 @@
 #include "giga.h"
 
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -75,6 +76,7 @@ struct DevCtx {
   std::vector<cudaEvent_t> ev_kchunk;  // pipeline: B K-chunk c present
   std::vector<cudaEvent_t> ev_rchunk;  // pipeline: C row-chunk q computed
   Buf A_lo, B_lo, A_pad, B_pad, C_pad, A_h, B_h, C_h;
+  Buf vec_ws;  // dot: kDotMaxBlocks fp64 partials, the fp64 result, the ticket (zeroed once)
 };
 
 struct State {
@@ -177,7 +179,8 @@ int ws_reserve(DevCtx &d, std::initializer_list<std::pair<Buf *, size_t>> req) {
 }
 
 void ws_free(DevCtx &d) {
-  for (Buf *b : {&d.A_lo, &d.B_lo, &d.A_pad, &d.B_pad, &d.C_pad, &d.A_h, &d.B_h, &d.C_h}) {
+  for (Buf *b :
+       {&d.A_lo, &d.B_lo, &d.A_pad, &d.B_pad, &d.C_pad, &d.A_h, &d.B_h, &d.C_h, &d.vec_ws}) {
     if (b->p) cudaFree(b->p);
     b->p = nullptr;
     b->bytes = 0;
@@ -379,6 +382,27 @@ int quiesce(int ngpus) {
     CK(cudaSetDevice(g.devs[i].dev));
     CK(cudaDeviceSynchronize());
   }
+  return GIGA_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// vector operations: per-GPU fp64 partial of a contiguous index range
+
+constexpr size_t kVecWsBytes = size_t(kDotMaxBlocks) * 8 + 64;
+
+int vec_ws(DevCtx &d) {
+  if (d.vec_ws.p) return GIGA_OK;
+  TRY(ws_reserve(d, {{&d.vec_ws, kVecWsBytes}}));
+  CK(cudaMemset(d.vec_ws.p, 0, kVecWsBytes));  // ticket starts at zero
+  return GIGA_OK;
+}
+double *vec_partials(DevCtx &d) { return static_cast<double *>(d.vec_ws.p); }
+double *vec_out(DevCtx &d) { return vec_partials(d) + kDotMaxBlocks; }
+unsigned *vec_ticket(DevCtx &d) { return reinterpret_cast<unsigned *>(vec_out(d) + 1); }
+
+int dot_partial(DevCtx &d, const float *x, const float *y, int64_t n, cudaStream_t st) {
+  TRY(vec_ws(d));
+  CK(launch_dot(x, y, n, vec_partials(d), vec_ticket(d), vec_out(d), st));
   return GIGA_OK;
 }
 
@@ -966,6 +990,95 @@ int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, i
     return shard_compute(d, st, A_shard, rows, B, C_full + r0 * N, N, N, K, nullptr);
   std::vector<Part> parts{{&d, g.rank_comm, g.rank, A_shard, B, C_full, st}};
   return run_pipeline(parts, g.world, M, N, K);
+}
+
+// ---- vector operations -------------------------------------------------
+
+int giga_dot(const float *x, const float *y, int64_t n, int ngpus, double *result) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.mode != 1) return fail(GIGA_ERR_NOT_INITIALIZED, "giga_dot: call giga_init first");
+  if (!x || !y || !result || n < 1)
+    return fail(GIGA_ERR_INVALID_ARG, "giga_dot: NULL pointer or n < 1");
+  if (ngpus < 1 || ngpus > int(g.devs.size()))
+    return fail(GIGA_ERR_INVALID_ARG, "ngpus=%d outside [1, %d]", ngpus, int(g.devs.size()));
+  int dx = -1, dy = -1;
+  const int kx = pointer_kind(x, &dx), ky = pointer_kind(y, &dy);
+  if (kx != ky) return fail(GIGA_ERR_INVALID_ARG, "x, y must be both host or both device");
+  const bool device = kx == 1;
+  if (device && (dx != g.devs[0].dev || dy != g.devs[0].dev))
+    return fail(GIGA_ERR_INVALID_ARG, "device pointers must live on GPU %d", g.devs[0].dev);
+  TRY(quiesce(ngpus));
+  // "halving, with remainder going on one", generalised: giga_partition's rule
+  for (int i = 0; i < ngpus; ++i) {
+    DevCtx &d = g.devs[i];
+    CK(cudaSetDevice(d.dev));
+    int64_t r0, rows;
+    partition_rows(n, ngpus, i, &r0, &rows);
+    TRY(vec_ws(d));
+    if (device && ngpus == 1) {
+      TRY(dot_partial(d, x, y, rows, d.compute));
+      continue;
+    }
+    TRY(ws_reserve(d, {{&d.A_h, size_t(std::max<int64_t>(rows, 1)) * 4},
+                       {&d.B_h, size_t(std::max<int64_t>(rows, 1)) * 4}}));
+    if (rows > 0) {
+      if (device) {
+        CK(cudaMemcpyPeerAsync(d.A_h.p, d.dev, x + r0, g.devs[0].dev, size_t(rows) * 4,
+                               d.compute));
+        CK(cudaMemcpyPeerAsync(d.B_h.p, d.dev, y + r0, g.devs[0].dev, size_t(rows) * 4,
+                               d.compute));
+      } else {
+        CK(cudaMemcpyAsync(d.A_h.p, x + r0, size_t(rows) * 4, cudaMemcpyHostToDevice,
+                           d.compute));
+        CK(cudaMemcpyAsync(d.B_h.p, y + r0, size_t(rows) * 4, cudaMemcpyHostToDevice,
+                           d.compute));
+      }
+    }
+    TRY(dot_partial(d, fptr(d.A_h), fptr(d.B_h), rows, d.compute));
+  }
+  // the host sums the per-GPU partials in device order, in fp64
+  double total = 0.0;
+  for (int i = 0; i < ngpus; ++i) {
+    DevCtx &d = g.devs[i];
+    CK(cudaSetDevice(d.dev));
+    double part = 0.0;
+    CK(cudaMemcpyAsync(&part, vec_out(d), sizeof(double), cudaMemcpyDeviceToHost, d.compute));
+    CK(cudaStreamSynchronize(d.compute));
+    total += part;
+  }
+  *result = total;
+  return GIGA_OK;
+}
+
+int giga_l2norm(const float *x, int64_t n, int ngpus, double *result) {
+  double d2 = 0.0;
+  TRY(giga_dot(x, x, n, ngpus, &d2));
+  *result = sqrt(d2);  // once, on the host, after the reduction
+  return GIGA_OK;
+}
+
+int giga_dot_rank(const float *x_shard, const float *y_shard, int64_t n, double *result,
+                  void *stream) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.mode != 2) return fail(GIGA_ERR_NOT_INITIALIZED, "giga_dot_rank: not initialised");
+  int64_t r0, rows;
+  if (n < 1) return fail(GIGA_ERR_INVALID_ARG, "giga_dot_rank: n < 1");
+  partition_rows(n, g.world, g.rank, &r0, &rows);
+  if (!result || (rows > 0 && (!x_shard || !y_shard)))
+    return fail(GIGA_ERR_INVALID_ARG, "giga_dot_rank: NULL pointer");
+  DevCtx &d = g.devs[0];
+  CK(cudaSetDevice(d.dev));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.compute;
+  TRY(dot_partial(d, x_shard, y_shard, rows, st));
+  if (g.rank_comm) {  // every rank gets the sum of the partials
+    const NcclApi *api = nccl_api(nullptr);
+    TRY(nccl_check(api->AllReduce(vec_out(d), vec_out(d), 1, ncclFloat64, ncclSum, g.rank_comm,
+                                  st),
+                   "ncclAllReduce(dot)"));
+  }
+  CK(cudaMemcpyAsync(result, vec_out(d), sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return GIGA_OK;
 }
 
 // ---- pipeline plan (host arithmetic) -----------------------------------------------------

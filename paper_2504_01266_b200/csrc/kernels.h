@@ -34,6 +34,13 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
                                int64_t ldc, int terms, int promote_kblocks, cudaStream_t st,
                                int cta_group = 0, const GemmExtra *ex = nullptr);
 
+// out[0] = sum_i x[i]*y[i] over n elements, fp64 accumulation (vecops.cu). `partials` must
+// hold kDotMaxBlocks doubles and `ticket` must be zero before the first launch (the kernel
+// resets it). Deterministic for a given device.
+constexpr int kDotMaxBlocks = 2048;
+cudaError_t launch_dot(const float *x, const float *y, int64_t n, double *partials,
+                       unsigned *ticket, double *out, cudaStream_t st);
+
 // Resolves cuTensorMapEncodeTiled through the runtime (no libcuda link). 0 on success.
 int ensure_tma_encoder();
 

@@ -36,6 +36,7 @@ const NcclApi *nccl_api(const char **why) {
               sym(h, "ncclCommGetAsyncError", g_api.CommGetAsyncError) &&
               sym(h, "ncclBroadcast", g_api.Broadcast) &&
               sym(h, "ncclAllGather", g_api.AllGather) &&
+              sym(h, "ncclAllReduce", g_api.AllReduce) &&
               sym(h, "ncclGroupStart", g_api.GroupStart) &&
               sym(h, "ncclGroupEnd", g_api.GroupEnd) &&
               sym(h, "ncclGetErrorString", g_api.GetErrorString);

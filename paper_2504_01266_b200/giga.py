@@ -26,7 +26,7 @@ EXPORTS = (
     "giga_matmul_sharded", "giga_last_error", "giga_comm_unique_id", "giga_rank_init",
     "giga_matmul_rank", "giga_split_lo", "giga_gemm_3xtf32", "giga_gemm_3xtf32_ex",
     "giga_timing_enable", "giga_timing_reset", "giga_timing_read", "giga_pipeline_plan",
-    "giga_plan_block",
+    "giga_plan_block", "giga_dot", "giga_l2norm", "giga_dot_rank",
 )
 
 
@@ -71,6 +71,9 @@ def _load():
         "giga_pipeline_plan": ([i64, i64, i64, i32, ctypes.POINTER(i32), P64,
                                 ctypes.POINTER(i32)], i32),
         "giga_plan_block": ([i64, i32, i32, i32, i32, P64, P64], i32),
+        "giga_dot": ([p, p, i64, i32, ctypes.POINTER(ctypes.c_double)], i32),
+        "giga_l2norm": ([p, i64, i32, ctypes.POINTER(ctypes.c_double)], i32),
+        "giga_dot_rank": ([p, p, i64, ctypes.POINTER(ctypes.c_double), p], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -167,6 +170,27 @@ def rank_init(rank: int, world: int, device: int, uid: bytes | None):
 
 def matmul_rank(A_shard, B, C_full, M: int, N: int, K: int, stream=None):
     _check(lib.giga_matmul_rank(_ptr(A_shard), _ptr(B), _ptr(C_full), M, N, K, _stream(stream)))
+
+
+def dot(x, y, n: int | None = None, ngpus: int = 1) -> float:
+    """giga_dot: x, y both host (numpy / torch CPU) or both device (GPU 0)."""
+    n = (x.size if isinstance(x, np.ndarray) else x.numel()) if n is None else n
+    r = ctypes.c_double()
+    _check(lib.giga_dot(_ptr(x), _ptr(y), n, ngpus, ctypes.byref(r)))
+    return r.value
+
+
+def l2norm(x, n: int | None = None, ngpus: int = 1) -> float:
+    n = (x.size if isinstance(x, np.ndarray) else x.numel()) if n is None else n
+    r = ctypes.c_double()
+    _check(lib.giga_l2norm(_ptr(x), n, ngpus, ctypes.byref(r)))
+    return r.value
+
+
+def dot_rank(x_shard, y_shard, n: int, stream=None) -> float:
+    r = ctypes.c_double()
+    _check(lib.giga_dot_rank(_ptr(x_shard), _ptr(y_shard), n, ctypes.byref(r), _stream(stream)))
+    return r.value
 
 
 def pipeline_plan(M: int, N: int, K: int, world: int):
