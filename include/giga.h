@@ -67,6 +67,14 @@ enum giga_status {
  * (fewer than n sm_100 GPUs), CUDA. */
 int giga_init(int ngpus_max);
 
+/* As giga_init on an explicit list of CUDA ordinals: library GPU g runs on devices[g].
+ * Ordinals may repeat: several "virtual GPUs" then share one device, each with its own
+ * streams and workspace, and the multi-GPU schedules run unchanged with device-local copies
+ * (how the N > 1 paths are exercised on a one-GPU machine). NCCL refuses repeated devices,
+ * so with repeats only $GIGA_TRANSPORT=p2p serves ngpus > 1. Errors: as giga_init,
+ * INVALID_ARG (NULL / n < 1). */
+int giga_init_devices(const int *devices, int n);
+
 /* Number of GPUs the library was initialised with (0 if not initialised). */
 int giga_num_devices(void);
 
@@ -91,7 +99,11 @@ int giga_partition(int64_t M, int ngpus, int g, int64_t *row0, int64_t *rows);
 int giga_matmul(const float *A, const float *B, float *C, int64_t M, int64_t N, int64_t K,
                 int ngpus);
 
-/* Device-resident, pre-sharded hot path (what bench.py times).
+/* Device-resident, pre-sharded hot path (what bench.py times). Transport for ngpus > 1
+ * ($GIGA_TRANSPORT): "nccl" (default) = NCCL broadcast of B in K-chunks overlapped with
+ * accumulating GEMMs + row-chunked NCCL gather of C; "p2p" = copy-engine chain broadcast of B
+ * (no SMs) + the gather fused into the GEMM epilogue (TMA stores of every C tile into every
+ * GPU's C_full over NVLink).
  * A_shard[g]: device pointer on GPU g to the rows_g x K block of A (giga_partition rule).
  * B_buf[0]:   device pointer on GPU 0 holding B (K x N). B_buf[g>0]: K x N receive buffers
  *             on GPU g, overwritten with B.

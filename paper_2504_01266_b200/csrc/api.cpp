@@ -620,6 +620,94 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
   return GIGA_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// Peer-to-peer transport (single process, $GIGA_TRANSPORT=p2p): no NCCL, no SMs spent on
+// communication.
+//   B: a pipelined chain of copy-engine transfers in the plan's K-chunks: GPU i pulls chunk c
+//      from GPU i-1 as soon as GPU i-1 has it (each GPU's ingress and egress = one copy of B;
+//      latency (pb + g - 2) chunk times); GPU i's GEMM on chunk c starts when it lands.
+//   C: the gather is fused into the GEMM epilogue: every 32 x 32 block of a GPU's rows is
+//      TMA-stored into its own C_full and into every peer's C_full (NVLink writes), tile by
+//      tile while the tensor cores work on the next tile.
+//   Completion: each GPU's stream waits for every GPU's last GEMM.
+// The devices may repeat (giga_init_devices): "virtual GPUs" on one device run exactly this
+// schedule with device-local copies and stores, which is how it is tested on a 1-GPU box.
+
+bool transport_p2p() {
+  const char *e = getenv("GIGA_TRANSPORT");
+  return e && strcmp(e, "p2p") == 0;
+}
+
+int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K) {
+  const int world = int(parts.size());
+  if (world > kMaxCDst)
+    return fail(GIGA_ERR_UNSUPPORTED, "p2p transport: at most %d GPUs", kMaxCDst);
+  bool aligned = (K % 4 == 0) && (N % 4 == 0);
+  for (auto &p : parts) aligned = aligned && aligned16(p.A) && aligned16(p.B) && aligned16(p.C);
+  if (!aligned)
+    return fail(GIGA_ERR_UNSUPPORTED, "p2p transport needs K %% 4 == N %% 4 == 0, aligned");
+  const Plan plan = make_plan(M, K, world, true);
+  // 0. join the callers' streams, workspace, split A
+  for (auto &p : parts) {
+    CK(cudaSetDevice(p.d->dev));
+    CK(cudaEventRecord(p.d->ev_start, p.st));
+    CK(cudaStreamWaitEvent(p.d->comm, p.d->ev_start, 0));
+    int64_t r0, rows;
+    partition_rows(M, world, p.rank, &r0, &rows);
+    TRY(ws_reserve(*p.d, {{&p.d->A_lo, size_t(std::max<int64_t>(rows, 1) * K) * 4},
+                          {&p.d->B_lo, size_t(K * N) * 4}}));
+    if (rows > 0) TRY(split(p.A, fptr(p.d->A_lo), rows * K, p.st));
+  }
+  // 1. B down the chain, chunk by chunk (copy engines)
+  for (int c = 0; c < plan.pb; ++c) {
+    const int64_t off = plan.kb[c] * N, cnt = (plan.kb[c + 1] - plan.kb[c]) * N;
+    for (int i = 0; i < world; ++i) {
+      Part &p = parts[i];
+      CK(cudaSetDevice(p.d->dev));
+      if (i > 0) {
+        Part &up = parts[i - 1];
+        CK(cudaStreamWaitEvent(p.d->comm, up.d->ev_kchunk[c], 0));
+        CK(cudaMemcpyPeerAsync(p.B + off, p.d->dev, up.B + off, up.d->dev, size_t(cnt) * 4,
+                               p.d->comm));
+      }
+      CK(cudaEventRecord(p.d->ev_kchunk[c], p.d->comm));
+    }
+  }
+  // 2. GEMMs over the K-chunks; every tile also goes to the peers' C_full
+  GemmExtra ex;
+  ex.lda = K;
+  ex.ldb = N;
+  for (auto &p : parts) {
+    CK(cudaSetDevice(p.d->dev));
+    int64_t r0, rows;
+    partition_rows(M, world, p.rank, &r0, &rows);
+    float *peer[kMaxCDst];
+    int np = 0;
+    for (auto &q : parts)
+      if (&q != &p) peer[np++] = q.C + r0 * N;
+    ex.peer_c = peer;
+    ex.n_peer_c = np;
+    for (int c = 0; c < plan.pb; ++c) {
+      const int64_t Kc = plan.kb[c + 1] - plan.kb[c];
+      CK(cudaStreamWaitEvent(p.st, p.d->ev_kchunk[c], 0));
+      TRY(split(p.B + plan.kb[c] * N, fptr(p.d->B_lo) + plan.kb[c] * N, Kc * N, p.st));
+      if (rows == 0) continue;
+      GemmExtra e = ex;
+      e.accumulate = c > 0;
+      TRY(gemm_chunk(p.A + plan.kb[c], fptr(p.d->A_lo) + plan.kb[c], p.B + plan.kb[c] * N,
+                     fptr(p.d->B_lo) + plan.kb[c] * N, p.C + r0 * N, rows, N, Kc, e, p.st));
+    }
+    CK(cudaEventRecord(p.d->ev_c, p.st));
+  }
+  // 3. a GPU's C_full is complete when every GPU's GEMMs are
+  for (auto &p : parts) {
+    CK(cudaSetDevice(p.d->dev));
+    for (auto &q : parts)
+      if (&q != &p) CK(cudaStreamWaitEvent(p.st, q.d->ev_c, 0));
+  }
+  return GIGA_OK;
+}
+
 // Device-resident path on GPUs 0..ngpus-1 (B_buf[0] root, C_full[g] all receive full C).
 int sharded_locked(const float *const *A_shard, float *const *B_buf, float *const *C_full,
                    int64_t M, int64_t N, int64_t K, int ngpus) {
@@ -628,6 +716,14 @@ int sharded_locked(const float *const *A_shard, float *const *B_buf, float *cons
     CK(cudaSetDevice(d.dev));
     TRY(shard_compute(d, d.compute, A_shard[0], M, B_buf[0], C_full[0], N, N, K, nullptr));
     return sync_all(1);
+  }
+  if (transport_p2p()) {
+    std::vector<Part> parts;
+    for (int i = 0; i < ngpus; ++i)
+      parts.push_back({&g.devs[i], nullptr, i, A_shard[i], B_buf[i], C_full[i],
+                       g.devs[i].compute});
+    TRY(run_p2p(parts, M, N, K));
+    return sync_all(ngpus);
   }
   std::vector<ncclComm_t> *comms = nullptr;
   TRY(get_comms(ngpus, &comms));
@@ -777,6 +873,37 @@ int matmul_locked(const float *A, const float *B, float *C, int64_t M, int64_t N
   return sync_all(ngpus);
 }
 
+// Library state for the single-process API on the given CUDA ordinals (repeats allowed).
+int init_devices_locked(const std::vector<int> &devs) {
+  const int n = int(devs.size());
+  for (int i = 0; i < n; ++i) TRY(check_sm100(devs[i]));
+  if (ensure_tma_encoder() != 0)
+    return fail(GIGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  g.devs.assign(n, DevCtx{});
+  for (int i = 0; i < n; ++i) {
+    int rc = ctx_create(g.devs[i], devs[i]);
+    if (rc != GIGA_OK) {
+      for (auto &d : g.devs) ctx_destroy(d);
+      g.devs.clear();
+      return rc;
+    }
+  }
+  // peer access so NCCL / copies / epilogue stores use NVLink directly (best effort)
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      if (devs[i] == devs[j]) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, devs[i], devs[j]);
+      if (can) {
+        cudaSetDevice(devs[i]);
+        cudaDeviceEnablePeerAccess(devs[j], 0);
+        cudaGetLastError();
+      }
+    }
+  g.mode = 1;
+  return GIGA_OK;
+}
+
 }  // namespace
 }  // namespace giga
 
@@ -812,32 +939,25 @@ int giga_init(int ngpus_max) {
   const int n = ngpus_max <= 0 ? count : ngpus_max;
   if (n > count)
     return fail(GIGA_ERR_NO_DEVICE, "asked for %d GPUs, %d visible", ngpus_max, count);
-  for (int i = 0; i < n; ++i) TRY(check_sm100(i));
-  if (ensure_tma_encoder() != 0)
-    return fail(GIGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-  g.devs.assign(n, DevCtx{});
-  for (int i = 0; i < n; ++i) {
-    int rc = ctx_create(g.devs[i], i);
-    if (rc != GIGA_OK) {
-      for (auto &d : g.devs) ctx_destroy(d);
-      g.devs.clear();
-      return rc;
-    }
+  std::vector<int> devs(n);
+  for (int i = 0; i < n; ++i) devs[i] = i;
+  return init_devices_locked(devs);
+}
+
+int giga_init_devices(const int *devices, int n) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.mode != 0)
+    return fail(GIGA_ERR_ALREADY_INITIALIZED, "giga_init_devices: already initialised");
+  if (!devices || n < 1) return fail(GIGA_ERR_INVALID_ARG, "giga_init_devices: empty list");
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(GIGA_ERR_NO_DEVICE, "no CUDA device visible");
   }
-  // peer access so NCCL / copies can use NVLink directly (best effort)
   for (int i = 0; i < n; ++i)
-    for (int j = 0; j < n; ++j) {
-      if (i == j) continue;
-      int can = 0;
-      cudaDeviceCanAccessPeer(&can, i, j);
-      if (can) {
-        cudaSetDevice(i);
-        cudaDeviceEnablePeerAccess(j, 0);
-        cudaGetLastError();
-      }
-    }
-  g.mode = 1;
-  return GIGA_OK;
+    if (devices[i] < 0 || devices[i] >= count)
+      return fail(GIGA_ERR_NO_DEVICE, "device %d not visible", devices[i]);
+  return init_devices_locked(std::vector<int>(devices, devices + n));
 }
 
 int giga_finalize(void) {

@@ -77,6 +77,12 @@ struct GemmParams {
   int m_tiles, n_tiles, num_tiles;
   int group_m;    // L2 raster: consecutive tiles walk group_m M-tiles before the next N-tile
   unsigned *wave_sync;  // non-null: zeroed counter for the producers' per-wave barrier
+  int n_cdst;     // C destinations in CMaps (1 + peers when the gather is fused)
+};
+
+// C tensor maps: [0] this GPU's C, [1..] the same rows of the peers' C_full buffers.
+struct CMaps {
+  CUtensorMap m[kMaxCDst];
 };
 
 // ---- UMMA descriptors -------------------------------------------------------------------
@@ -125,7 +131,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
                        const __grid_constant__ CUtensorMap tmAlo,
                        const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmBlo,
-                       const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
+                       const __grid_constant__ CMaps cmaps, const GemmParams p) {
   using namespace cfg;
   using T = Tile<CG>;
   constexpr int STAGES = T::STAGES;
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       ptx::prefetch_tmap(&tmAlo);
       ptx::prefetch_tmap(&tmBlo);
     }
-    ptx::prefetch_tmap(&tmC);
+    for (int dst = 0; dst < p.n_cdst; ++dst) ptx::prefetch_tmap(&cmaps.m[dst]);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -369,10 +375,16 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (p.accumulate)
-            ptx::tma_store_add_2d(&tmC, epi_stage + e * EPI_STAGE_BYTES, ccol0 + 32 * c, crow0);
-          else
-            ptx::tma_store_2d(&tmC, epi_stage + e * EPI_STAGE_BYTES, ccol0 + 32 * c, crow0);
+          // every destination C buffer (this GPU's, then the peers' when the gather is fused
+          // into the epilogue: the same rows land in every GPU's C_full over NVLink)
+          for (int dst = 0; dst < p.n_cdst; ++dst) {
+            if (p.accumulate)
+              ptx::tma_store_add_2d(&cmaps.m[dst], epi_stage + e * EPI_STAGE_BYTES,
+                                    ccol0 + 32 * c, crow0);
+            else
+              ptx::tma_store_2d(&cmaps.m[dst], epi_stage + e * EPI_STAGE_BYTES, ccol0 + 32 * c,
+                                crow0);
+          }
           ptx::bulk_commit();
         }
       }
@@ -549,11 +561,16 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   if (ex->max_ctas > 0 && ex->max_ctas < num_sms) num_sms = ex->max_ctas & ~1;
   if (num_sms < 2) num_sms = 2;
   const int cg = (cta_group == 1 || cta_group == 2) ? cta_group : choose_cta_group(M, N, num_sms);
-  CUtensorMap tA, tAlo, tB, tBlo, tC;
+  CUtensorMap tA, tAlo, tB, tBlo;
+  CMaps tC;
+  if (ex->n_peer_c < 0 || ex->n_peer_c > kMaxCDst - 1) return cudaErrorInvalidValue;
   if (!make_map(&tA, A, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
       !make_map(&tB, B, N, K, ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
-      !make_map(&tC, C, N, M, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+      !make_map(&tC.m[0], C, N, M, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
+  for (int i = 0; i < ex->n_peer_c; ++i)
+    if (!make_map(&tC.m[1 + i], ex->peer_c[i], N, M, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
   if (terms == 3) {
     if (!make_map(&tAlo, A_lo, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
         !make_map(&tBlo, B_lo, N, K, ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
@@ -583,6 +600,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   }();
   p.group_m = group_env ? group_env : GROUP_M;
   p.wave_sync = nullptr;
+  p.n_cdst = 1 + ex->n_peer_c;
   static const bool wave_env = [] {  // producers' per-wave barrier; $GIGA_WAVE_SYNC=0 disables
     const char *e = getenv("GIGA_WAVE_SYNC");
     return !(e && *e == '0');

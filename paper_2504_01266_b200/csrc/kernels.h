@@ -23,11 +23,16 @@ cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t s
 // Extra operand/launch options: lda / ldb = row strides of A and B in elements (0 = K and
 // N, i.e. dense; K-chunked pipelines pass A + k0 with lda = the full K); accumulate = 1 adds
 // into C (C += A*B, fp32 RN) instead of overwriting; max_ctas caps the persistent grid (SMs
-// left free for concurrent communication kernels; 0 = all SMs).
+// left free for concurrent communication kernels; 0 = all SMs); peer_c[0..n_peer_c) are
+// further C buffers (same shape and ldc, e.g. the peers' C_full rows over NVLink) that receive
+// the same tiles from the epilogue: the gather fused into the GEMM.
+constexpr int kMaxCDst = 8;
 struct GemmExtra {
   int64_t lda = 0, ldb = 0;
   int accumulate = 0;
   int max_ctas = 0;
+  float *const *peer_c = nullptr;
+  int n_peer_c = 0;
 };
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
                                const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,

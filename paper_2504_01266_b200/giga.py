@@ -26,7 +26,7 @@ EXPORTS = (
     "giga_matmul_sharded", "giga_last_error", "giga_comm_unique_id", "giga_rank_init",
     "giga_matmul_rank", "giga_split_lo", "giga_gemm_3xtf32", "giga_gemm_3xtf32_ex",
     "giga_timing_enable", "giga_timing_reset", "giga_timing_read", "giga_pipeline_plan",
-    "giga_plan_block", "giga_dot", "giga_l2norm", "giga_dot_rank",
+    "giga_plan_block", "giga_dot", "giga_l2norm", "giga_dot_rank", "giga_init_devices",
 )
 
 
@@ -74,6 +74,7 @@ def _load():
         "giga_dot": ([p, p, i64, i32, ctypes.POINTER(ctypes.c_double)], i32),
         "giga_l2norm": ([p, i64, i32, ctypes.POINTER(ctypes.c_double)], i32),
         "giga_dot_rank": ([p, p, i64, ctypes.POINTER(ctypes.c_double), p], i32),
+        "giga_init_devices": ([p, i32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -123,6 +124,12 @@ def _stream(stream):
 
 def init(ngpus_max: int = 0):
     _check(lib.giga_init(ngpus_max))
+
+
+def init_devices(devices):
+    """giga_init_devices: library GPU g on CUDA device devices[g] (repeats allowed)."""
+    arr = (ctypes.c_int * len(devices))(*devices)
+    _check(lib.giga_init_devices(ctypes.cast(arr, ctypes.c_void_p), len(devices)))
 
 
 def num_devices() -> int:

@@ -1,0 +1,98 @@
+"""Multi-GPU schedules on "virtual GPUs": giga_init_devices([0, 0, ...]) gives several library
+GPUs on one device, each with its own streams, workspace and buffers, so the N > 1 code paths
+run unchanged on a one-GPU box (copies become device-local). NCCL refuses repeated devices, so
+these exercise the peer-to-peer transport (copy-engine chain broadcast of B + the gather fused
+into the GEMM epilogue) and the host-summed dot; the NCCL pipeline itself is covered at world
+size 1 in test_gpu.py (GIGA_FORCE_COMM) and by the gloo schedule tests.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle.check import check_close, check_exact
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+@pytest.fixture
+def giga_virtual(torch_cuda):
+    from paper_2504_01266_b200 import build
+    build.build()
+    from paper_2504_01266_b200 import giga as g
+    made = []
+
+    def make(n):
+        g.finalize()
+        g.init_devices([0] * n)
+        made.append(n)
+        return g
+
+    yield make
+    g.finalize()
+
+
+def _shards(torch, A, world, giga):
+    out = []
+    for r in range(world):
+        r0, rows = giga.partition(A.shape[0], world, r)
+        out.append(torch.from_numpy(np.ascontiguousarray(A[r0:r0 + rows])).cuda()
+                   if rows else torch.empty(0, device="cuda"))
+    return out
+
+
+@pytest.mark.parametrize("world,M,N,K,dist", [(2, 1000, 520, 1040, "d3"), (3, 1031, 256, 2064, "d3"),
+                                               (4, 4096, 1024, 2048, "d1"), (2, 3, 8, 520, "d3"),
+                                               (8, 2048, 512, 1024, "d2")])
+def test_p2p_transport_fused_gather(giga_virtual, torch_cuda, monkeypatch, world, M, N, K, dist):
+    torch = torch_cuda
+    monkeypatch.setenv("GIGA_TRANSPORT", "p2p")
+    monkeypatch.setenv("GIGA_BCAST_CHUNKS", "3")
+    giga = giga_virtual(world)
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, dist)
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
+    A_sh = _shards(torch, A, world, giga)
+    B_bufs = [torch.from_numpy(B).cuda()] + [torch.full((K, N), float("nan"), device="cuda")
+                                             for _ in range(world - 1)]
+    C_full = [torch.full((M, N), float("nan"), device="cuda") for _ in range(world)]
+    giga.matmul_sharded(A_sh, B_bufs, C_full, M, N, K)
+    Cref, S = oracle.gemm(A, B)
+    for r in range(world):
+        assert torch.equal(B_bufs[r], B_bufs[0]), f"B not distributed to rank {r}"
+        C = C_full[r].cpu().numpy()
+        ok, st = check_exact(C, Cref) if dist == "d3" else check_close(C, Cref, S)
+        assert ok, (r, st)
+    # every rank's copy is identical (one writer per block, same bits everywhere)
+    for r in range(1, world):
+        assert torch.equal(C_full[r], C_full[0])
+
+
+def test_nccl_with_repeated_devices_is_refused(giga_virtual, torch_cuda, monkeypatch):
+    torch = torch_cuda
+    monkeypatch.setenv("GIGA_TRANSPORT", "nccl")
+    giga = giga_virtual(2)
+    M = N = K = 64
+    A = torch.ones(M, K, device="cuda")
+    bufs = [torch.ones(K, N, device="cuda"), torch.empty(K, N, device="cuda")]
+    C = [torch.empty(M, N, device="cuda") for _ in range(2)]
+    with pytest.raises(giga.GigaError) as e:
+        giga.matmul_sharded([A[:32].contiguous(), A[32:].contiguous()], bufs, C, M, N, K)
+    assert e.value.status == "GIGA_ERR_COMM"
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_dot_over_virtual_gpus(giga_virtual, torch_cuda, world):
+    giga = giga_virtual(world)
+    n = (1 << 21) + 13
+    x = synth.gen_vector(n, synth.VECTOR_X, "d3")
+    y = synth.gen_vector(n, synth.VECTOR_Y, "d3")
+    assert giga.dot(x, y, ngpus=world) == oracle.dot(x, y)[0]
+    xd, yd = torch_cuda.from_numpy(x).cuda(), torch_cuda.from_numpy(y).cuda()
+    assert giga.dot(xd, yd, ngpus=world) == oracle.dot(x, y)[0]
