@@ -171,6 +171,22 @@ int giga_pipeline_plan(int64_t M, int64_t N, int64_t K, int world, int *kchunks,
 int giga_plan_block(int64_t M, int world, int rchunks, int owner, int q, int64_t *row0,
                     int64_t *rows);
 
+/* Peer-to-peer transport for the rank API ($GIGA_TRANSPORT=p2p, set before giga_rank_init;
+ * no NCCL communicator is created then, and several ranks may share one device). Each rank
+ * registers the B and C_full buffers it will pass to giga_matmul_rank:
+ *   giga_rank_p2p_export fills GIGA_P2P_BLOB_BYTES bytes (CUDA IPC handles of B, C_full and a
+ *   library flag page); the caller all-gathers the blobs (any channel, e.g.
+ *   torch.distributed) into world * GIGA_P2P_BLOB_BYTES bytes ordered by rank and passes them
+ *   to giga_rank_p2p_import on every rank.
+ * giga_matmul_rank then pulls B down a rank chain in K-chunks with copy engines and writes
+ * each rank's C rows straight into every rank's C_full from the GEMM epilogue, ordered across
+ * processes by device-side flags (no host synchronisation); giga_dot_rank all-reduces through
+ * the flag pages. Errors: NOT_INITIALIZED, INVALID_ARG (not device allocations / wrong
+ * world), UNSUPPORTED, CUDA. */
+#define GIGA_P2P_BLOB_BYTES 256
+int giga_rank_p2p_export(const float *B, float *C_full, uint8_t *blob);
+int giga_rank_p2p_import(const uint8_t *blobs, int world);
+
 /* ------------------------------------------------------------------------------------ */
 /* Single-device building blocks (device pointers on the current CUDA device; work is
  * enqueued on `stream`, a cudaStream_t, 0 = legacy default stream; no host sync). They do

@@ -27,7 +27,9 @@ EXPORTS = (
     "giga_matmul_rank", "giga_split_lo", "giga_gemm_3xtf32", "giga_gemm_3xtf32_ex",
     "giga_timing_enable", "giga_timing_reset", "giga_timing_read", "giga_pipeline_plan",
     "giga_plan_block", "giga_dot", "giga_l2norm", "giga_dot_rank", "giga_init_devices",
+    "giga_rank_p2p_export", "giga_rank_p2p_import",
 )
+P2P_BLOB_BYTES = 256
 
 
 class GigaError(RuntimeError):
@@ -75,6 +77,8 @@ def _load():
         "giga_l2norm": ([p, i64, i32, ctypes.POINTER(ctypes.c_double)], i32),
         "giga_dot_rank": ([p, p, i64, ctypes.POINTER(ctypes.c_double), p], i32),
         "giga_init_devices": ([p, i32], i32),
+        "giga_rank_p2p_export": ([p, p, p], i32),
+        "giga_rank_p2p_import": ([p, i32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -173,6 +177,20 @@ def rank_init(rank: int, world: int, device: int, uid: bytes | None):
     buf = (ctypes.c_uint8 * 128)(*uid) if uid is not None else None
     _check(lib.giga_rank_init(rank, world, device,
                               ctypes.cast(buf, ctypes.c_void_p) if buf is not None else None))
+
+
+def p2p_export(B, C_full) -> bytes:
+    """giga_rank_p2p_export: this rank's registration blob (CUDA IPC handles)."""
+    buf = (ctypes.c_uint8 * P2P_BLOB_BYTES)()
+    _check(lib.giga_rank_p2p_export(_ptr(B), _ptr(C_full), ctypes.cast(buf, ctypes.c_void_p)))
+    return bytes(buf)
+
+
+def p2p_import(blobs):
+    """giga_rank_p2p_import: every rank's blob, in rank order."""
+    raw = b"".join(blobs)
+    buf = (ctypes.c_uint8 * len(raw)).from_buffer_copy(raw)
+    _check(lib.giga_rank_p2p_import(ctypes.cast(buf, ctypes.c_void_p), len(blobs)))
 
 
 def matmul_rank(A_shard, B, C_full, M: int, N: int, K: int, stream=None):

@@ -96,3 +96,80 @@ def test_dot_over_virtual_gpus(giga_virtual, torch_cuda, world):
     assert giga.dot(x, y, ngpus=world) == oracle.dot(x, y)[0]
     xd, yd = torch_cuda.from_numpy(x).cuda(), torch_cuda.from_numpy(y).cuda()
     assert giga.dot(xd, yd, ngpus=world) == oracle.dot(x, y)[0]
+
+
+# ---- rank API (one process per rank) with the peer-to-peer transport ----------------------
+
+def _rank_worker(rank, world, port, M, N, K, q):
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ.update({"GIGA_TRANSPORT": "p2p", "GIGA_BCAST_CHUNKS": "3",
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    try:
+        import torch
+        import torch.distributed as dist
+        import oracle
+        import synth
+        from paper_2504_01266_b200 import giga
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        giga.rank_init(rank, world, 0, None)
+        r0, rows = giga.partition(M, world, rank)
+        A = synth.gen_rows(r0, rows, K, synth.MATRIX_A, "d3")
+        Bn = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+        dA = torch.from_numpy(A).cuda() if rows else torch.empty(0, device="cuda")
+        dB = torch.from_numpy(Bn).cuda() if rank == 0 else torch.full((K, N), float("nan"),
+                                                                      device="cuda")
+        dC = torch.full((M, N), float("nan"), device="cuda")
+        blob = giga.p2p_export(dB, dC)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, blob)
+        giga.p2p_import(blobs)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        for _ in range(3):  # repeated calls: flag call numbers and back-pressure
+            giga.matmul_rank(dA, dB, dC, M, N, K, stream=s)
+        s.synchronize()
+        Cref, _ = oracle.gemm(synth.gen_matrix(M, K, synth.MATRIX_A, "d3"), Bn)
+        ok_c = bool(np.array_equal(dC.cpu().numpy().astype(np.float64), Cref))
+        ok_b = bool(np.array_equal(dB.cpu().numpy(), Bn))
+        n = 100003
+        x = synth.gen_vector(n, synth.VECTOR_X, "d3")
+        y = synth.gen_vector(n, synth.VECTOR_Y, "d3")
+        x0, xr = giga.partition(n, world, rank)
+        xs = torch.from_numpy(x[x0:x0 + xr]).cuda()
+        ys = torch.from_numpy(y[x0:x0 + xr]).cuda()
+        dots = [giga.dot_rank(xs, ys, n, stream=s) for _ in range(2)]
+        ok_d = all(v == oracle.dot(x, y)[0] for v in dots)
+        dist.barrier()
+        giga.finalize()
+        q.put((rank, ok_c, ok_b, ok_d, ""))
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, False, False, False, repr(e)))
+
+
+@pytest.mark.parametrize("world,M,N,K", [(2, 1000, 520, 1040), (3, 517, 256, 2064)])
+def test_rank_p2p_across_processes(torch_cuda, world, M, N, K):
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_worker, args=(r, world, port, M, N, K, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        res = sorted(q.get(timeout=240) for _ in range(world))
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for rank, ok_c, ok_b, ok_d, err in res:
+        assert ok_c and ok_b and ok_d, (rank, ok_c, ok_b, ok_d, err)
