@@ -174,8 +174,13 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=60.0,
                     help="total seconds of oracle work for --impl reference")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--transport", default=os.environ.get("GIGA_TRANSPORT", "nccl"),
+                    choices=["nccl", "p2p"],
+                    help="N > 1: NCCL pipeline (default) or the peer-to-peer transport "
+                         "(copy-engine B chain + gather fused into the GEMM epilogue)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    os.environ["GIGA_TRANSPORT"] = args.transport
     if args.impl == "reference":
         return run_reference(args)
 
@@ -209,6 +214,10 @@ def main():
     else:
         B = torch.empty((K, N), dtype=torch.float32, device=dev)
     C = torch.empty((M, N), dtype=torch.float32, device=dev)
+    if world > 1 and args.transport == "p2p":  # register B / C_full with every peer (IPC)
+        blobs = [None] * world
+        pg.all_gather_object(blobs, giga.p2p_export(B, C))
+        giga.p2p_import(blobs)
     stream = torch.cuda.Stream(device=dev)
     stream.wait_stream(torch.cuda.current_stream(dev))  # inputs are produced on torch's stream
 
@@ -317,6 +326,7 @@ def main():
             "dtype": "f32 (3xTF32 tensor, fp32-accurate)", "data": "synthetic",
             "config": {"workload": f"{args.config} M={M} N={N} K={K}", "dist": args.dist,
                        "parallelism": f"row-split x{world}",
+                       "transport": args.transport if world > 1 else "none (1 GPU)",
                        "l2": "inputs larger than L2 (A, B, C 1 GiB each at c3)"},
             "roofline": roof, "roofline_step": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(kt["gemm_launches"] + kt["split_launches"]),
