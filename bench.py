@@ -193,18 +193,31 @@ def main():
         if world == 1 and args.gpus > 1:
             print(f"--gpus {args.gpus} needs torchrun with {args.gpus} processes", file=sys.stderr)
             return 2
+    # GIGA_BENCH_ONE_DEVICE=1 (tests only): every rank on cuda:0, gloo plumbing, p2p
+    # transport -- exercises the N > 1 bench path on a one-GPU box; its numbers mean nothing
+    one_dev = os.environ.get("GIGA_BENCH_ONE_DEVICE") == "1" and world > 1
+    if one_dev:
+        local = 0
+        args.transport = os.environ["GIGA_TRANSPORT"] = "p2p"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         pg = dist
-        obj = [giga.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        giga.rank_init(rank, world, local, obj[0])
+        if args.transport == "p2p":
+            giga.rank_init(rank, world, local, None)
+        else:
+            obj = [giga.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            giga.rank_init(rank, world, local, obj[0])
     else:
         giga.rank_init(0, 1, local, None)
+    red_dev = torch.device("cpu") if one_dev else dev  # tensor device for max-over-ranks
 
     M, N, K = CONFIGS[args.config]
     r0, rows = giga.partition(M, world, rank)
@@ -253,7 +266,7 @@ def main():
     kt = giga.timing_read()
     giga.timing_enable(False)
     if pg is not None:
-        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_total], dtype=torch.float64, device=red_dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
@@ -307,7 +320,8 @@ def main():
     # ---- end to end: host buffers through the C ABI ----
     e2e = None
     if args.e2e_steps > 0:
-        e2e = measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev, pg)
+        e2e = measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev, pg,
+                          red_dev, (A, B, C))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -339,7 +353,8 @@ def main():
     return 0
 
 
-def measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev, pg):
+def measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev, pg, red_dev,
+                dev_bufs):
     """Same metric with the inputs in pinned HOST memory: every step copies this rank's A
     rows (and B on rank 0) host->device, runs the hot path and copies this rank's C rows
     back (N = 1: the single giga_matmul host-pointer call of the C ABI)."""
@@ -370,9 +385,7 @@ def measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev, pg):
     if rank == 0:
         Bh = synth.gen_rows_torch(0, K, N, synth.MATRIX_B, args.dist, device=dev).cpu().pin_memory()
     Ch = torch.empty((rows, N), dtype=torch.float32).pin_memory()
-    A = torch.empty((rows, K), dtype=torch.float32, device=dev)
-    B = torch.empty((K, N), dtype=torch.float32, device=dev)
-    C = torch.empty((M, N), dtype=torch.float32, device=dev)
+    A, B, C = dev_bufs  # the device buffers of the timed run (registered with peers for p2p)
     s = torch.cuda.Stream(device=dev)
     s.wait_stream(torch.cuda.current_stream(dev))
 
@@ -391,7 +404,7 @@ def measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev, pg):
         pg.barrier()
         t0 = time.perf_counter()
         one()
-        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         ts.append(float(t.item()))
     t = statistics.median(ts)

@@ -173,3 +173,29 @@ def test_rank_p2p_across_processes(torch_cuda, world, M, N, K):
                 p.kill()
     for rank, ok_c, ok_b, ok_d, err in res:
         assert ok_c and ok_b and ok_d, (rank, ok_c, ok_b, ok_d, err)
+
+
+def test_bench_two_ranks_on_one_device(torch_cuda):
+    """bench.py's N > 1 path end to end under torchrun (2 ranks sharing cuda:0, gloo plumbing,
+    p2p transport): rank init, IPC registration, max-over-ranks timing, one JSON line."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ, GIGA_BENCH_ONE_DEVICE="1")
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+         "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+         "--steps", "2", "--warmup", "3", "--config", "c2_4096", "--no-cpu-baseline",
+         "--e2e-steps", "1"], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["transport"] == "p2p" and d["value"] > 0
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
