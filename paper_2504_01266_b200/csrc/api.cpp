@@ -500,6 +500,7 @@ struct Part {
   float *B;         // K x N: source on rank 0, receive buffer elsewhere
   float *C;         // M x N: every rank ends with all of C
   cudaStream_t st;  // compute stream
+  float *C_rows = nullptr;  // p2p without gather: this rank's rows only (rows x N)
 };
 
 bool force_comm() { return env_int("GIGA_FORCE_COMM", 0) != 0; }
@@ -657,12 +658,15 @@ bool transport_p2p() {
   return e && strcmp(e, "p2p") == 0;
 }
 
-int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K) {
+// gather = false: no fused gather; each part's GEMM writes only its own rows into C_rows.
+int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K, bool gather = true) {
   const int world = int(parts.size());
   if (world > kMaxCDst)
     return fail(GIGA_ERR_UNSUPPORTED, "p2p transport: at most %d GPUs", kMaxCDst);
   bool aligned = (K % 4 == 0) && (N % 4 == 0);
-  for (auto &p : parts) aligned = aligned && aligned16(p.A) && aligned16(p.B) && aligned16(p.C);
+  for (auto &p : parts)
+    aligned = aligned && aligned16(p.A) && aligned16(p.B) &&
+              aligned16(gather ? p.C : p.C_rows);
   if (!aligned)
     return fail(GIGA_ERR_UNSUPPORTED, "p2p transport needs K %% 4 == N %% 4 == 0, aligned");
   const Plan plan = make_plan(M, K, world, true);
@@ -702,10 +706,12 @@ int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K) {
     partition_rows(M, world, p.rank, &r0, &rows);
     float *peer[kMaxCDst];
     int np = 0;
-    for (auto &q : parts)
-      if (&q != &p) peer[np++] = q.C + r0 * N;
+    if (gather)
+      for (auto &q : parts)
+        if (&q != &p) peer[np++] = q.C + r0 * N;
     ex.peer_c = peer;
     ex.n_peer_c = np;
+    float *Cr = gather ? p.C + r0 * N : p.C_rows;
     for (int c = 0; c < plan.pb; ++c) {
       const int64_t Kc = plan.kb[c + 1] - plan.kb[c];
       CK(cudaStreamWaitEvent(p.st, p.d->ev_kchunk[c], 0));
@@ -714,10 +720,11 @@ int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K) {
       GemmExtra e = ex;
       e.accumulate = c > 0;
       TRY(gemm_chunk(p.A + plan.kb[c], fptr(p.d->A_lo) + plan.kb[c], p.B + plan.kb[c] * N,
-                     fptr(p.d->B_lo) + plan.kb[c] * N, p.C + r0 * N, rows, N, Kc, e, p.st));
+                     fptr(p.d->B_lo) + plan.kb[c] * N, Cr, rows, N, Kc, e, p.st));
     }
     CK(cudaEventRecord(p.d->ev_c, p.st));
   }
+  if (!gather) return GIGA_OK;  // every rank only needs its own rows
   // 3. a GPU's C_full is complete when every GPU's GEMMs are
   for (auto &p : parts) {
     CK(cudaSetDevice(p.d->dev));
@@ -1005,6 +1012,28 @@ int matmul_locked(const float *A, const float *B, float *C, int64_t M, int64_t N
       CK(cudaMemcpyAsync(d.B_h.p, B, size_t(K * N) * 4, cudaMemcpyHostToDevice, d.compute));
   }
   const float *B0 = device ? B : fptr(g.devs[0].B_h);
+  if (ngpus > 1 && !device && transport_p2p() && K % 4 == 0 && N % 4 == 0) {
+    // copy-engine chain for B; each GPU writes only its rows and copies them straight home
+    std::vector<Part> parts;
+    for (int i = 0; i < ngpus; ++i) {
+      DevCtx &d = g.devs[i];
+      Part p{&d, nullptr, i, fptr(d.A_h), i == 0 ? const_cast<float *>(B0) : fptr(d.B_h),
+             nullptr, d.compute};
+      p.C_rows = fptr(d.C_h);
+      parts.push_back(p);
+    }
+    TRY(run_p2p(parts, M, N, K, /*gather=*/false));
+    for (int i = 0; i < ngpus; ++i) {
+      DevCtx &d = g.devs[i];
+      CK(cudaSetDevice(d.dev));
+      int64_t r0, rows;
+      partition_rows(M, ngpus, i, &r0, &rows);
+      if (rows > 0)
+        CK(cudaMemcpyAsync(C + r0 * N, d.C_h.p, size_t(rows * N) * 4, cudaMemcpyDeviceToHost,
+                           d.compute));
+    }
+    return sync_all(ngpus);
+  }
   if (ngpus > 1) {
     std::vector<ncclComm_t> *comms = nullptr;
     TRY(get_comms(ngpus, &comms));

@@ -199,3 +199,18 @@ def test_bench_two_ranks_on_one_device(torch_cuda):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["transport"] == "p2p" and d["value"] > 0
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+
+
+@pytest.mark.parametrize("world,M,N,K", [(2, 777, 520, 1040), (4, 1000, 256, 2048)])
+def test_host_buffers_p2p_virtual(giga_virtual, torch_cuda, monkeypatch, world, M, N, K):
+    """giga_matmul with host buffers over several (virtual) GPUs: per-GPU H2D of the A rows,
+    B to GPU 0 then down the copy-engine chain, each GPU copies its own C rows home."""
+    monkeypatch.setenv("GIGA_TRANSPORT", "p2p")
+    giga = giga_virtual(world)
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+    C = np.full((M, N), np.nan, np.float32)
+    giga.matmul(A, B, C, M, N, K, world)
+    Cref, _ = oracle.gemm(A, B)
+    ok, st = check_exact(C, Cref)
+    assert ok, st
