@@ -75,6 +75,8 @@ struct DevCtx {
   cudaEvent_t ev_b = nullptr;      // B present on this GPU
   cudaEvent_t ev_c = nullptr;      // this GPU's C rows computed
   cudaEvent_t ev_start = nullptr;  // caller-stream entry (rank mode)
+  cudaEvent_t ev_last = nullptr;   // rank mode: end of the previous call (workspace reuse)
+  bool has_last = false;
   std::vector<cudaEvent_t> ev_kchunk;  // pipeline: B K-chunk c present
   std::vector<cudaEvent_t> ev_rchunk;  // pipeline: C row-chunk q computed
   Buf A_lo, B_lo, A_pad, B_pad, C_pad, A_h, B_h, C_h;
@@ -217,6 +219,7 @@ int ctx_create(DevCtx &d, int dev) {
   CK(cudaEventCreateWithFlags(&d.ev_b, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d.ev_c, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d.ev_start, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&d.ev_last, cudaEventDisableTiming));
   for (auto *v : {&d.ev_kchunk, &d.ev_rchunk}) {
     v->assign(kMaxChunks, nullptr);
     for (auto &e : *v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -232,7 +235,7 @@ void ctx_destroy(DevCtx &d) {
   if (d.compute) cudaStreamDestroy(d.compute);
   if (d.comm) cudaStreamDestroy(d.comm);
   if (d.d2h) cudaStreamDestroy(d.d2h);
-  for (cudaEvent_t e : {d.ev_b, d.ev_c, d.ev_start})
+  for (cudaEvent_t e : {d.ev_b, d.ev_c, d.ev_start, d.ev_last})
     if (e) cudaEventDestroy(e);
   for (auto *v : {&d.ev_kchunk, &d.ev_rchunk})
     for (cudaEvent_t e : *v)
@@ -1317,12 +1320,22 @@ int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, i
   DevCtx &d = g.devs[0];
   CK(cudaSetDevice(d.dev));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.compute;
-  if (g.p2p.ready && transport_p2p())
-    return run_p2p_rank(d, st, A_shard, B, C_full, M, N, K);
-  if (!g.rank_comm)
-    return shard_compute(d, st, A_shard, rows, B, C_full + r0 * N, N, N, K, nullptr);
-  std::vector<Part> parts{{&d, g.rank_comm, g.rank, A_shard, B, C_full, st}};
-  return run_pipeline(parts, g.world, M, N, K);
+  // calls share the rank's workspace: a call starts after the previous one, whatever the
+  // caller's streams
+  if (d.has_last) CK(cudaStreamWaitEvent(st, d.ev_last, 0));
+  int rc;
+  if (g.p2p.ready && transport_p2p()) {
+    rc = run_p2p_rank(d, st, A_shard, B, C_full, M, N, K);
+  } else if (!g.rank_comm) {
+    rc = shard_compute(d, st, A_shard, rows, B, C_full + r0 * N, N, N, K, nullptr);
+  } else {
+    std::vector<Part> parts{{&d, g.rank_comm, g.rank, A_shard, B, C_full, st}};
+    rc = run_pipeline(parts, g.world, M, N, K);
+  }
+  TRY(rc);
+  CK(cudaEventRecord(d.ev_last, st));
+  d.has_last = true;
+  return GIGA_OK;
 }
 
 // ---- vector operations -------------------------------------------------
