@@ -316,6 +316,18 @@ int nccl_check(ncclResult_t r, const char *what) {
   return fail(GIGA_ERR_COMM, "%s failed: %s", what, api ? api->GetErrorString(r) : "?");
 }
 
+int env_int(const char *name, int dflt);
+
+// Communicator config: NCCL runs beside a persistent GEMM that leaves $GIGA_COMM_SMS (8) SMs
+// free, so its kernels are capped at that many CTAs ($GIGA_NCCL_MAX_CTAS overrides; 0 = NCCL
+// default) instead of queueing behind the GEMM's CTAs.
+ncclConfig_t comm_config() {
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  const int cap = env_int("GIGA_NCCL_MAX_CTAS", env_int("GIGA_COMM_SMS", 8));
+  if (cap > 0) cfg.maxCTAs = cap;
+  return cfg;
+}
+
 int get_comms(int ngpus, std::vector<ncclComm_t> **out) {
   auto it = g.comms.find(ngpus);
   if (it != g.comms.end()) {
@@ -325,10 +337,20 @@ int get_comms(int ngpus, std::vector<ncclComm_t> **out) {
   const char *why = nullptr;
   const NcclApi *api = nccl_api(&why);
   if (!api) return fail(GIGA_ERR_COMM, "NCCL unavailable: %s", why ? why : "?");
-  std::vector<int> devs(ngpus);
-  for (int i = 0; i < ngpus; ++i) devs[i] = g.devs[i].dev;
+  ncclUniqueId id;
+  TRY(nccl_check(api->GetUniqueId(&id), "ncclGetUniqueId"));
   std::vector<ncclComm_t> comms(ngpus, nullptr);
-  TRY(nccl_check(api->CommInitAll(comms.data(), ngpus, devs.data()), "ncclCommInitAll"));
+  TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
+  for (int i = 0; i < ngpus; ++i) {
+    CK(cudaSetDevice(g.devs[i].dev));
+    ncclConfig_t cfg = comm_config();
+    ncclResult_t r = api->CommInitRankConfig(&comms[i], ngpus, id, i, &cfg);
+    if (r != ncclSuccess) {
+      api->GroupEnd();
+      return nccl_check(r, "ncclCommInitRankConfig");
+    }
+  }
+  TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd(init)"));
   g.comms[ngpus] = comms;
   *out = &g.comms[ngpus];
   return GIGA_OK;
@@ -1295,7 +1317,9 @@ int giga_rank_init(int rank, int world, int device, const uint8_t id[128]) {
       return rc;
     }
     cudaSetDevice(device);
-    rc = nccl_check(api->CommInitRank(&g.rank_comm, world, u, rank), "ncclCommInitRank");
+    ncclConfig_t cfg = comm_config();
+    rc = nccl_check(api->CommInitRankConfig(&g.rank_comm, world, u, rank, &cfg),
+                    "ncclCommInitRankConfig");
     if (rc != GIGA_OK) {
       ctx_destroy(g.devs[0]);
       g.devs.clear();

@@ -32,6 +32,7 @@ const NcclApi *nccl_api(const char **why) {
     bool ok = sym(h, "ncclGetUniqueId", g_api.GetUniqueId) &&
               sym(h, "ncclCommInitRank", g_api.CommInitRank) &&
               sym(h, "ncclCommInitAll", g_api.CommInitAll) &&
+              sym(h, "ncclCommInitRankConfig", g_api.CommInitRankConfig) &&
               sym(h, "ncclCommDestroy", g_api.CommDestroy) &&
               sym(h, "ncclCommGetAsyncError", g_api.CommGetAsyncError) &&
               sym(h, "ncclBroadcast", g_api.Broadcast) &&
