@@ -1,0 +1,97 @@
+"""Seeded shape fuzzing: random (M, N, K) from 1 to ~700 (ragged everywhere: K and N not
+multiples of 4 take the padded path, M < tile, tails in every dimension) through every public
+entry point, integer inputs (bit-exact against the oracle), C prefilled with NaN."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle.check import check_exact
+import synth
+
+pytestmark = pytest.mark.gpu
+
+RNG = np.random.default_rng(20261017)
+SHAPES = [tuple(int(v) for v in RNG.integers(1, 700, 3)) for _ in range(14)] + [
+    (1, 1, 1), (1, 700, 3), (700, 1, 5), (2, 3, 1), (257, 255, 4), (513, 4, 1023)]
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+@pytest.fixture(scope="module")
+def giga(torch_cuda):
+    from paper_2504_01266_b200 import build
+    build.build()
+    from paper_2504_01266_b200 import giga as g
+    g.finalize()
+    g.init(1)
+    yield g
+    g.finalize()
+
+
+def _inputs(M, N, K):
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+    ref, _ = oracle.gemm(A, B)
+    return A, B, ref
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_fuzz_host_device_sharded(giga, torch_cuda, M, N, K):
+    torch = torch_cuda
+    A, B, ref = _inputs(M, N, K)
+    C = np.full((M, N), np.nan, np.float32)
+    giga.matmul(A, B, C, M, N, K, 1)
+    assert check_exact(C, ref)[0], "host"
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    dC = torch.full((M, N), float("nan"), device="cuda")
+    giga.matmul(dA, dB, dC, M, N, K, 1)
+    assert check_exact(dC.cpu().numpy(), ref)[0], "device"
+    dC.fill_(float("nan"))
+    giga.matmul_sharded([dA], [dB], [dC], M, N, K)
+    assert check_exact(dC.cpu().numpy(), ref)[0], "sharded"
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES[:10])
+def test_fuzz_forced_comm_pipeline(giga, torch_cuda, monkeypatch, M, N, K):
+    torch = torch_cuda
+    monkeypatch.setenv("GIGA_FORCE_COMM", "1")
+    monkeypatch.setenv("GIGA_BCAST_CHUNKS", "4")
+    monkeypatch.setenv("GIGA_GATHER_CHUNKS", "3")
+    A, B, ref = _inputs(M, N, K)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    dC = torch.full((M, N), float("nan"), device="cuda")
+    giga.matmul_sharded([dA], [dB], [dC], M, N, K)
+    assert check_exact(dC.cpu().numpy(), ref)[0]
+
+
+@pytest.mark.parametrize("M,N,K", [s for s in SHAPES if s[1] % 4 == 0 and s[2] % 4 == 0][:6]
+                         + [(700, 256, 1024), (5, 8, 520)])
+def test_fuzz_p2p_virtual(torch_cuda, monkeypatch, M, N, K):
+    torch = torch_cuda
+    from paper_2504_01266_b200 import giga as g
+    monkeypatch.setenv("GIGA_TRANSPORT", "p2p")
+    monkeypatch.setenv("GIGA_BCAST_CHUNKS", "2")
+    world = 3
+    g.finalize()
+    g.init_devices([0] * world)
+    try:
+        A, B, ref = _inputs(M, N, K)
+        shards = []
+        for r in range(world):
+            r0, rows = g.partition(M, world, r)
+            shards.append(torch.from_numpy(np.ascontiguousarray(A[r0:r0 + rows])).cuda()
+                          if rows else torch.empty(0, device="cuda"))
+        Bs = [torch.from_numpy(B).cuda()] + [torch.empty(K, N, device="cuda")
+                                             for _ in range(world - 1)]
+        Cs = [torch.full((M, N), float("nan"), device="cuda") for _ in range(world)]
+        g.matmul_sharded(shards, Bs, Cs, M, N, K)
+        for r in range(world):
+            assert check_exact(Cs[r].cpu().numpy(), ref)[0], r
+    finally:
+        g.finalize()
+        g.init(1)
