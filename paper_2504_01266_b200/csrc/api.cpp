@@ -79,6 +79,7 @@ struct DevCtx {
   bool has_last = false;
   std::vector<cudaEvent_t> ev_kchunk;  // pipeline: B K-chunk c present
   std::vector<cudaEvent_t> ev_rchunk;  // pipeline: C row-chunk q computed
+  std::vector<cudaEvent_t> ev_done;    // host pipeline: late row block q computed
   Buf A_lo, B_lo, A_pad, B_pad, C_pad, A_h, B_h, C_h;
   Buf vec_ws;  // dot: kDotMaxBlocks fp64 partials, the fp64 result, the ticket (zeroed once)
 };
@@ -220,7 +221,7 @@ int ctx_create(DevCtx &d, int dev) {
   CK(cudaEventCreateWithFlags(&d.ev_c, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d.ev_start, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d.ev_last, cudaEventDisableTiming));
-  for (auto *v : {&d.ev_kchunk, &d.ev_rchunk}) {
+  for (auto *v : {&d.ev_kchunk, &d.ev_rchunk, &d.ev_done}) {
     v->assign(kMaxChunks, nullptr);
     for (auto &e : *v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
@@ -237,7 +238,7 @@ void ctx_destroy(DevCtx &d) {
   if (d.d2h) cudaStreamDestroy(d.d2h);
   for (cudaEvent_t e : {d.ev_b, d.ev_c, d.ev_start, d.ev_last})
     if (e) cudaEventDestroy(e);
-  for (auto *v : {&d.ev_kchunk, &d.ev_rchunk})
+  for (auto *v : {&d.ev_kchunk, &d.ev_rchunk, &d.ev_done})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
   d = DevCtx{};
@@ -954,44 +955,85 @@ int sharded_locked(const float *const *A_shard, float *const *B_buf, float *cons
   return GIGA_OK;
 }
 
-// Host buffers on one GPU (the paper's call): a row-block pipeline over three
+// Host buffers on one GPU (the paper's call): a two-phase schedule over three
 // engines -- host-to-device copies on the comm stream, splits + GEMMs on the compute stream,
-// device-to-host copies on the d2h stream. B goes first; then A row block q is copied while
-// block q-1 computes, and block q's C rows are copied back while block q+1 computes. With
-// pinned host memory the PCIe transfers overlap the tensor-core work. $GIGA_HOST_CHUNKS
-// (default 8) row blocks.
+// device-to-host copies on the d2h stream -- so that the PCIe transfers hide behind the
+// tensor cores instead of preceding them (with pinned host memory).
+//   phase 1, the first `Me` rows ($GIGA_HOST_EARLY_PCT = 50% of M): their A columns and the B
+//     rows of K-chunk c arrive together and the GEMM of chunk c accumulates into C (C += A_c
+//     B_c), so compute starts after 1/P of the early inputs instead of after all of B;
+//   phase 2, the remaining rows in row blocks ($GIGA_HOST_CHUNKS = 8) over the full K (B is
+//     complete by then): block q's A rows are copied while q-1 computes, and C goes back to
+//     the host -- the early rows first, then block by block -- over the other PCIe direction.
 int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M, int64_t N,
                   int64_t K) {
   CK(cudaSetDevice(d.dev));
+  int P = std::min(std::max(env_int("GIGA_HOST_KCHUNKS", 8), 1), kMaxChunks);
+  P = int(std::min<int64_t>(P, std::max<int64_t>(1, K / 512)));
+  const int pct = std::min(std::max(env_int("GIGA_HOST_EARLY_PCT", 50), 0), 100);
+  int64_t Me = (P > 1) ? std::min<int64_t>(M, (M * pct / 100 + 255) / 256 * 256) : 0;
   int Q = std::min(std::max(env_int("GIGA_HOST_CHUNKS", 8), 1), kMaxChunks);
-  Q = int(std::min<int64_t>(Q, std::max<int64_t>(1, M / 256)));
+  Q = int(std::min<int64_t>(Q, std::max<int64_t>(1, (M - Me) / 256)));
+  if (Me == 0) P = 1;  // B in one piece, row blocks only
+  int64_t kb[kMaxChunks + 1];
+  for (int c = 0; c < P; ++c) kb[c] = (K * c / P) / 16 * 16;
+  kb[P] = K;
   TRY(ws_reserve(d, {{&d.A_h, size_t(M * K) * 4},
                      {&d.B_h, size_t(K * N) * 4},
                      {&d.C_h, size_t(M * N) * 4},
                      {&d.A_lo, size_t(M * K) * 4},
                      {&d.B_lo, size_t(K * N) * 4}}));
-  float *Ad = fptr(d.A_h), *Bd = fptr(d.B_h), *Cd = fptr(d.C_h);
-  CK(cudaMemcpyAsync(Bd, B, size_t(K * N) * 4, cudaMemcpyHostToDevice, d.comm));
-  CK(cudaEventRecord(d.ev_b, d.comm));
+  float *Ad = fptr(d.A_h), *Bd = fptr(d.B_h), *Cd = fptr(d.C_h), *Alo = fptr(d.A_lo),
+        *Blo = fptr(d.B_lo);
+  // host -> device: (early A columns, B rows) per K-chunk, then the late A row blocks
+  for (int c = 0; c < P; ++c) {
+    const int64_t Kc = kb[c + 1] - kb[c];
+    if (Me > 0)
+      CK(cudaMemcpy2DAsync(Ad + kb[c], size_t(K) * 4, A + kb[c], size_t(K) * 4,
+                           size_t(Kc) * 4, size_t(Me), cudaMemcpyHostToDevice, d.comm));
+    CK(cudaMemcpyAsync(Bd + kb[c] * N, B + kb[c] * N, size_t(Kc * N) * 4,
+                       cudaMemcpyHostToDevice, d.comm));
+    CK(cudaEventRecord(d.ev_kchunk[c], d.comm));
+  }
   for (int q = 0; q < Q; ++q) {
-    const int64_t q0 = M * q / Q, q1 = M * (q + 1) / Q;
+    const int64_t q0 = Me + (M - Me) * q / Q, q1 = Me + (M - Me) * (q + 1) / Q;
     if (q1 > q0)
       CK(cudaMemcpyAsync(Ad + q0 * K, A + q0 * K, size_t((q1 - q0) * K) * 4,
                          cudaMemcpyHostToDevice, d.comm));
-    CK(cudaEventRecord(d.ev_kchunk[q], d.comm));
+    CK(cudaEventRecord(d.ev_rchunk[q], d.comm));
   }
-  CK(cudaStreamWaitEvent(d.compute, d.ev_b, 0));
-  TRY(split(Bd, fptr(d.B_lo), K * N, d.compute));
+  // phase 1: early rows, K-chunk by K-chunk, accumulating in C
+  GemmExtra ex;
+  ex.lda = K;
+  ex.ldb = N;
+  for (int c = 0; c < P; ++c) {
+    const int64_t Kc = kb[c + 1] - kb[c];
+    CK(cudaStreamWaitEvent(d.compute, d.ev_kchunk[c], 0));
+    TRY(split(Bd + kb[c] * N, Blo + kb[c] * N, Kc * N, d.compute));
+    if (Me == 0) continue;
+    CK(timed(1, d.compute, [&] {
+      return launch_split_lo_2d(Ad + kb[c], Alo + kb[c], Me, Kc, K, d.compute);
+    }));
+    GemmExtra e = ex;
+    e.accumulate = c > 0;
+    TRY(gemm_chunk(Ad + kb[c], Alo + kb[c], Bd + kb[c] * N, Blo + kb[c] * N, Cd, Me, N, Kc, e,
+                   d.compute));
+  }
+  if (Me > 0) {
+    CK(cudaEventRecord(d.ev_c, d.compute));
+    CK(cudaStreamWaitEvent(d.d2h, d.ev_c, 0));
+    CK(cudaMemcpyAsync(C, Cd, size_t(Me * N) * 4, cudaMemcpyDeviceToHost, d.d2h));
+  }
+  // phase 2: late row blocks over the full K
   for (int q = 0; q < Q; ++q) {
-    const int64_t q0 = M * q / Q, q1 = M * (q + 1) / Q;
-    CK(cudaStreamWaitEvent(d.compute, d.ev_kchunk[q], 0));
+    const int64_t q0 = Me + (M - Me) * q / Q, q1 = Me + (M - Me) * (q + 1) / Q;
+    CK(cudaStreamWaitEvent(d.compute, d.ev_rchunk[q], 0));
     if (q1 > q0) {
-      TRY(split(Ad + q0 * K, fptr(d.A_lo) + q0 * K, (q1 - q0) * K, d.compute));
-      TRY(gemm(Ad + q0 * K, fptr(d.A_lo) + q0 * K, Bd, fptr(d.B_lo), Cd + q0 * N, q1 - q0, N, K,
-               N, d.compute));
+      TRY(split(Ad + q0 * K, Alo + q0 * K, (q1 - q0) * K, d.compute));
+      TRY(gemm(Ad + q0 * K, Alo + q0 * K, Bd, Blo, Cd + q0 * N, q1 - q0, N, K, N, d.compute));
     }
-    CK(cudaEventRecord(d.ev_rchunk[q], d.compute));
-    CK(cudaStreamWaitEvent(d.d2h, d.ev_rchunk[q], 0));
+    CK(cudaEventRecord(d.ev_done[q], d.compute));
+    CK(cudaStreamWaitEvent(d.d2h, d.ev_done[q], 0));
     if (q1 > q0)
       CK(cudaMemcpyAsync(C + q0 * N, Cd + q0 * N, size_t((q1 - q0) * N) * 4,
                          cudaMemcpyDeviceToHost, d.d2h));

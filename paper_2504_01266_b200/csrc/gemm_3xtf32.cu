@@ -524,6 +524,33 @@ cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t s
   return cudaGetLastError();
 }
 
+// The same split over a rows x cols block with row stride ld (elements); cols % 4 == 0,
+// ld % 4 == 0 and 16-byte aligned bases (a K-chunk of a row-major A shard).
+__global__ void __launch_bounds__(256) split_lo_2d_kernel(const float *__restrict__ x,
+                                                          float *__restrict__ lo, int64_t rows,
+                                                          int64_t cols, int64_t ld) {
+  const int64_t c4 = cols >> 2, total = rows * c4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int64_t r = i / c4, c = (i - r * c4) << 2;
+    const float4 v = __ldcs(reinterpret_cast<const float4 *>(x + r * ld + c));
+    __stcs(reinterpret_cast<float4 *>(lo + r * ld + c),
+           make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w)));
+  }
+}
+
+cudaError_t launch_split_lo_2d(const float *x, float *lo, int64_t rows, int64_t cols,
+                               int64_t ld, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  if ((cols & 3) || (ld & 3)) return cudaErrorInvalidValue;
+  int64_t blocks = (rows * (cols / 4) + 255) / 256;
+  const int64_t cap = int64_t(num_sms_current()) * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  split_lo_2d_kernel<<<unsigned(blocks), 256, 0, st>>>(x, lo, rows, cols, ld);
+  return cudaGetLastError();
+}
+
 // the smem opt-in is a per-device function attribute
 template <int CG>
 static cudaError_t ensure_smem_attr() {

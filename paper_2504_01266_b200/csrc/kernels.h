@@ -14,6 +14,9 @@ int default_promote_kblocks();
 
 // lo = x - tf32(x) over n elements (HBM-bound elementwise split).
 cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t st);
+// The same over a rows x cols block of a row-major matrix with row stride ld (cols, ld % 4 == 0).
+cudaError_t launch_split_lo_2d(const float *x, float *lo, int64_t rows, int64_t cols,
+                               int64_t ld, cudaStream_t st);
 
 // C[M x N, row stride ldc] = A[M x K] * B[K x N] by 3xTF32 (terms = 3) or 1xTF32 (terms = 1)
 // on the tcgen05 tensor cores. Requires K % 4 == 0, N % 4 == 0, ldc % 4 == 0, 16B-aligned

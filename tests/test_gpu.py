@@ -262,7 +262,8 @@ def test_pipeline_forced_comm_rank_api(torch_cuda, monkeypatch):
 
 
 @pytest.mark.parametrize("M,N,K,pinned", [(2000, 520, 1028, True), (4096, 256, 512, False),
-                                          (300, 64, 40, True)])
+                                          (300, 64, 40, True), (1500, 300, 4100, True),
+                                          (256, 128, 8192, False), (2049, 1024, 2048, True)])
 def test_host_pipeline_row_blocks(giga, torch_cuda, M, N, K, pinned):
     """giga_matmul with host buffers: row-block H2D / GEMM / D2H pipeline, bit-exact."""
     torch = torch_cuda
