@@ -6,10 +6,11 @@
 
 One step = the whole hot path over one synthetic problem: broadcast B from
 rank 0 (N > 1), split A and B into TF32 hi/lo, the 3xTF32 tcgen05 shard GEMM, gather the C
-row blocks on every rank. Default workload: BASELINE.json configs[2], M = N = K = 16384,
-strong scaling (the same problem split over N GPUs). Inputs are seeded synthetic fp32
-(synth "d2", U[-1,1)), resident in HBM before the timed region; A, B, C are each 1 GiB,
-larger than the 126 MB L2, so no flush is needed between steps.
+row blocks on every rank. Default workload: M = N = K = 32768 (BASELINE.json configs[4], the
+problem the north_star's targets are quoted on), strong scaling (the same problem split over
+N GPUs); --config picks the others. Inputs are seeded synthetic fp32 (synth "d2", U[-1,1)),
+resident in HBM before the timed region; each step is bracketed by CUDA events and the L2 is
+flushed between steps.
 
 Prints ONE JSON line (rank 0). Metric: logical TFLOP/s = 2 M N K / t (whole job).
 """
@@ -34,7 +35,9 @@ CONFIGS = {
     "c4_tall": (262144, 1024, 1024),
     "c5_32768": (32768, 32768, 32768),
 }
-DEFAULT_CONFIG = "c3_16384"
+# The north_star's targets are quoted on 32768^3 (>= 60% of the 8-GPU roofline, >= 6.5x from 1
+# to 8 GPUs); it fits one GPU, so it is the default workload at every N (strong scaling).
+DEFAULT_CONFIG = "c5_32768"
 METRIC = "GEMM TFLOP/s (fp32-accurate) at 1/2/4/8 B200 and % of TF32 tensor roofline"
 
 
@@ -253,23 +256,27 @@ def main():
     stream.synchronize()
     torch.cuda.synchronize()
 
-    # ---- timed region: K steps, device events on the launching stream ----
+    # ---- timed region: K steps, device events on the launching stream around each step;
+    #      between steps (outside the events) a 512 MiB write flushes the 126 MB L2 ----
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     giga.timing_enable(True)
     giga.timing_reset()
     clocks = ClockSampler(local).start()
     barrier()
     torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    ev1.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with torch.cuda.stream(stream):
+        for e0, e1 in evs:
+            flush.fill_(1)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+    evs[-1][1].synchronize()
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    ms_total = ev0.elapsed_time(ev1)
+    ms_total = sum(e0.elapsed_time(e1) for e0, e1 in evs)
     kt = giga.timing_read()
     giga.timing_enable(False)
     if pg is not None:
@@ -339,16 +346,21 @@ def main():
                "sample": f"first {r['rows']} rows of C (of {M}), full N={N}, K={K}: "
                          f"{r['seconds']:.1f} s fp64 i-k-j C triple loop"}
 
+    # the paper's only number for this metric is 32768^3 on its 2 GPUs
+    # (159 s -> 0.443 TFLOP/s derived, 2x Quadro RTX 6000); context, not the target
+    vs_base = (round(tflops / 0.443, 1) if (args.config == "c5_32768" and world == 2)
+               else None)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(tflops, 3), "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": vs_base,
             "dtype": "f32 (3xTF32 tensor, fp32-accurate)", "data": "synthetic",
             "config": {"workload": f"{args.config} M={M} N={N} K={K}", "dist": args.dist,
                        "parallelism": f"row-split x{world}",
                        "transport": args.transport if world > 1 else "none (1 GPU)",
-                       "l2": "inputs larger than L2 (A, B, C 1 GiB each at c3)"},
+                       "l2": "L2 flushed between timed steps (512 MiB write outside the "
+                             "per-step events)"},
             "roofline": roof, "roofline_step": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(kt["gemm_launches"] + kt["split_launches"]),
             "clocks": clk,
