@@ -198,14 +198,16 @@ int giga_rank_p2p_import(const uint8_t *blobs, int world);
  * 16-byte aligned. Errors: INVALID_ARG, CUDA. */
 int giga_split_lo(const float *x, float *lo, int64_t n, void *stream);
 
-/* C[i*ldc + j] = sum_k A[i*K+k] B[k*N+j] for i < M, j < N, with A_lo / B_lo the low parts
- * produced by giga_split_lo. Requirements: K % 4 == 0, N % 4 == 0, ldc % 4 == 0, ldc >= N,
- * all pointers 16-byte aligned (TMA). Errors: INVALID_ARG, CUDA. */
+/* C[i*ldc + j] = sum_k A[i*K+k] B[k*N+j] for i < M, j < N. A_lo / B_lo: either both NULL
+ * (the kernel computes lo = x - tf32(x) of each staged tile in shared memory; the product
+ * path's mode) or both the low parts produced by giga_split_lo (TMA-loaded from HBM).
+ * Requirements: K % 4 == 0, N % 4 == 0, ldc % 4 == 0, ldc >= N, all pointers 16-byte
+ * aligned (TMA). Errors: INVALID_ARG (incl. exactly one of A_lo / B_lo NULL), CUDA. */
 int giga_gemm_3xtf32(const float *A, const float *A_lo, const float *B, const float *B_lo,
                      float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, void *stream);
 
 /* As giga_gemm_3xtf32 with the numerics and tiling knobs exposed (tests and probes):
- * terms = 3 (3xTF32) or 1 (plain TF32: a_hi*b_hi only; A_lo/B_lo may be NULL);
+ * terms = 3 (3xTF32) or 1 (plain TF32: a_hi*b_hi only; A_lo/B_lo ignored);
  * promote_kblocks = number of 16-wide k-blocks accumulated in TMEM before the partial sum
  * is added into the fp32 register sum; 0 = never promote (one TMEM accumulation over K);
  * -1 = the library default;

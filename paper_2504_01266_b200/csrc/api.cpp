@@ -258,7 +258,25 @@ int check_sm100(int dev) {
 // C (rows x N, row stride ldc). If `wait_b` is given, B is only touched after it fires (the
 // A split overlaps the distribution of B).
 
+// The lo = x - tf32(x) operands are computed inside the GEMM from the raw tiles (the
+// default). GIGA_LO_PRESPLIT=1 restores the pre-split design (split_lo_kernel writes lo
+// arrays to HBM, the GEMM TMA-loads them: twice the operand traffic; for comparison).
+bool lo_presplit() {
+  static const bool v = [] {
+    const char *e = getenv("GIGA_LO_PRESPLIT");
+    return e && *e == '1';
+  }();
+  return v;
+}
+size_t lo_bytes(int64_t elems) { return lo_presplit() ? size_t(elems) * 4 : 0; }
+float *lo_at(Buf &b, int64_t off = 0) { return lo_presplit() ? fptr(b) + off : nullptr; }
+template <class T>
+T *at(T *p, int64_t off) {
+  return p ? p + off : nullptr;
+}
+
 int split(const float *x, float *lo, int64_t n, cudaStream_t st) {
+  if (!lo) return GIGA_OK;  // lo computed in the GEMM
   CK(timed(1, st, [&] { return launch_split_lo(x, lo, n, st); }));
   return GIGA_OK;
 }
@@ -280,11 +298,11 @@ int shard_compute(DevCtx &d, cudaStream_t st, const float *A, int64_t rows, cons
   const bool direct = (K % 4 == 0) && (N % 4 == 0) && (ldc % 4 == 0) && aligned16(A) &&
                       aligned16(B) && aligned16(C);
   if (direct) {
-    TRY(ws_reserve(d, {{&d.A_lo, size_t(rows * K) * 4}, {&d.B_lo, size_t(K * N) * 4}}));
-    TRY(split(A, fptr(d.A_lo), rows * K, st));
+    TRY(ws_reserve(d, {{&d.A_lo, lo_bytes(rows * K)}, {&d.B_lo, lo_bytes(K * N)}}));
+    TRY(split(A, lo_at(d.A_lo), rows * K, st));
     if (wait_b) CK(cudaStreamWaitEvent(st, wait_b, 0));
-    TRY(split(B, fptr(d.B_lo), K * N, st));
-    return gemm(A, fptr(d.A_lo), B, fptr(d.B_lo), C, rows, N, K, ldc, st);
+    TRY(split(B, lo_at(d.B_lo), K * N, st));
+    return gemm(A, lo_at(d.A_lo), B, lo_at(d.B_lo), C, rows, N, K, ldc, st);
   }
   // Unaligned shapes (H6): zero-padded copies with K, N rounded up to multiples of 4. Zero
   // columns of A / rows of B add nothing to any dot product.
@@ -292,16 +310,16 @@ int shard_compute(DevCtx &d, cudaStream_t st, const float *A, int64_t rows, cons
   TRY(ws_reserve(d, {{&d.A_pad, size_t(rows * K4) * 4},
                      {&d.B_pad, size_t(K4 * N4) * 4},
                      {&d.C_pad, size_t(rows * N4) * 4},
-                     {&d.A_lo, size_t(rows * K4) * 4},
-                     {&d.B_lo, size_t(K4 * N4) * 4}}));
+                     {&d.A_lo, lo_bytes(rows * K4)},
+                     {&d.B_lo, lo_bytes(K4 * N4)}}));
   CK(cudaMemsetAsync(d.A_pad.p, 0, size_t(rows * K4) * 4, st));
   CK(cudaMemcpy2DAsync(d.A_pad.p, K4 * 4, A, K * 4, K * 4, rows, cudaMemcpyDeviceToDevice, st));
-  TRY(split(fptr(d.A_pad), fptr(d.A_lo), rows * K4, st));
+  TRY(split(fptr(d.A_pad), lo_at(d.A_lo), rows * K4, st));
   if (wait_b) CK(cudaStreamWaitEvent(st, wait_b, 0));
   CK(cudaMemsetAsync(d.B_pad.p, 0, size_t(K4 * N4) * 4, st));
   CK(cudaMemcpy2DAsync(d.B_pad.p, N4 * 4, B, N * 4, N * 4, K, cudaMemcpyDeviceToDevice, st));
-  TRY(split(fptr(d.B_pad), fptr(d.B_lo), K4 * N4, st));
-  TRY(gemm(fptr(d.A_pad), fptr(d.A_lo), fptr(d.B_pad), fptr(d.B_lo), fptr(d.C_pad), rows, N4,
+  TRY(split(fptr(d.B_pad), lo_at(d.B_lo), K4 * N4, st));
+  TRY(gemm(fptr(d.A_pad), lo_at(d.A_lo), fptr(d.B_pad), lo_at(d.B_lo), fptr(d.C_pad), rows, N4,
            K4, N4, st));
   CK(cudaMemcpy2DAsync(C, ldc * 4, d.C_pad.p, N4 * 4, N * 4, rows, cudaMemcpyDeviceToDevice,
                        st));
@@ -565,9 +583,9 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
     int64_t r0, rows;
     partition_rows(M, world, p.rank, &r0, &rows);
     if (aligned) {
-      TRY(ws_reserve(*p.d, {{&p.d->A_lo, size_t(std::max<int64_t>(rows, 1) * K) * 4},
-                            {&p.d->B_lo, size_t(K * N) * 4}}));
-      if (rows > 0) TRY(split(p.A, fptr(p.d->A_lo), rows * K, p.st));
+      TRY(ws_reserve(*p.d, {{&p.d->A_lo, lo_bytes(std::max<int64_t>(rows, 1) * K)},
+                            {&p.d->B_lo, lo_bytes(K * N)}}));
+      if (rows > 0) TRY(split(p.A, lo_at(p.d->A_lo), rows * K, p.st));
     }
   }
   // 1. broadcast B from rank 0, K-chunk by K-chunk
@@ -600,18 +618,18 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
       CK(cudaEventRecord(p.d->ev_rchunk[0], p.st));
       continue;
     }
-    const float *Alo = fptr(p.d->A_lo);
-    float *Blo = fptr(p.d->B_lo);
+    const float *Alo = lo_at(p.d->A_lo);
+    float *Blo = lo_at(p.d->B_lo);
     for (int c = 0; c < pb; ++c) {
       const int64_t Kc = kb[c + 1] - kb[c];
       CK(cudaStreamWaitEvent(p.st, p.d->ev_kchunk[c], 0));
-      TRY(split(p.B + kb[c] * N, Blo + kb[c] * N, Kc * N, p.st));
+      TRY(split(p.B + kb[c] * N, at(Blo, kb[c] * N), Kc * N, p.st));
       GemmExtra e = ex;
       e.accumulate = c > 0;
-      const float *Bc = p.B + kb[c] * N, *Bloc = Blo + kb[c] * N;
+      const float *Bc = p.B + kb[c] * N, *Bloc = at(Blo, kb[c] * N);
       if (c < pb - 1) {
         if (rows > 0)
-          TRY(gemm_chunk(p.A + kb[c], Alo + kb[c], Bc, Bloc, Cs, rows, N, Kc, e, p.st));
+          TRY(gemm_chunk(p.A + kb[c], at(Alo, kb[c]), Bc, Bloc, Cs, rows, N, Kc, e, p.st));
         continue;
       }
       for (int q = 0; q < pc; ++q) {
@@ -619,7 +637,7 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
         plan_block(M, world, pc, p.rank, q, &b0, &brows);
         const int64_t q0 = b0 - r0;  // offset inside this rank's shard
         if (brows > 0)
-          TRY(gemm_chunk(p.A + q0 * K + kb[c], Alo + q0 * K + kb[c], Bc, Bloc, Cs + q0 * N,
+          TRY(gemm_chunk(p.A + q0 * K + kb[c], at(Alo, q0 * K + kb[c]), Bc, Bloc, Cs + q0 * N,
                          brows, N, Kc, e, p.st));
         CK(cudaEventRecord(p.d->ev_rchunk[q], p.st));
       }
@@ -703,9 +721,9 @@ int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K, bool gath
     CK(cudaStreamWaitEvent(p.d->comm, p.d->ev_start, 0));
     int64_t r0, rows;
     partition_rows(M, world, p.rank, &r0, &rows);
-    TRY(ws_reserve(*p.d, {{&p.d->A_lo, size_t(std::max<int64_t>(rows, 1) * K) * 4},
-                          {&p.d->B_lo, size_t(K * N) * 4}}));
-    if (rows > 0) TRY(split(p.A, fptr(p.d->A_lo), rows * K, p.st));
+    TRY(ws_reserve(*p.d, {{&p.d->A_lo, lo_bytes(std::max<int64_t>(rows, 1) * K)},
+                          {&p.d->B_lo, lo_bytes(K * N)}}));
+    if (rows > 0) TRY(split(p.A, lo_at(p.d->A_lo), rows * K, p.st));
   }
   // 1. B down the chain, chunk by chunk (copy engines)
   for (int c = 0; c < plan.pb; ++c) {
@@ -741,12 +759,12 @@ int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K, bool gath
     for (int c = 0; c < plan.pb; ++c) {
       const int64_t Kc = plan.kb[c + 1] - plan.kb[c];
       CK(cudaStreamWaitEvent(p.st, p.d->ev_kchunk[c], 0));
-      TRY(split(p.B + plan.kb[c] * N, fptr(p.d->B_lo) + plan.kb[c] * N, Kc * N, p.st));
+      TRY(split(p.B + plan.kb[c] * N, lo_at(p.d->B_lo, plan.kb[c] * N), Kc * N, p.st));
       if (rows == 0) continue;
       GemmExtra e = ex;
       e.accumulate = c > 0;
-      TRY(gemm_chunk(p.A + plan.kb[c], fptr(p.d->A_lo) + plan.kb[c], p.B + plan.kb[c] * N,
-                     fptr(p.d->B_lo) + plan.kb[c] * N, Cr, rows, N, Kc, e, p.st));
+      TRY(gemm_chunk(p.A + plan.kb[c], lo_at(p.d->A_lo, plan.kb[c]), p.B + plan.kb[c] * N,
+                     lo_at(p.d->B_lo, plan.kb[c] * N), Cr, rows, N, Kc, e, p.st));
     }
     CK(cudaEventRecord(p.d->ev_c, p.st));
   }
@@ -842,9 +860,9 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
   partition_rows(M, world, r, &r0, &rows);
   CK(cudaEventRecord(d.ev_start, st));
   CK(cudaStreamWaitEvent(d.comm, d.ev_start, 0));
-  TRY(ws_reserve(d, {{&d.A_lo, size_t(std::max<int64_t>(rows, 1) * K) * 4},
-                     {&d.B_lo, size_t(K * N) * 4}}));
-  if (rows > 0) TRY(split(A, fptr(d.A_lo), rows * K, st));
+  TRY(ws_reserve(d, {{&d.A_lo, lo_bytes(std::max<int64_t>(rows, 1) * K)},
+                     {&d.B_lo, lo_bytes(K * N)}}));
+  if (rows > 0) TRY(split(A, lo_at(d.A_lo), rows * K, st));
   // B down the chain (copy engine on the comm stream, ordered by flags)
   for (int c = 0; c < plan.pb; ++c) {
     const int64_t off = plan.kb[c] * N, cnt = (plan.kb[c + 1] - plan.kb[c]) * N;
@@ -871,12 +889,12 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
   for (int c = 0; c < plan.pb; ++c) {
     const int64_t Kc = plan.kb[c + 1] - plan.kb[c];
     CK(cudaStreamWaitEvent(st, d.ev_kchunk[c], 0));
-    TRY(split(B + plan.kb[c] * N, fptr(d.B_lo) + plan.kb[c] * N, Kc * N, st));
+    TRY(split(B + plan.kb[c] * N, lo_at(d.B_lo, plan.kb[c] * N), Kc * N, st));
     if (rows == 0) continue;
     GemmExtra e = ex;
     e.accumulate = c > 0;
-    TRY(gemm_chunk(A + plan.kb[c], fptr(d.A_lo) + plan.kb[c], B + plan.kb[c] * N,
-                   fptr(d.B_lo) + plan.kb[c] * N, C + r0 * N, rows, N, Kc, e, st));
+    TRY(gemm_chunk(A + plan.kb[c], lo_at(d.A_lo, plan.kb[c]), B + plan.kb[c] * N,
+                   lo_at(d.B_lo, plan.kb[c] * N), C + r0 * N, rows, N, Kc, e, st));
   }
   for (int q = 0; q < world; ++q)
     if (q != r) TRY(write_flag(st, flag_cdone(x.peerF[q], r), s));
@@ -981,10 +999,10 @@ int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M
   TRY(ws_reserve(d, {{&d.A_h, size_t(M * K) * 4},
                      {&d.B_h, size_t(K * N) * 4},
                      {&d.C_h, size_t(M * N) * 4},
-                     {&d.A_lo, size_t(M * K) * 4},
-                     {&d.B_lo, size_t(K * N) * 4}}));
-  float *Ad = fptr(d.A_h), *Bd = fptr(d.B_h), *Cd = fptr(d.C_h), *Alo = fptr(d.A_lo),
-        *Blo = fptr(d.B_lo);
+                     {&d.A_lo, lo_bytes(M * K)},
+                     {&d.B_lo, lo_bytes(K * N)}}));
+  float *Ad = fptr(d.A_h), *Bd = fptr(d.B_h), *Cd = fptr(d.C_h), *Alo = lo_at(d.A_lo),
+        *Blo = lo_at(d.B_lo);
   // host -> device: (early A columns, B rows) per K-chunk, then the late A row blocks
   for (int c = 0; c < P; ++c) {
     const int64_t Kc = kb[c + 1] - kb[c];
@@ -1009,15 +1027,16 @@ int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M
   for (int c = 0; c < P; ++c) {
     const int64_t Kc = kb[c + 1] - kb[c];
     CK(cudaStreamWaitEvent(d.compute, d.ev_kchunk[c], 0));
-    TRY(split(Bd + kb[c] * N, Blo + kb[c] * N, Kc * N, d.compute));
+    TRY(split(Bd + kb[c] * N, at(Blo, kb[c] * N), Kc * N, d.compute));
     if (Me == 0) continue;
-    CK(timed(1, d.compute, [&] {
-      return launch_split_lo_2d(Ad + kb[c], Alo + kb[c], Me, Kc, K, d.compute);
-    }));
+    if (Alo)
+      CK(timed(1, d.compute, [&] {
+        return launch_split_lo_2d(Ad + kb[c], Alo + kb[c], Me, Kc, K, d.compute);
+      }));
     GemmExtra e = ex;
     e.accumulate = c > 0;
-    TRY(gemm_chunk(Ad + kb[c], Alo + kb[c], Bd + kb[c] * N, Blo + kb[c] * N, Cd, Me, N, Kc, e,
-                   d.compute));
+    TRY(gemm_chunk(Ad + kb[c], at(Alo, kb[c]), Bd + kb[c] * N, at(Blo, kb[c] * N), Cd, Me, N,
+                   Kc, e, d.compute));
   }
   if (Me > 0) {
     CK(cudaEventRecord(d.ev_c, d.compute));
@@ -1029,8 +1048,9 @@ int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M
     const int64_t q0 = Me + (M - Me) * q / Q, q1 = Me + (M - Me) * (q + 1) / Q;
     CK(cudaStreamWaitEvent(d.compute, d.ev_rchunk[q], 0));
     if (q1 > q0) {
-      TRY(split(Ad + q0 * K, Alo + q0 * K, (q1 - q0) * K, d.compute));
-      TRY(gemm(Ad + q0 * K, Alo + q0 * K, Bd, Blo, Cd + q0 * N, q1 - q0, N, K, N, d.compute));
+      TRY(split(Ad + q0 * K, at(Alo, q0 * K), (q1 - q0) * K, d.compute));
+      TRY(gemm(Ad + q0 * K, at(Alo, q0 * K), Bd, Blo, Cd + q0 * N, q1 - q0, N, K, N,
+               d.compute));
     }
     CK(cudaEventRecord(d.ev_done[q], d.compute));
     CK(cudaStreamWaitEvent(d.d2h, d.ev_done[q], 0));
@@ -1613,7 +1633,7 @@ int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const
                         int promote_kblocks, int cta_group, void *stream) {
   if (cta_group < 0 || cta_group > 2)
     return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_3xtf32_ex: cta_group must be 0, 1 or 2");
-  if (!A || !B || !C || (terms == 3 && (!A_lo || !B_lo)) || (terms != 1 && terms != 3))
+  if (!A || !B || !C || (!A_lo) != (!B_lo) || (terms != 1 && terms != 3))
     return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_3xtf32: bad pointers/terms");
   TRY(check_dims(M, N, K));
   if ((K & 3) || (N & 3) || (ldc & 3) || ldc < N || !aligned16(A) || !aligned16(B) ||

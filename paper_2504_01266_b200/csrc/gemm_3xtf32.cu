@@ -7,7 +7,9 @@
 //
 //   * fp32 accuracy from TF32 tensor cores (BASELINE.json north_star (3)): x = hi + lo with
 //     hi = the tensor core's own TF32 reading of the raw fp32 bits (truncation, measured)
-//     and lo = x - hi (exact), produced by split_lo_kernel. Per 8-wide k step three
+//     and lo = x - hi (exact), computed in shared memory from the raw tile each k-block
+//     (transform warps; or, GIGA_LO_PRESPLIT=1, TMA-loaded from arrays split_lo_kernel
+//     wrote -- twice the operand traffic, kept for comparison). Per 8-wide k step three
 //     tcgen05.mma.kind::tf32 are issued into one TMEM accumulator, small terms first:
 //     a_lo*b_hi, a_hi*b_lo, a_hi*b_hi (a_lo*b_lo, ~2^-20 relative, is dropped). hi is never
 //     materialised: the MMA is fed the raw fp32 tile and reads only its TF32 part.
@@ -21,13 +23,19 @@
 //     TMEM. Per SM this halves the B operand traffic (smem and L2) of the 1-CTA tile.
 //     CG = 1 (128 x 256 per CTA) serves small problems.
 //   * Warp specialisation, persistent clusters (one CTA per SM, 1 CTA/SM by smem):
-//       warp 0 lane 0  TMA producer: A, A_lo tiles (K-major, 64B swizzle) and B, B_lo tiles
-//                      (N-major, 128B/32B-atom swizzle) into a smem ring (mbarriers)
-//       warp 1 lane 0  MMA issuer (leader CTA): 3 UMMAs per k8; tcgen05.commit frees smem
-//                      stages in both CTAs and publishes finished accumulators
+//       warp 0 lane 0  TMA producer: raw A tiles (K-major, 64B swizzle) and B tiles
+//                      (N-major, 128B/32B-atom swizzle) into a smem ring (mbarriers `full`)
+//       warps 10..11   transform: wait `full`, write lo = x - tf32(x) of both tiles next to
+//                      them (same swizzled offsets: the map is elementwise), proxy fence,
+//                      arrive on the leader's `lofull`
+//       warp 1 lane 0  MMA issuer (leader CTA): waits `lofull`, 3 UMMAs per k8;
+//                      tcgen05.commit frees smem stages in both CTAs and publishes finished
+//                      accumulators
 //       warps 2..9     epilogue: tcgen05.ld TMEM -> registers, RN fp32 promotion adds,
 //                      swizzled smem staging -> TMA bulk stores (reduce-add when a K-chunked
 //                      pipeline accumulates) into the shard's rows of C.
+//     Computing lo on chip halves the L2 -> SM operand traffic and the HBM footprint of the
+//     3xTF32 operands (measured: -11% GEMM time at 32768^3 for the same MMAs).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -46,7 +54,9 @@ constexpr int BM = 128;  // rows of A per CTA (UMMA M per CTA)
 constexpr int BN = 256;  // UMMA N: columns of the tile (a CTA pair stages 128 each)
 constexpr int BK = 16;   // k-block: two k8 UMMA steps
 constexpr int NUM_EPI_WARPS = 8;
-constexpr int NUM_THREADS = 64 + NUM_EPI_WARPS * 32;
+constexpr int NUM_XFORM_WARPS = 2;
+constexpr int XFORM_WARP0 = 2 + NUM_EPI_WARPS;
+constexpr int NUM_THREADS = 64 + NUM_EPI_WARPS * 32 + NUM_XFORM_WARPS * 32;
 constexpr uint32_t A_BYTES = BM * BK * 4;        // 8 KiB: 128 rows x 64 B
 constexpr uint32_t B_CHUNK_BYTES = BK * 32 * 4;  // 2 KiB: one 32-column chunk of B
 constexpr uint32_t ACC_COLS = BN;                // fp32 accumulator: 1 TMEM column per n
@@ -78,6 +88,7 @@ struct GemmParams {
   int group_m;    // L2 raster: consecutive tiles walk group_m M-tiles before the next N-tile
   unsigned *wave_sync;  // non-null: zeroed counter for the producers' per-wave barrier
   int n_cdst;     // C destinations in CMaps (1 + peers when the gather is fused)
+  int lo_smem;    // 1: lo tiles computed in smem from the raw tiles; 0: TMA-loaded (A_lo, B_lo)
 };
 
 // C tensor maps: [0] this GPU's C, [1..] the same rows of the peers' C_full buffers.
@@ -115,6 +126,16 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
          (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
+// ---- split: lo = x - tf32(x) ------------------------------------------------------------
+// tf32(x) is what kind::tf32 reads from raw fp32 bits: the top 19 bits (sign, exponent,
+// 10 mantissa bits), i.e. truncation toward zero of the low 13 mantissa bits (measured on
+// B200 by tests/test_gpu.py::test_probe_tf32_operand_conversion_is_truncation). x - tf32(x)
+// is exact in fp32 (same sign, the 13 low bits of x's significand).
+__device__ __forceinline__ float tf32_lo(float x) {
+  const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  return __fsub_rn(x, hi);
+}
+
 __device__ __forceinline__ void tile_coords(int t, const GemmParams &p, int &mb, int &nb) {
   const int group_size = p.group_m * p.n_tiles;
   const int g = t / group_size;
@@ -143,7 +164,9 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
   uint64_t *empty = full + STAGES;
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  uint64_t *lofull = tempty + 2;  // stage ready for the MMA: raw + lo tiles of both CTAs
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(lofull + STAGES);
+  uint8_t *sig = reinterpret_cast<uint8_t *>(lofull + STAGES) + 16;  // 16 B aligned, 32 B
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -155,7 +178,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
-    if (p.terms == 3) {
+    if (p.terms == 3 && !p.lo_smem) {
       ptx::prefetch_tmap(&tmAlo);
       ptx::prefetch_tmap(&tmBlo);
     }
@@ -163,6 +186,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&lofull[s], NUM_XFORM_WARPS);
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
@@ -188,7 +212,8 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
   if (warp == 0) {
     // ======================= TMA producer (both CTAs) =======================
     if (lane == 0) {
-      const uint32_t tx_cta = p.terms == 3 ? T::STAGE_BYTES : (A_BYTES + T::B_BYTES);
+      const bool load_lo = p.terms == 3 && !p.lo_smem;
+      const uint32_t tx_cta = load_lo ? T::STAGE_BYTES : (A_BYTES + T::B_BYTES);
       int stage = 0;
       uint32_t phase = 0;
       int wave = 0;
@@ -221,33 +246,17 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
           uint8_t *sB = sA + 2 * A_BYTES;
           uint8_t *sBlo = sB + T::B_BYTES;
           const int k0 = kb * BK;
-          if (CG == 1) {
-            ptx::mbar_expect_tx(&full[stage], tx_cta);
-            ptx::tma_load_2d(sA, &tmA, &full[stage], k0, m0);
+          // every CTA's tiles land on its own `full` barrier (its transform warps wait there)
+          ptx::mbar_expect_tx(&full[stage], tx_cta);
+          ptx::tma_load_2d(sA, &tmA, &full[stage], k0, m0);
+#pragma unroll
+          for (int c = 0; c < T::B_COLS / 32; ++c)
+            ptx::tma_load_2d(sB + c * B_CHUNK_BYTES, &tmB, &full[stage], n0 + 32 * c, k0);
+          if (load_lo) {
+            ptx::tma_load_2d(sAlo, &tmAlo, &full[stage], k0, m0);
 #pragma unroll
             for (int c = 0; c < T::B_COLS / 32; ++c)
-              ptx::tma_load_2d(sB + c * B_CHUNK_BYTES, &tmB, &full[stage], n0 + 32 * c, k0);
-            if (p.terms == 3) {
-              ptx::tma_load_2d(sAlo, &tmAlo, &full[stage], k0, m0);
-#pragma unroll
-              for (int c = 0; c < T::B_COLS / 32; ++c)
-                ptx::tma_load_2d(sBlo + c * B_CHUNK_BYTES, &tmBlo, &full[stage], n0 + 32 * c,
-                                 k0);
-            }
-          } else {
-            // both CTAs' bytes are counted on the leader's full barrier
-            if (leader) ptx::mbar_expect_tx(&full[stage], 2 * tx_cta);
-            const uint32_t bar = ptx::smem_u32(&full[stage]) & ptx::kPeerBitMask;
-            ptx::tma_load_2d_cg2(sA, &tmA, bar, k0, m0);
-#pragma unroll
-            for (int c = 0; c < T::B_COLS / 32; ++c)
-              ptx::tma_load_2d_cg2(sB + c * B_CHUNK_BYTES, &tmB, bar, n0 + 32 * c, k0);
-            if (p.terms == 3) {
-              ptx::tma_load_2d_cg2(sAlo, &tmAlo, bar, k0, m0);
-#pragma unroll
-              for (int c = 0; c < T::B_COLS / 32; ++c)
-                ptx::tma_load_2d_cg2(sBlo + c * B_CHUNK_BYTES, &tmBlo, bar, n0 + 32 * c, k0);
-            }
+              ptx::tma_load_2d(sBlo + c * B_CHUNK_BYTES, &tmBlo, &full[stage], n0 + 32 * c, k0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -273,7 +282,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
           const int kb_end = min(kb + p.p_kb, p.n_kb);
           uint32_t acc = 0;
           for (; kb < kb_end; ++kb) {
-            ptx::mbar_wait(&full[stage], phase);
+            ptx::mbar_wait(&lofull[stage], phase);
             ptx::tc_fence_after();
             const uint32_t sA = ptx::smem_u32(smem + stage * T::STAGE_BYTES);
             const uint32_t sAlo = sA + A_BYTES;
@@ -315,6 +324,65 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
             ptx::mma_commit(&tfull[buf]);
           else
             ptx::mma_commit_cg2(&tfull[buf], 0x3);
+        }
+      }
+    }
+  } else if (warp >= XFORM_WARP0) {
+    // ======================= transform (2 warps per CTA) =======================
+    // lo = x - tf32(x) of this CTA's raw A and B tiles, written at the same offsets in the lo
+    // slots (the swizzle is a permutation of 16-byte chunks and the map is elementwise).
+    // 64 threads, consecutive 16-byte chunks per warp instruction: conflict-free.
+    const int xt = threadIdx.x - XFORM_WARP0 * 32;
+    const bool do_lo = p.terms == 3 && p.lo_smem;
+    constexpr int NA = int(A_BYTES / 16) / (NUM_XFORM_WARPS * 32);    // 8
+    constexpr int NB = int(T::B_BYTES / 16) / (NUM_XFORM_WARPS * 32); // 8 (CG=2), 16 (CG=1)
+    // Pair protocol for `lofull[s]` (leader's): its own two transform warps arrive (the first
+    // also expects 16 transaction bytes per peer warp), each peer transform warp completes 16
+    // bytes with an async-proxy bulk signal after its proxy fence (ptx::bulk_signal_leader).
+    const uint32_t lofull_leader = ptx::smem_u32(&lofull[0]) & ptx::kPeerBitMask;
+    const uint32_t sig_leader = ptx::smem_u32(sig) & ptx::kPeerBitMask;
+    const int xw = warp - XFORM_WARP0;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+      for (int kb = 0; kb < p.n_kb; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
+        if (do_lo) {
+          const uint32_t sA = ptx::smem_u32(smem + stage * T::STAGE_BYTES);
+          const uint32_t sB = sA + 2 * A_BYTES;
+          float4 va[NA], vb[NB];
+#pragma unroll
+          for (int i = 0; i < NA; ++i)
+            va[i] = ptx::ld_shared_v4(sA + uint32_t(i * NUM_XFORM_WARPS * 32 + xt) * 16);
+#pragma unroll
+          for (int i = 0; i < NB; ++i)
+            vb[i] = ptx::ld_shared_v4(sB + uint32_t(i * NUM_XFORM_WARPS * 32 + xt) * 16);
+#pragma unroll
+          for (int i = 0; i < NA; ++i)
+            ptx::st_shared_v4(sA + A_BYTES + uint32_t(i * NUM_XFORM_WARPS * 32 + xt) * 16,
+                              tf32_lo(va[i].x), tf32_lo(va[i].y), tf32_lo(va[i].z),
+                              tf32_lo(va[i].w));
+#pragma unroll
+          for (int i = 0; i < NB; ++i)
+            ptx::st_shared_v4(sB + T::B_BYTES + uint32_t(i * NUM_XFORM_WARPS * 32 + xt) * 16,
+                              tf32_lo(vb[i].x), tf32_lo(vb[i].y), tf32_lo(vb[i].z),
+                              tf32_lo(vb[i].w));
+          ptx::fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 1 || leader) {
+            if (CG == 2 && xw == 0)
+              ptx::mbar_arrive_expect_tx(&lofull[stage], 16 * NUM_XFORM_WARPS);
+            else
+              ptx::mbar_arrive(&lofull[stage]);
+          } else {
+            ptx::bulk_signal_leader(sig_leader, sig + 16, lofull_leader + uint32_t(stage) * 8);
+          }
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
@@ -406,15 +474,6 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
   }
 }
 
-// ---- split: lo = x - tf32(x) ------------------------------------------------------------
-// tf32(x) is what kind::tf32 reads from raw fp32 bits: the top 19 bits (sign, exponent,
-// 10 mantissa bits), i.e. truncation toward zero of the low 13 mantissa bits (measured on
-// B200 by tests/test_gpu.py::test_probe_tf32_operand_conversion_is_truncation). x - tf32(x)
-// is exact in fp32 (same sign, the 13 low bits of x's significand).
-__device__ __forceinline__ float tf32_lo(float x) {
-  const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  return __fsub_rn(x, hi);
-}
 
 __global__ void __launch_bounds__(256) split_lo_kernel(const float *__restrict__ x,
                                                        float *__restrict__ lo, int64_t n) {
@@ -581,7 +640,8 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || ldc > INT32_MAX)
     return cudaErrorInvalidValue;
   if (terms != 1 && terms != 3) return cudaErrorInvalidValue;
-  if (terms == 3 && (!A_lo || !B_lo)) return cudaErrorInvalidValue;
+  if (terms == 3 && (!A_lo) != (!B_lo)) return cudaErrorInvalidValue;  // both or neither
+  const bool lo_smem = terms == 3 && !A_lo;
   if (ensure_tma_encoder() != 0) return cudaErrorNotSupported;
 
   int num_sms = num_sms_current();
@@ -598,7 +658,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   for (int i = 0; i < ex->n_peer_c; ++i)
     if (!make_map(&tC.m[1 + i], ex->peer_c[i], N, M, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
-  if (terms == 3) {
+  if (terms == 3 && !lo_smem) {
     if (!make_map(&tAlo, A_lo, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
         !make_map(&tBlo, B_lo, N, K, ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
       return cudaErrorInvalidValue;
@@ -614,6 +674,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.ldc = int(ldc);
   p.accumulate = ex->accumulate ? 1 : 0;
   p.terms = terms;
+  p.lo_smem = lo_smem ? 1 : 0;
   p.n_kb = int((K + BK - 1) / BK);
   int pk = promote_kblocks < 0 ? default_promote_kblocks() : promote_kblocks;
   p.p_kb = (pk == 0 || pk > p.n_kb) ? p.n_kb : pk;

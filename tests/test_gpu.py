@@ -192,22 +192,60 @@ def test_cta_group_variants_bit_exact(giga, torch_cuda, M, N, K, cta_group):
     assert ok, st
 
 
+@pytest.mark.parametrize("lo", ["smem", "presplit"])
 @pytest.mark.parametrize("cta_group", [1, 2])
-def test_cta_group_variants_tolerance(giga, torch_cuda, cta_group):
+def test_cta_group_variants_tolerance(giga, torch_cuda, cta_group, lo):
+    """Non-integer inputs, so the lo terms matter: lo computed in shared memory by the
+    transform warps (A_lo = B_lo = NULL, the product path) or TMA-loaded from split arrays."""
     torch = torch_cuda
     M, N, K = 700, 900, 3000
     A = synth.gen_matrix(M, K, synth.MATRIX_A, "d1")
     B = synth.gen_matrix(K, N, synth.MATRIX_B, "d1")
     dA, dB = _dev(torch, A), _dev(torch, B)
-    dAlo, dBlo = torch.empty_like(dA), torch.empty_like(dB)
-    giga.split_lo(dA, dAlo)
-    giga.split_lo(dB, dBlo)
+    dAlo = dBlo = None
+    if lo == "presplit":
+        dAlo, dBlo = torch.empty_like(dA), torch.empty_like(dB)
+        giga.split_lo(dA, dAlo)
+        giga.split_lo(dB, dBlo)
     dC = torch.full((M, N), float("nan"), device="cuda")
     giga.gemm_3xtf32(dA, dAlo, dB, dBlo, dC, M, N, K, cta_group=cta_group)
     torch.cuda.synchronize()
     Cref, S = oracle.gemm(A, B)
     ok, st = check_close(dC.cpu().numpy(), Cref, S)
     assert ok, st
+
+
+@pytest.mark.parametrize("cta_group", [1, 2])
+@pytest.mark.parametrize("M,N,K,dist", [(1, 4, 4, "d2"), (257, 516, 36, "d4"),
+                                        (600, 1000, 1028, "d2"), (1500, 2048, 4100, "d4")])
+def test_lo_in_smem_equals_presplit_bitwise(giga, torch_cuda, M, N, K, dist, cta_group):
+    """The in-kernel lo (transform warps) and split_lo_kernel's lo are the same function of
+    the same bits, fed to the same MMAs in the same order: C must agree bit for bit. Any
+    stale, torn or mis-addressed lo tile in shared memory breaks this."""
+    torch = torch_cuda
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, dist)
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
+    dA, dB = _dev(torch, A), _dev(torch, B)
+    dAlo, dBlo = torch.empty_like(dA), torch.empty_like(dB)
+    giga.split_lo(dA, dAlo)
+    giga.split_lo(dB, dBlo)
+    C1 = torch.full((M, N), float("nan"), device="cuda")
+    C2 = torch.full((M, N), float("nan"), device="cuda")
+    giga.gemm_3xtf32(dA, None, dB, None, C1, M, N, K, cta_group=cta_group)
+    giga.gemm_3xtf32(dA, dAlo, dB, dBlo, C2, M, N, K, cta_group=cta_group)
+    torch.cuda.synchronize()
+    assert torch.equal(C1.view(torch.int32), C2.view(torch.int32))
+    Cref, S = oracle.gemm(A, B)
+    ok, st = check_close(C1.cpu().numpy(), Cref, S)
+    assert ok, st
+
+
+def test_gemm_lo_pointers_both_or_neither(giga, torch_cuda):
+    torch = torch_cuda
+    d = torch.ones((8, 8), device="cuda")
+    with pytest.raises(giga.GigaError) as e:
+        giga.gemm_3xtf32(d, d, d, None, torch.empty_like(d), 8, 8, 8)
+    assert e.value.status == "GIGA_ERR_INVALID_ARG"
 
 
 PIPE_CASES = [(1000, 1000, 4096, "d3"), (777, 260, 2052, "d3"), (1024, 512, 3072, "d1"),
