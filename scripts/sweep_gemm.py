@@ -1,4 +1,4 @@
-"""Shard-GEMM kernel time vs promotion interval (and tile config), 1 GPU, CUDA events."""
+"""Shard-GEMM kernel time vs promotion interval (and tile config, LO=presplit), 1 GPU, CUDA events."""
 import json, os, sys, time
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -11,9 +11,11 @@ if os.environ.get("MNK"):
 dev = torch.device("cuda", 0)
 A = synth.gen_rows_torch(0, M, K, 1, "d2", device=dev)
 B = synth.gen_rows_torch(0, K, N, 2, "d2", device=dev)
-Alo, Blo = torch.empty_like(A), torch.empty_like(B)
 C = torch.empty((M, N), device=dev)
-giga.split_lo(A, Alo); giga.split_lo(B, Blo)
+Alo = Blo = None  # lo computed in the GEMM's shared memory (the product path)
+if os.environ.get("LO") == "presplit":  # the pre-split design, for comparison
+    Alo, Blo = torch.empty_like(A), torch.empty_like(B)
+    giga.split_lo(A, Alo); giga.split_lo(B, Blo)
 torch.cuda.synchronize()
 res = {}
 for pk in [int(x) for x in os.environ.get("PKS", "4,8,16,32").split(",")]:
