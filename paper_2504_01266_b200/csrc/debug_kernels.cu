@@ -12,6 +12,24 @@
 namespace giga {
 namespace dbg {
 
+// Nothing but the pair TMEM allocation the GEMM does (cta_group::2 alloc, cluster sync,
+// dealloc): isolates the toolchain's own alloc handshake for compute-sanitizer racecheck.
+__global__ void __cluster_dims__(2, 1, 1) tmem_pair_alloc_kernel(int *out) {
+  __shared__ uint32_t slot;
+  if (threadIdx.x < 32) ptx::tmem_alloc_cg2(&slot, 512);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t base = slot;
+  if (threadIdx.x == 0) out[blockIdx.x] = int(base);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (threadIdx.x < 32) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_cg2(base, 512);
+  }
+}
+
 // TMA one box into smem, dump the raw smem bytes (box_bytes) to out.
 __global__ void tma_dump_kernel(const __grid_constant__ CUtensorMap tm, int c0, int c1,
                                 uint32_t box_bytes, float *out) {
@@ -134,6 +152,12 @@ extern "C" int giga_dbg_mma_once(const float *a_img, int a_bytes, const float *b
                        smem);
   dbg::mma_once_kernel<<<1, 128, smem>>>(a_img, a_bytes, b_img, b_bytes, a_lbo, a_sbo,
                                          a_layout, b_lbo, b_sbo, b_layout, idesc, n, D);
+  if (cudaGetLastError() != cudaSuccess) return -3;
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : -4;
+}
+
+extern "C" int giga_dbg_tmem_pair_alloc(int nclusters, int *out) {
+  dbg::tmem_pair_alloc_kernel<<<2 * nclusters, 64>>>(out);
   if (cudaGetLastError() != cudaSuccess) return -3;
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : -4;
 }

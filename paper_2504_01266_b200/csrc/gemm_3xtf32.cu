@@ -194,7 +194,12 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) {
+  // TMEM allocation by warp 0: with cta_group::2 the allocation handshakes with the peer
+  // through a barrier in reserved shared memory (0x58) that racecheck sees written by warp 0
+  // (lane 31, outside this kernel's code); allocating from another warp ran correctly but was
+  // reported as a RAW hazard on that barrier.
+  if (warp == 0) {
+    __syncwarp();
     if (CG == 2)
       ptx::tmem_alloc_cg2(tmem_slot, TMEM_COLS);
     else
@@ -465,7 +470,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     ptx::cluster_sync();  // no CTA leaves while its peer may still signal its barriers
   else
     __syncthreads();
-  if (warp == 1) {
+  if (warp == 0) {
     ptx::tc_fence_after();
     if (CG == 2)
       ptx::tmem_dealloc_cg2(tmem_base, TMEM_COLS);
