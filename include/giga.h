@@ -171,6 +171,19 @@ int giga_pipeline_plan(int64_t M, int64_t N, int64_t K, int world, int *kchunks,
 int giga_plan_block(int64_t M, int world, int rchunks, int owner, int q, int64_t *row0,
                     int64_t *rows);
 
+/* The schedule giga_matmul uses for HOST buffers on one GPU (inputs built
+ * on the host, results copied back; PCIe both ways overlapped with the GEMM):
+ *   phase 1: rows [0, *Me): K-chunk c = [kb[c], kb[c+1]) of A's columns and B's rows is
+ *            copied host->device, then its GEMM accumulates into C[0:Me];
+ *   phase 2: row blocks [rb[q], rb[q+1]) (rb[0] = *Me, rb[*Q] = M) over the full K; each block's
+ *            C rows are copied back while the next computes (the early rows after phase 1).
+ * Chosen by a three-engine (H2D, GEMM, D2H) model over a few thousand candidates; *t_model is
+ * its makespan in seconds. kb and rb need room for 17 entries each. num_sms <= 0 means 148.
+ * Model rates: $GIGA_HOST_H2D_GBS, $GIGA_HOST_D2H_GBS (50), $GIGA_HOST_GEMM_TFLOPS (255).
+ * No GPU needed. Errors: INVALID_ARG. */
+int giga_host_plan(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *Me, int *P,
+                   int64_t *kb, int *Q, int64_t *rb, double *t_model);
+
 /* Peer-to-peer transport for the rank API ($GIGA_TRANSPORT=p2p, set before giga_rank_init;
  * no NCCL communicator is created then, and several ranks may share one device). Each rank
  * registers the B and C_full buffers it will pass to giga_matmul_rank:

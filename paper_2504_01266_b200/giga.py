@@ -27,7 +27,7 @@ EXPORTS = (
     "giga_matmul_rank", "giga_split_lo", "giga_gemm_3xtf32", "giga_gemm_3xtf32_ex",
     "giga_timing_enable", "giga_timing_reset", "giga_timing_read", "giga_pipeline_plan",
     "giga_plan_block", "giga_dot", "giga_l2norm", "giga_dot_rank", "giga_init_devices",
-    "giga_rank_p2p_export", "giga_rank_p2p_import",
+    "giga_rank_p2p_export", "giga_rank_p2p_import", "giga_host_plan",
 )
 P2P_BLOB_BYTES = 256
 
@@ -79,6 +79,9 @@ def _load():
         "giga_init_devices": ([p, i32], i32),
         "giga_rank_p2p_export": ([p, p, p], i32),
         "giga_rank_p2p_import": ([p, i32], i32),
+        "giga_host_plan": ([i64, i64, i64, i32, P64, ctypes.POINTER(ctypes.c_int), P64,
+                            ctypes.POINTER(ctypes.c_int), P64,
+                            ctypes.POINTER(ctypes.c_double)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -230,6 +233,16 @@ def plan_block(M: int, world: int, rchunks: int, owner: int, q: int):
     r0, rows = ctypes.c_int64(), ctypes.c_int64()
     _check(lib.giga_plan_block(M, world, rchunks, owner, q, ctypes.byref(r0), ctypes.byref(rows)))
     return r0.value, rows.value
+
+
+def host_plan(M: int, N: int, K: int, num_sms: int = 148):
+    """The host-buffer schedule of giga_matmul on one GPU (see include/giga.h)."""
+    Me, P, Q, t = ctypes.c_int64(), ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+    kb, rb = (ctypes.c_int64 * 17)(), (ctypes.c_int64 * 17)()
+    _check(lib.giga_host_plan(M, N, K, num_sms, ctypes.byref(Me), ctypes.byref(P), kb,
+                              ctypes.byref(Q), rb, ctypes.byref(t)))
+    return {"Me": Me.value, "kb": list(kb[:P.value + 1]), "rb": list(rb[:Q.value + 1]),
+            "t_model": t.value}
 
 
 # ---- building blocks --------------------------------------------------------------------
