@@ -1,0 +1,341 @@
+// runtime.cpp -- libgiga's host runtime: errors, library state, kernel timing, the per-GPU
+// workspace cache, the row-block partitioner, argument checks and the one-shard compute
+// (each GPU multiplies its row block of A by B).
+#include "runtime.h"
+
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+
+namespace giga {
+
+thread_local std::string t_err;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return code;
+}
+
+int fail_cuda(cudaError_t e, const char *what, const char *file, int line) {
+  cudaGetLastError();  // clear a non-sticky error so the next call starts clean
+  const int code = (e == cudaErrorMemoryAllocation) ? GIGA_ERR_OOM : GIGA_ERR_CUDA;
+  const char *base = strrchr(file, '/');
+  return fail(code, "%s failed at %s:%d: %s (%s)", what, base ? base + 1 : file, line,
+              cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+State g;
+std::mutex g_tmu;
+bool g_timing = false;
+std::vector<TimeRec> g_tpending;
+std::vector<std::pair<int, cudaEvent_t>> g_tpool;
+double g_tms[2] = {0, 0};
+int64_t g_tcount[2] = {0, 0};
+
+cudaEvent_t pool_event(int dev) {
+  for (size_t i = 0; i < g_tpool.size(); ++i)
+    if (g_tpool[i].first == dev) {
+      cudaEvent_t e = g_tpool[i].second;
+      g_tpool.erase(g_tpool.begin() + i);
+      return e;
+    }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return e;
+}
+
+// ---------------------------------------------------------------------------------------
+// workspace: grow-only per-GPU buffers, reserved transactionally so a failed call leaves the
+// device memory footprint exactly as it found it.
+
+int ws_reserve(DevCtx &d, std::initializer_list<std::pair<Buf *, size_t>> req) {
+  std::vector<std::pair<Buf *, void *>> fresh;
+  for (auto &r : req) {
+    if (r.first->bytes >= r.second) continue;
+    bool dup = false;
+    for (auto &f : fresh) dup |= (f.first == r.first);
+    if (dup) continue;
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, r.second);
+    if (e != cudaSuccess) {
+      for (auto &f : fresh) cudaFree(f.second);
+      return fail_cuda(e, "cudaMalloc(workspace)", __FILE__, __LINE__);
+    }
+    fresh.push_back({r.first, p});
+  }
+  for (auto &f : fresh) {
+    size_t want = 0;
+    for (auto &r : req)
+      if (r.first == f.first) want = std::max(want, r.second);
+    if (f.first->p) cudaFree(f.first->p);
+    f.first->p = f.second;
+    f.first->bytes = want;
+  }
+  return GIGA_OK;
+}
+
+void ws_free(DevCtx &d) {
+  for (Buf *b :
+       {&d.A_lo, &d.B_lo, &d.A_pad, &d.B_pad, &d.C_pad, &d.A_h, &d.B_h, &d.C_h, &d.vec_ws}) {
+    if (b->p) cudaFree(b->p);
+    b->p = nullptr;
+    b->bytes = 0;
+  }
+}
+
+float *fptr(Buf &b) { return static_cast<float *>(b.p); }
+
+int ctx_create(DevCtx &d, int dev) {
+  d.dev = dev;
+  CK(cudaSetDevice(dev));
+  CK(cudaStreamCreateWithFlags(&d.compute, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&d.comm, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&d.d2h, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&d.ev_b, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&d.ev_c, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&d.ev_start, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&d.ev_last, cudaEventDisableTiming));
+  for (auto *v : {&d.ev_kchunk, &d.ev_rchunk, &d.ev_done}) {
+    v->assign(kMaxChunks, nullptr);
+    for (auto &e : *v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  return GIGA_OK;
+}
+
+void ctx_destroy(DevCtx &d) {
+  if (d.dev < 0) return;
+  cudaSetDevice(d.dev);
+  cudaDeviceSynchronize();
+  ws_free(d);
+  if (d.compute) cudaStreamDestroy(d.compute);
+  if (d.comm) cudaStreamDestroy(d.comm);
+  if (d.d2h) cudaStreamDestroy(d.d2h);
+  for (cudaEvent_t e : {d.ev_b, d.ev_c, d.ev_start, d.ev_last})
+    if (e) cudaEventDestroy(e);
+  for (auto *v : {&d.ev_kchunk, &d.ev_rchunk, &d.ev_done, &d.ev_trace})
+    for (cudaEvent_t e : *v)
+      if (e) cudaEventDestroy(e);
+  d = DevCtx{};
+}
+
+int check_sm100(int dev) {
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10)
+    return fail(GIGA_ERR_NO_DEVICE, "device %d is sm_%d%d, this build is sm_100a only", dev,
+                prop.major, prop.minor);
+  return GIGA_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// one shard on one GPU: split A and B into TF32 hi/lo and run the tensor-core GEMM into
+// C (rows x N, row stride ldc). If `wait_b` is given, B is only touched after it fires (the
+// A split overlaps the distribution of B).
+
+// The lo = x - tf32(x) operands are computed inside the GEMM from the raw tiles (the
+// default). GIGA_LO_PRESPLIT=1 restores the pre-split design (split_lo_kernel writes lo
+// arrays to HBM, the GEMM TMA-loads them: twice the operand traffic; for comparison).
+bool lo_presplit() {
+  static const bool v = [] {
+    const char *e = getenv("GIGA_LO_PRESPLIT");
+    return e && *e == '1';
+  }();
+  return v;
+}
+size_t lo_bytes(int64_t elems) { return lo_presplit() ? size_t(elems) * 4 : 0; }
+float *lo_at(Buf &b, int64_t off) { return lo_presplit() ? fptr(b) + off : nullptr; }
+
+int split(const float *x, float *lo, int64_t n, cudaStream_t st) {
+  if (!lo) return GIGA_OK;  // lo computed in the GEMM
+  CK(timed(1, st, [&] { return launch_split_lo(x, lo, n, st); }));
+  return GIGA_OK;
+}
+
+int gemm(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
+         int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st) {
+  CK(timed(0, st, [&] {
+    return launch_gemm_3xtf32(A, Alo, B, Blo, C, M, N, K, ldc, 3, -1, st);
+  }));
+  return GIGA_OK;
+}
+
+int shard_compute(DevCtx &d, cudaStream_t st, const float *A, int64_t rows, const float *B,
+                  float *C, int64_t ldc, int64_t N, int64_t K, cudaEvent_t wait_b) {
+  if (rows <= 0) {
+    if (wait_b) CK(cudaStreamWaitEvent(st, wait_b, 0));
+    return GIGA_OK;
+  }
+  const bool direct = (K % 4 == 0) && (N % 4 == 0) && (ldc % 4 == 0) && aligned16(A) &&
+                      aligned16(B) && aligned16(C);
+  if (direct) {
+    TRY(ws_reserve(d, {{&d.A_lo, lo_bytes(rows * K)}, {&d.B_lo, lo_bytes(K * N)}}));
+    TRY(split(A, lo_at(d.A_lo), rows * K, st));
+    if (wait_b) CK(cudaStreamWaitEvent(st, wait_b, 0));
+    TRY(split(B, lo_at(d.B_lo), K * N, st));
+    return gemm(A, lo_at(d.A_lo), B, lo_at(d.B_lo), C, rows, N, K, ldc, st);
+  }
+  // Unaligned shapes (H6): zero-padded copies with K, N rounded up to multiples of 4. Zero
+  // columns of A / rows of B add nothing to any dot product.
+  const int64_t K4 = (K + 3) / 4 * 4, N4 = (N + 3) / 4 * 4;
+  TRY(ws_reserve(d, {{&d.A_pad, size_t(rows * K4) * 4},
+                     {&d.B_pad, size_t(K4 * N4) * 4},
+                     {&d.C_pad, size_t(rows * N4) * 4},
+                     {&d.A_lo, lo_bytes(rows * K4)},
+                     {&d.B_lo, lo_bytes(K4 * N4)}}));
+  CK(cudaMemsetAsync(d.A_pad.p, 0, size_t(rows * K4) * 4, st));
+  CK(cudaMemcpy2DAsync(d.A_pad.p, K4 * 4, A, K * 4, K * 4, rows, cudaMemcpyDeviceToDevice, st));
+  TRY(split(fptr(d.A_pad), lo_at(d.A_lo), rows * K4, st));
+  if (wait_b) CK(cudaStreamWaitEvent(st, wait_b, 0));
+  CK(cudaMemsetAsync(d.B_pad.p, 0, size_t(K4 * N4) * 4, st));
+  CK(cudaMemcpy2DAsync(d.B_pad.p, N4 * 4, B, N * 4, N * 4, K, cudaMemcpyDeviceToDevice, st));
+  TRY(split(fptr(d.B_pad), lo_at(d.B_lo), K4 * N4, st));
+  TRY(gemm(fptr(d.A_pad), lo_at(d.A_lo), fptr(d.B_pad), lo_at(d.B_lo), fptr(d.C_pad), rows, N4,
+           K4, N4, st));
+  CK(cudaMemcpy2DAsync(C, ldc * 4, d.C_pad.p, N4 * 4, N * 4, rows, cudaMemcpyDeviceToDevice,
+                       st));
+  return GIGA_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// row-block partition (floor split, the remainder to the last GPU)
+
+void partition_rows(int64_t M, int ngpus, int gi, int64_t *row0, int64_t *rows) {
+  const int64_t base = M / ngpus;
+  *row0 = int64_t(gi) * base;
+  *rows = (gi == ngpus - 1) ? M - int64_t(ngpus - 1) * base : base;
+}
+
+// ---------------------------------------------------------------------------------------
+// argument checks
+
+bool overlaps(const void *a, size_t abytes, const void *b, size_t bbytes) {
+  const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + bbytes && y < x + abytes;
+}
+
+int check_dims(int64_t M, int64_t N, int64_t K) {
+  if (M < 1 || N < 1 || K < 1)
+    return fail(GIGA_ERR_INVALID_ARG, "M, N, K must be >= 1 (got %lld, %lld, %lld)",
+                (long long)M, (long long)N, (long long)K);
+  const int64_t lim = int64_t(1) << 31;
+  if (M >= lim || N >= lim || K >= lim || M > (int64_t(1) << 62) / N ||
+      K > (int64_t(1) << 62) / N || M > (int64_t(1) << 62) / K)
+    return fail(GIGA_ERR_INVALID_ARG, "matrix dimensions too large");
+  return GIGA_OK;
+}
+
+// pointer kind: 1 = device (dev set), 0 = host
+int pointer_kind(const void *p, int *dev) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (a.type == cudaMemoryTypeDevice) {
+    *dev = a.device;
+    return 1;
+  }
+  return 0;
+}
+
+// The single-process calls are blocking ("synchronize and copy back"): they
+// start after everything already queued on the participating devices (e.g. the producer of
+// A or B on another stream) and return after their own work is done.
+int quiesce(int ngpus) {
+  for (int i = 0; i < ngpus; ++i) {
+    CK(cudaSetDevice(g.devs[i].dev));
+    CK(cudaDeviceSynchronize());
+  }
+  return GIGA_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// vector operations: per-GPU fp64 partial of a contiguous index range
+
+constexpr size_t kVecWsBytes = size_t(kDotMaxBlocks) * 8 + 64;
+
+int vec_ws(DevCtx &d) {
+  if (d.vec_ws.p) return GIGA_OK;
+  TRY(ws_reserve(d, {{&d.vec_ws, kVecWsBytes}}));
+  CK(cudaMemset(d.vec_ws.p, 0, kVecWsBytes));  // ticket starts at zero
+  return GIGA_OK;
+}
+double *vec_partials(DevCtx &d) { return static_cast<double *>(d.vec_ws.p); }
+double *vec_out(DevCtx &d) { return vec_partials(d) + kDotMaxBlocks; }
+unsigned *vec_ticket(DevCtx &d) { return reinterpret_cast<unsigned *>(vec_out(d) + 1); }
+
+int dot_partial(DevCtx &d, const float *x, const float *y, int64_t n, cudaStream_t st) {
+  TRY(vec_ws(d));
+  CK(launch_dot(x, y, n, vec_partials(d), vec_ticket(d), vec_out(d), st));
+  return GIGA_OK;
+}
+
+int sync_all(int ngpus) {
+  for (int i = 0; i < ngpus; ++i) {
+    DevCtx &d = g.devs[i];
+    CK(cudaSetDevice(d.dev));
+    CK(cudaStreamSynchronize(d.compute));
+    CK(cudaStreamSynchronize(d.comm));
+  }
+  return GIGA_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// pipeline plan and chunked GEMM (shared by the NCCL pipeline, p2p and host paths)
+
+int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
+Plan make_plan(int64_t M, int64_t K, int world, bool aligned) {
+  Plan pl;
+  int64_t rows_max = 0;
+  for (int r = 0; r < world; ++r) {
+    int64_t r0, rows;
+    partition_rows(M, world, r, &r0, &rows);
+    rows_max = std::max(rows_max, rows);
+  }
+  if (aligned) {
+    pl.pb = std::min(std::max(env_int("GIGA_BCAST_CHUNKS", 4), 1), kMaxChunks);
+    pl.pb = int(std::min<int64_t>(pl.pb, std::max<int64_t>(1, K / 512)));
+    pl.pc = std::min(std::max(env_int("GIGA_GATHER_CHUNKS", 4), 1), kMaxChunks);
+    pl.pc = int(std::min<int64_t>(pl.pc, std::max<int64_t>(1, rows_max / 256)));
+  }
+  for (int c = 0; c < pl.pb; ++c) pl.kb[c] = (K * c / pl.pb) / 16 * 16;
+  pl.kb[pl.pb] = K;
+  return pl;
+}
+
+void plan_block(int64_t M, int world, int pc, int owner, int q, int64_t *row0, int64_t *rows) {
+  int64_t o0, orows;
+  partition_rows(M, world, owner, &o0, &orows);
+  const int64_t q0 = orows * q / pc, q1 = orows * (q + 1) / pc;
+  *row0 = o0 + q0;
+  *rows = q1 - q0;
+}
+
+bool force_comm() { return env_int("GIGA_FORCE_COMM", 0) != 0; }
+
+int gemm_chunk(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
+               int64_t rows, int64_t N, int64_t Kc, const GemmExtra &ex, cudaStream_t st) {
+  CK(timed(0, st, [&] {
+    return launch_gemm_3xtf32(A, Alo, B, Blo, C, rows, N, Kc, N, 3, -1, st, 0, &ex);
+  }));
+  return GIGA_OK;
+}
+
+}  // namespace giga
