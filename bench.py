@@ -5,8 +5,8 @@
     python bench.py --impl reference ...                      (the CPU fp64 oracle arm)
 
 One step = the whole hot path over one synthetic problem: broadcast B from
-rank 0 (N > 1), split A and B into TF32 hi/lo, the 3xTF32 tcgen05 shard GEMM, gather the C
-row blocks on every rank. Default workload: M = N = K = 32768 (BASELINE.json configs[4], the
+rank 0 (N > 1), the 3xTF32 tcgen05 shard GEMM (the TF32 hi/lo split happens on chip, inside
+the GEMM), gather the C row blocks on every rank. Default workload: M = N = K = 32768 (BASELINE.json configs[4], the
 problem the north_star's targets are quoted on), strong scaling (the same problem split over
 N GPUs); --config picks the others. Inputs are seeded synthetic fp32 (synth "d2", U[-1,1)),
 resident in HBM before the timed region; each step is bracketed by CUDA events and the L2 is
