@@ -310,7 +310,11 @@ Plan make_plan(int64_t M, int64_t K, int world, bool aligned) {
     rows_max = std::max(rows_max, rows);
   }
   if (aligned) {
-    pl.pb = std::min(std::max(env_int("GIGA_BCAST_CHUNKS", 4), 1), kMaxChunks);
+    // NCCL pipelines a broadcast internally, so 4 chunks suffice for overlap; the p2p chain
+    // forwards whole chunks GPU to GPU, so the last of g GPUs waits (g - 1) chunk hops for its
+    // first chunk: 16 chunks keep that start-up latency to (g - 1)/16 of B's transfer time.
+    const int pb_default = transport_p2p() ? kMaxChunks : 4;
+    pl.pb = std::min(std::max(env_int("GIGA_BCAST_CHUNKS", pb_default), 1), kMaxChunks);
     pl.pb = int(std::min<int64_t>(pl.pb, std::max<int64_t>(1, K / 512)));
     pl.pc = std::min(std::max(env_int("GIGA_GATHER_CHUNKS", 4), 1), kMaxChunks);
     pl.pc = int(std::min<int64_t>(pl.pc, std::max<int64_t>(1, rows_max / 256)));
