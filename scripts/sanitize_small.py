@@ -31,4 +31,22 @@ for cg in (1, 2):
 x = synth.gen_vector(100003, 3, "d3"); y = synth.gen_vector(100003, 4, "d3")
 print("dot", giga.dot(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()))
 giga.finalize()
+# peer-to-peer transport on 3 virtual GPUs of device 0: copy-engine chain for B, C gather
+# fused into the GEMM epilogue (TMA stores into every virtual GPU's C_full)
+os.environ["GIGA_TRANSPORT"] = "p2p"
+giga.init_devices([0, 0, 0])
+M, N, K = 700, 260, 1040
+A = synth.gen_matrix(M, K, 1, "d3"); B = synth.gen_matrix(K, N, 2, "d3")
+shards, Bs, Cs = [], [], []
+for gi in range(3):
+    r0, rows = giga.partition(M, 3, gi)
+    shards.append(torch.from_numpy(A[r0:r0 + rows]).cuda())
+    Bs.append(torch.from_numpy(B).cuda() if gi == 0 else torch.empty((K, N), device="cuda"))
+    Cs.append(torch.full((M, N), float("nan"), device="cuda"))
+giga.matmul_sharded(shards, Bs, Cs, M, N, K)
+ref = torch.from_numpy(A.astype(np.float64) @ B.astype(np.float64)).float()
+for C in Cs:
+    assert torch.equal(C.cpu(), ref)
+giga.finalize()
+del os.environ["GIGA_TRANSPORT"]
 print("sanitize script ok")
