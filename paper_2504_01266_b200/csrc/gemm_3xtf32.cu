@@ -742,3 +742,27 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
 }
 
 }  // namespace giga
+
+// Bring-up probe (libgiga_debug.so only calls it): how many clusters of `cluster_size` CTAs
+// with this kernel's resources (384 threads, Tile<2>::SMEM_BYTES) fit on the device at once.
+extern "C" int giga_dbg_max_active_clusters(int cluster_size) {
+  using namespace giga;
+  if (ensure_smem_attr<2>() != cudaSuccess) return -1;
+  if (cluster_size > 8)
+    cudaFuncSetAttribute(gemm_3xtf32_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                         1);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(unsigned(cluster_size * 64));
+  lc.blockDim = dim3(cfg::NUM_THREADS);
+  lc.dynamicSmemBytes = Tile<2>::SMEM_BYTES;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(cluster_size);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_3xtf32_kernel<2>, &lc) != cudaSuccess) return -2;
+  return n;
+}
