@@ -484,3 +484,47 @@ def test_rank_api_world1_on_torch_stream(torch_cuda):
     finally:
         g.finalize()
         g.init(1)
+
+
+def test_presplit_comparison_mode_end_to_end(torch_cuda, tmp_path):
+    """GIGA_LO_PRESPLIT=1 (lo arrays split in HBM, the earlier design kept for comparison)
+    through the public calls -- device shards, host buffers, the forced-NCCL pipeline -- gives
+    the same bits as the default lo-in-shared-memory path. The mode is read once per process,
+    so each runs in a child process."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+import synth
+from paper_2504_01266_b200 import giga
+giga.init(1)
+M, N, K = 700, 516, 2056
+A = synth.gen_matrix(M, K, synth.MATRIX_A, "d2"); B = synth.gen_matrix(K, N, synth.MATRIX_B, "d2")
+dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+C1 = torch.empty((M, N), device="cuda")
+giga.matmul_sharded([dA], [dB], [C1], M, N, K)
+C2 = np.empty((M, N), np.float32)
+giga.matmul(A, B, C2, M, N, K, 1)
+np.save(sys.argv[1], np.stack([C1.cpu().numpy(), C2]))
+'''
+    outs = {}
+    for mode in ("0", "1"):
+        for comm in ("0", "1"):
+            f = str(tmp_path / f"c_{mode}_{comm}.npy")
+            env = dict(os.environ, GIGA_LO_PRESPLIT=mode, GIGA_FORCE_COMM=comm)
+            r = subprocess.run([sys.executable, "-c", code, f], cwd=root, env=env,
+                               capture_output=True, text=True, timeout=300)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs[(mode, comm)] = np.load(f)
+    # same path (same K-chunking), lo from HBM or from shared memory: the same bits
+    for comm in ("0", "1"):
+        assert np.array_equal(outs[("1", comm)].view(np.int32), outs[("0", comm)].view(np.int32))
+    A = synth.gen_matrix(700, 2056, synth.MATRIX_A, "d2")
+    B = synth.gen_matrix(2056, 516, synth.MATRIX_B, "d2")
+    Cref, S = oracle.gemm(A, B)
+    for v in outs.values():
+        for C in v:
+            ok, st = check_close(C, Cref, S)
+            assert ok, st
