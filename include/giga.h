@@ -162,10 +162,12 @@ int giga_dot_rank(const float *x_shard, const float *y_shard, int64_t n, double 
 /* The N > 1 pipeline's chunk plan (pure host arithmetic, identical on every rank; the
  * orchestration of giga_matmul_sharded / giga_matmul_rank uses exactly these functions).
  * B is broadcast from rank 0 in *kchunks K-row chunks [kbounds[c], kbounds[c+1]) (kbounds
- * needs room for 17 entries), the shard GEMM accumulates chunk by chunk, and the C row
- * blocks are gathered in *rchunks rounds; in round q owner o broadcasts the rows returned
- * by giga_plan_block(M, world, rchunks, o, q). Knobs: $GIGA_BCAST_CHUNKS (default 4 with NCCL,
- * 16 with $GIGA_TRANSPORT=p2p), $GIGA_GATHER_CHUNKS (default 4). Errors: INVALID_ARG. */
+ * needs room for 17 entries), growing geometrically so the GEMM starts after a small first
+ * chunk; the shard GEMM accumulates chunk by chunk, and the C row blocks are gathered in
+ * *rchunks rounds; in round q owner o broadcasts the rows returned by
+ * giga_plan_block(M, world, rchunks, o, q) (largest first). Knobs: $GIGA_BCAST_CHUNKS
+ * (default 6 with NCCL, 16 with $GIGA_TRANSPORT=p2p), $GIGA_GATHER_CHUNKS (default 4).
+ * Errors: INVALID_ARG. */
 int giga_pipeline_plan(int64_t M, int64_t N, int64_t K, int world, int *kchunks,
                        int64_t *kbounds, int *rchunks);
 int giga_plan_block(int64_t M, int world, int rchunks, int owner, int q, int64_t *row0,

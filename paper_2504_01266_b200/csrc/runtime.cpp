@@ -301,6 +301,30 @@ int env_int(const char *name, int dflt) {
   return (e && *e) ? atoi(e) : dflt;
 }
 
+// Geometric chunk bounds: n pieces of [0, total) with weights ratio^i, interior bounds rounded
+// to the nearest multiple of `align`; false if a piece would be shorter than `min_piece`.
+static bool geometric_bounds(int64_t total, int n, double ratio, int64_t align,
+                             int64_t min_piece, int64_t *b) {
+  double sum = 0, w = 1;
+  for (int i = 0; i < n; ++i, w *= ratio) sum += w;
+  double cum = 0;
+  w = 1;
+  b[0] = 0;
+  for (int i = 1; i < n; ++i, w *= ratio) {
+    cum += w;
+    b[i] = int64_t(double(total) * cum / sum / double(align) + 0.5) * align;
+    if (b[i] - b[i - 1] < min_piece) return false;
+  }
+  b[n] = total;
+  return b[n] - b[n - 1] >= min_piece;
+}
+
+// The K-chunks of B's distribution grow geometrically: the GEMM starts once the first (small)
+// chunk has landed, and each later chunk's transfer hides behind the previous chunk's GEMM as
+// long as the growth r stays below (GEMM time per K-row) / (transfer time per K-row)
+// = (2 rows_max / R) / (4 / BW) = rows_max BW / (2 R), R ~ 255 TFLOP/s, BW ~ 600 GB/s (NCCL
+// broadcast) or 770 GB/s (a copy-engine hop). r = 0.8 of that, at most 4, lowered until every
+// chunk is >= 256 deep. E.g. 32768^3 on 8 GPUs (NCCL): 555, 1094, 2155, 4245, 8364, 16479.
 Plan make_plan(int64_t M, int64_t K, int world, bool aligned) {
   Plan pl;
   int64_t rows_max = 0;
@@ -309,27 +333,38 @@ Plan make_plan(int64_t M, int64_t K, int world, bool aligned) {
     partition_rows(M, world, r, &r0, &rows);
     rows_max = std::max(rows_max, rows);
   }
-  if (aligned) {
-    // NCCL pipelines a broadcast internally, so 4 chunks suffice for overlap; the p2p chain
-    // forwards whole chunks GPU to GPU, so the last of g GPUs waits (g - 1) chunk hops for its
-    // first chunk: 16 chunks keep that start-up latency to (g - 1)/16 of B's transfer time.
-    const int pb_default = transport_p2p() ? kMaxChunks : 4;
-    pl.pb = std::min(std::max(env_int("GIGA_BCAST_CHUNKS", pb_default), 1), kMaxChunks);
-    pl.pb = int(std::min<int64_t>(pl.pb, std::max<int64_t>(1, K / 512)));
-    pl.pc = std::min(std::max(env_int("GIGA_GATHER_CHUNKS", 4), 1), kMaxChunks);
-    pl.pc = int(std::min<int64_t>(pl.pc, std::max<int64_t>(1, rows_max / 256)));
+  pl.kb[0] = 0;
+  pl.kb[1] = K;
+  if (!aligned) return pl;
+  // NCCL pipelines a broadcast internally; the p2p chain forwards whole chunks GPU to GPU, so
+  // the last of g GPUs waits (g - 1) hops of the first chunks: more, smaller chunks there.
+  const bool p2p = transport_p2p();
+  pl.pb = std::min(std::max(env_int("GIGA_BCAST_CHUNKS", p2p ? kMaxChunks : 6), 1), kMaxChunks);
+  pl.pb = int(std::min<int64_t>(pl.pb, std::max<int64_t>(1, K / 256)));
+  const double bw = p2p ? 770e9 : 600e9, R = 255e12;
+  double r = std::min(4.0, std::max(1.0, 0.8 * double(rows_max) * bw / (2.0 * R)));
+  while (r > 1.0 && !geometric_bounds(K, pl.pb, r, 16, 256, pl.kb)) r = std::max(1.0, r * 0.9);
+  if (r <= 1.0 && !geometric_bounds(K, pl.pb, 1.0, 16, 256, pl.kb)) {
+    for (int c = 0; c < pl.pb; ++c) pl.kb[c] = (K * c / pl.pb) / 16 * 16;
+    pl.kb[pl.pb] = K;
   }
-  for (int c = 0; c < pl.pb; ++c) pl.kb[c] = (K * c / pl.pb) / 16 * 16;
-  pl.kb[pl.pb] = K;
+  pl.pc = std::min(std::max(env_int("GIGA_GATHER_CHUNKS", 4), 1), kMaxChunks);
+  pl.pc = int(std::min<int64_t>(pl.pc, std::max<int64_t>(1, rows_max / 256)));
   return pl;
 }
 
+// Row chunks of the last K-chunk's GEMM, gathered one by one: owner o's rows split with
+// weights 0.7^q (largest first, rounded to 256-row tiles) so the gather of the last, exposed
+// chunk is small (13% of the rows for 4 chunks instead of 25%) while the first gather still
+// starts early; shards too small for that split evenly.
 void plan_block(int64_t M, int world, int pc, int owner, int q, int64_t *row0, int64_t *rows) {
   int64_t o0, orows;
   partition_rows(M, world, owner, &o0, &orows);
-  const int64_t q0 = orows * q / pc, q1 = orows * (q + 1) / pc;
-  *row0 = o0 + q0;
-  *rows = q1 - q0;
+  int64_t b[kMaxChunks + 1];
+  if (pc > kMaxChunks || !geometric_bounds(orows, pc, 0.7, 256, 256, b))
+    for (int i = 0; i <= pc && i <= kMaxChunks; ++i) b[i] = orows * i / pc;
+  *row0 = o0 + b[q];
+  *rows = b[q + 1] - b[q];
 }
 
 bool force_comm() { return env_int("GIGA_FORCE_COMM", 0) != 0; }

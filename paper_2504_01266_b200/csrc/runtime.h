@@ -140,10 +140,11 @@ cudaError_t timed(int kind, cudaStream_t st, F fn) {
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// The chunk plan: B is broadcast in pb K-chunks [kb[c], kb[c+1]) (multiples of 16, at least
-// 512 deep); the last K-chunk's GEMM and the C gather run in pc row chunks; chunk q of owner
-// o is rows [o0 + orows*q/pc, o0 + orows*(q+1)/pc) of its shard (plan_block). Knobs:
-// $GIGA_BCAST_CHUNKS (4), $GIGA_GATHER_CHUNKS (4); unaligned shapes use one chunk of each.
+// The chunk plan (runtime.cpp make_plan / plan_block): B is distributed in pb K-chunks
+// [kb[c], kb[c+1]) growing geometrically (multiples of 16, at least 256 deep); the last
+// K-chunk's GEMM and the C gather run in pc row chunks per owner, shrinking geometrically.
+// Knobs: $GIGA_BCAST_CHUNKS (6 with NCCL, 16 with p2p), $GIGA_GATHER_CHUNKS (4); unaligned
+// shapes use one chunk of each.
 struct Plan {
   int pb = 1, pc = 1;
   int64_t kb[kMaxChunks + 1] = {0};

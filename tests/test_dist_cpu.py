@@ -117,12 +117,20 @@ def test_plan_blocks_cover_every_row_once():
 
 def test_plan_knobs_and_limits(monkeypatch):
     from paper_2504_01266_b200 import giga
+    monkeypatch.delenv("GIGA_TRANSPORT", raising=False)
     kb, rc = giga.pipeline_plan(16384, 16384, 16384, 8)
-    assert len(kb) == 5 and rc == 4 and all(b % 16 == 0 for b in kb)
+    sizes = np.diff(kb)
+    assert len(kb) == 7 and rc == 4 and all(b % 16 == 0 for b in kb) and kb[-1] == 16384
+    assert sizes[0] >= 256 and np.all(np.diff(sizes) > 0)  # small first chunk, then growing
+    blocks = [giga.plan_block(16384, 8, rc, 3, q)[1] for q in range(rc)]
+    assert np.all(np.diff(blocks) <= 0) and blocks[-1] < blocks[0]  # largest gather first
+    monkeypatch.setenv("GIGA_TRANSPORT", "p2p")
+    assert len(giga.pipeline_plan(32768, 32768, 32768, 8)[0]) == 17
+    monkeypatch.delenv("GIGA_TRANSPORT")
     monkeypatch.setenv("GIGA_BCAST_CHUNKS", "16")
     monkeypatch.setenv("GIGA_GATHER_CHUNKS", "1")
     kb, rc = giga.pipeline_plan(4096, 4096, 4096, 2)
-    assert len(kb) == 9 and rc == 1  # at least 512 deep per K-chunk
+    assert len(kb) == 17 and rc == 1 and np.all(np.diff(kb) >= 256)  # >= 256 deep per chunk
     kb, rc = giga.pipeline_plan(64, 6, 6, 2)  # unaligned shapes: a single chunk of each
     assert kb == [0, 6] and rc == 1
     with pytest.raises(giga.GigaError):
