@@ -75,12 +75,13 @@ struct Tile {
   static constexpr uint32_t STAGE_BYTES = 2 * cfg::A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = int(cfg::SMEM_RING / STAGE_BYTES);  // 4 (CG=1), 6 (CG=2)
   static constexpr size_t SMEM_BYTES =
-      size_t(STAGES) * STAGE_BYTES + cfg::EPI_BYTES + 1024 + 256;
+      size_t(STAGES) * STAGE_BYTES + cfg::EPI_BYTES + 1024 + 512;
 };
 
 struct GemmParams {
   int M, N, K, ldc;
   int accumulate; // 1: C += A*B (K-chunked pipelines), 0: C = A*B
+  int load_c;     // 1: epilogue adds the block's current C before storing (see GemmExtra)
   int terms;      // 3 = 3xTF32, 1 = TF32 (hi*hi only)
   int p_kb;       // k-blocks per TMEM accumulation interval (>= 1)
   int n_kb;       // k-blocks per tile
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
   uint64_t *lofull = tempty + 2;  // stage ready for the MMA: raw + lo tiles of both CTAs
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(lofull + STAGES);
   uint8_t *sig = reinterpret_cast<uint8_t *>(lofull + STAGES) + 16;  // 16 B aligned, 32 B
+  uint64_t *cbar = reinterpret_cast<uint64_t *>(sig + 32);  // per epilogue warp: C block loads
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -188,6 +190,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       ptx::mbar_init(&empty[s], 1);
       ptx::mbar_init(&lofull[s], NUM_XFORM_WARPS);
     }
+    for (int w = 0; w < NUM_EPI_WARPS; ++w) ptx::mbar_init(&cbar[w], 1);
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], NUM_EPI_WARPS * CG);
@@ -399,6 +402,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     const uint32_t tempty_leader0 = ptx::smem_u32(&tempty[0]) & ptx::kPeerBitMask;
     const uint32_t tempty_leader1 = ptx::smem_u32(&tempty[1]) & ptx::kPeerBitMask;
     uint32_t acc_iter = 0;
+    uint32_t cphase = 0;  // parity of this warp's C-load barrier
     for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
       int mb, nb;
       tile_coords(t, p, mb, nb);
@@ -439,6 +443,27 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       for (int c = 0; c < 4; ++c) {
         if (lane == 0) ptx::bulk_wait_read<0>();  // previous store has left the staging tile
         __syncwarp();
+        if (p.load_c) {
+          // C += this partial, in registers: TMA-load the block (zero-filled outside C) into
+          // the staging tile, then add row `lane` (same swizzle as the store below)
+          if (lane == 0) {
+            ptx::mbar_expect_tx(&cbar[e], EPI_STAGE_BYTES);
+            ptx::tma_load_2d(epi_stage + e * EPI_STAGE_BYTES, &cmaps.m[0], &cbar[e],
+                             ccol0 + 32 * c, crow0);
+          }
+          ptx::mbar_wait(&cbar[e], cphase);
+          cphase ^= 1;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 o = ptx::ld_shared_v4(
+                stg + uint32_t(lane) * 128 + uint32_t((j ^ (lane & 7)) * 16));
+            sum[c * 32 + 4 * j] = __fadd_rn(sum[c * 32 + 4 * j], o.x);
+            sum[c * 32 + 4 * j + 1] = __fadd_rn(sum[c * 32 + 4 * j + 1], o.y);
+            sum[c * 32 + 4 * j + 2] = __fadd_rn(sum[c * 32 + 4 * j + 2], o.z);
+            sum[c * 32 + 4 * j + 3] = __fadd_rn(sum[c * 32 + 4 * j + 3], o.w);
+          }
+          __syncwarp();  // every lane has read the block before it is overwritten
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const uint32_t off = uint32_t(lane) * 128 + uint32_t((j ^ (lane & 7)) * 16);
@@ -678,6 +703,8 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.K = int(K);
   p.ldc = int(ldc);
   p.accumulate = ex->accumulate ? 1 : 0;
+  p.load_c = ex->load_c ? 1 : 0;
+  if (p.accumulate && p.load_c) return cudaErrorInvalidValue;
   p.terms = terms;
   p.lo_smem = lo_smem ? 1 : 0;
   p.n_kb = int((K + BK - 1) / BK);

@@ -28,7 +28,10 @@ cudaError_t launch_split_lo_2d(const float *x, float *lo, int64_t rows, int64_t 
 // into C (C += A*B, fp32 RN) instead of overwriting; max_ctas caps the persistent grid (SMs
 // left free for concurrent communication kernels; 0 = all SMs); peer_c[0..n_peer_c) are
 // further C buffers (same shape and ldc, e.g. the peers' C_full rows over NVLink) that receive
-// the same tiles from the epilogue: the gather fused into the GEMM.
+// the same tiles from the epilogue: the gather fused into the GEMM. load_c = 1 (with
+// accumulate = 0): the epilogue first reads each block of C and adds it (fp32 RN, the same
+// bits as accumulate's reduce-add), then stores the sum to C and every peer -- the last chunk
+// of a K-chunked series, so that only final values cross NVLink.
 constexpr int kMaxCDst = 8;
 struct GemmExtra {
   int64_t lda = 0, ldb = 0;
@@ -36,6 +39,7 @@ struct GemmExtra {
   int max_ctas = 0;
   float *const *peer_c = nullptr;
   int n_peer_c = 0;
+  int load_c = 0;
 };
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
                                const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,

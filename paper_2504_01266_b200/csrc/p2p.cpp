@@ -26,6 +26,22 @@ namespace giga {
 // The devices may repeat (giga_init_devices): "virtual GPUs" on one device run exactly this
 // schedule with device-local copies and stores, which is how it is tested on a 1-GPU box.
 
+// The GEMM options of K-chunk c of pb when `ex` carries the peers' C buffers: the partial
+// sums stay local (chunk 0 stores, later chunks reduce-add into this GPU's C) and only the
+// last chunk, which reads back the local partial and adds its own (load_c), stores the final
+// values into every peer -- each C element crosses NVLink once, not once per chunk.
+static GemmExtra chunk_extra(const GemmExtra &ex, int c, int pb) {
+  GemmExtra e = ex;
+  const bool last = c == pb - 1;
+  e.accumulate = (c > 0 && !last) ? 1 : 0;
+  e.load_c = (c > 0 && last) ? 1 : 0;
+  if (!last) {
+    e.peer_c = nullptr;
+    e.n_peer_c = 0;
+  }
+  return e;
+}
+
 bool transport_p2p() {
   const char *e = getenv("GIGA_TRANSPORT");
   return e && strcmp(e, "p2p") == 0;
@@ -90,10 +106,9 @@ int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K, bool gath
       CK(cudaStreamWaitEvent(p.st, p.d->ev_kchunk[c], 0));
       TRY(split(p.B + plan.kb[c] * N, lo_at(p.d->B_lo, plan.kb[c] * N), Kc * N, p.st));
       if (rows == 0) continue;
-      GemmExtra e = ex;
-      e.accumulate = c > 0;
       TRY(gemm_chunk(p.A + plan.kb[c], lo_at(p.d->A_lo, plan.kb[c]), p.B + plan.kb[c] * N,
-                     lo_at(p.d->B_lo, plan.kb[c] * N), Cr, rows, N, Kc, e, p.st));
+                     lo_at(p.d->B_lo, plan.kb[c] * N), Cr, rows, N, Kc,
+                     chunk_extra(ex, c, plan.pb), p.st));
     }
     CK(cudaEventRecord(p.d->ev_c, p.st));
   }
@@ -214,10 +229,9 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
     CK(cudaStreamWaitEvent(st, d.ev_kchunk[c], 0));
     TRY(split(B + plan.kb[c] * N, lo_at(d.B_lo, plan.kb[c] * N), Kc * N, st));
     if (rows == 0) continue;
-    GemmExtra e = ex;
-    e.accumulate = c > 0;
     TRY(gemm_chunk(A + plan.kb[c], lo_at(d.A_lo, plan.kb[c]), B + plan.kb[c] * N,
-                   lo_at(d.B_lo, plan.kb[c] * N), C + r0 * N, rows, N, Kc, e, st));
+                   lo_at(d.B_lo, plan.kb[c] * N), C + r0 * N, rows, N, Kc,
+                   chunk_extra(ex, c, plan.pb), st));
   }
   for (int q = 0; q < world; ++q)
     if (q != r) TRY(write_flag(st, flag_cdone(x.peerF[q], r), s));
