@@ -67,7 +67,8 @@ int matmul_locked(const float *A, const float *B, float *C, int64_t M, int64_t N
     TRY(shard_compute(d, d.compute, A, M, B, C, N, N, K, nullptr));
     return sync_all(1);
   }
-  if (!device && ngpus == 1 && K % 4 == 0 && N % 4 == 0) return host_pipeline(g.devs[0], A, B, C, M, N, K);
+  if (!device && ngpus == 1 && K % 4 == 0 && N % 4 == 0)
+    return host_pipeline(g.devs[0], A, B, C, M, N, K);
 
   // Stage: every GPU gets its A row block and a B buffer; GPU 0 gets B.
   for (int i = 0; i < ngpus; ++i) {
