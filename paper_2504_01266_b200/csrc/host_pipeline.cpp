@@ -43,20 +43,13 @@ int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M
                      {&d.B_lo, lo_bytes(K * N)}}));
   float *Ad = fptr(d.A_h), *Bd = fptr(d.B_h), *Cd = fptr(d.C_h), *Alo = lo_at(d.A_lo),
         *Blo = lo_at(d.B_lo);
-  // $GIGA_HOST_TRACE=1: timing events after every piece of every engine, printed as one JSON
-  // line on stderr (a timeline to compare with the plan's model)
-  const bool trace = env_int("GIGA_HOST_TRACE", 0) != 0;
-  enum { T0 = 0, TK = 1, TR = TK + kMaxChunks, TG1 = TR + kMaxChunks, TG2 = TG1 + kMaxChunks,
-         TDE = TG2 + kMaxChunks, TD = TDE + 1, TN = TD + kMaxChunks };
-  if (trace && d.ev_trace.empty()) {
-    d.ev_trace.assign(TN, nullptr);
-    for (auto &e : d.ev_trace) CK(cudaEventCreate(&e));
-  }
-  auto mark = [&](int slot, cudaStream_t st) -> int {
-    if (trace) CK(cudaEventRecord(d.ev_trace[slot], st));
-    return GIGA_OK;
-  };
-  TRY(mark(T0, d.comm));
+  Trace tr(d, "host_pipeline");  // $GIGA_TRACE=1: the measured timeline of the plan
+  tr.meta("M", double(M));
+  tr.meta("N", double(N));
+  tr.meta("K", double(K));
+  tr.meta("Me", double(Me));
+  tr.meta("model_ms", plan.t_model * 1e3);
+  TRY(tr.start(d.comm));
   // host -> device: (early A columns, B rows) per K-chunk, then the late A row blocks
   for (int c = 0; c < P; ++c) {
     const int64_t Kc = kb[c + 1] - kb[c];
@@ -66,7 +59,7 @@ int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M
     CK(cudaMemcpyAsync(Bd + kb[c] * N, B + kb[c] * N, size_t(Kc * N) * 4,
                        cudaMemcpyHostToDevice, d.comm));
     CK(cudaEventRecord(d.ev_kchunk[c], d.comm));
-    TRY(mark(TK + c, d.comm));
+    TRY(tr.mark("h2d_k", d.comm));
   }
   for (int q = 0; q < Q; ++q) {
     const int64_t q0 = plan.rb[q], q1 = plan.rb[q + 1];
@@ -74,7 +67,7 @@ int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M
       CK(cudaMemcpyAsync(Ad + q0 * K, A + q0 * K, size_t((q1 - q0) * K) * 4,
                          cudaMemcpyHostToDevice, d.comm));
     CK(cudaEventRecord(d.ev_rchunk[q], d.comm));
-    TRY(mark(TR + q, d.comm));
+    TRY(tr.mark("h2d_r", d.comm));
   }
   // phase 1: early rows, K-chunk by K-chunk, accumulating in C
   GemmExtra ex;
@@ -93,13 +86,13 @@ int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M
     e.accumulate = c > 0;
     TRY(gemm_chunk(Ad + kb[c], at(Alo, kb[c]), Bd + kb[c] * N, at(Blo, kb[c] * N), Cd, Me, N,
                    Kc, e, d.compute));
-    TRY(mark(TG1 + c, d.compute));
+    TRY(tr.mark("gemm1", d.compute));
   }
   if (Me > 0) {
     CK(cudaEventRecord(d.ev_c, d.compute));
     CK(cudaStreamWaitEvent(d.d2h, d.ev_c, 0));
     CK(cudaMemcpyAsync(C, Cd, size_t(Me * N) * 4, cudaMemcpyDeviceToHost, d.d2h));
-    TRY(mark(TDE, d.d2h));
+    TRY(tr.mark("d2h_early", d.d2h));
   }
   // phase 2: late row blocks over the full K (phase 1 waited for every K-chunk of B)
   for (int q = 0; q < Q; ++q) {
@@ -111,35 +104,17 @@ int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M
                d.compute));
     }
     CK(cudaEventRecord(d.ev_done[q], d.compute));
-    TRY(mark(TG2 + q, d.compute));
+    TRY(tr.mark("gemm2", d.compute));
     CK(cudaStreamWaitEvent(d.d2h, d.ev_done[q], 0));
     if (q1 > q0)
       CK(cudaMemcpyAsync(C + q0 * N, Cd + q0 * N, size_t((q1 - q0) * N) * 4,
                          cudaMemcpyDeviceToHost, d.d2h));
-    TRY(mark(TD + q, d.d2h));
+    TRY(tr.mark("d2h", d.d2h));
   }
   CK(cudaStreamSynchronize(d.d2h));
   CK(cudaStreamSynchronize(d.compute));
   CK(cudaStreamSynchronize(d.comm));
-  if (trace) {
-    auto ms = [&](int slot) {
-      float v = 0;
-      cudaEventElapsedTime(&v, d.ev_trace[T0], d.ev_trace[slot]);
-      return double(v);
-    };
-    auto list = [&](int base, int n) {
-      std::string o = "[";
-      for (int i = 0; i < n; ++i) o += (i ? ", " : "") + std::to_string(ms(base + i));
-      return o + "]";
-    };
-    fprintf(stderr,
-            "{\"host_trace\": {\"M\": %lld, \"N\": %lld, \"K\": %lld, \"Me\": %lld, "
-            "\"P\": %d, \"Q\": %d, \"model_ms\": %.3f, \"h2d_k\": %s, \"h2d_r\": %s, "
-            "\"gemm1\": %s, \"gemm2\": %s, \"d2h_early\": %.3f, \"d2h\": %s}}\n",
-            (long long)M, (long long)N, (long long)K, (long long)Me, P, Q, plan.t_model * 1e3,
-            list(TK, P).c_str(), list(TR, Q).c_str(), list(TG1, Me > 0 ? P : 0).c_str(),
-            list(TG2, Q).c_str(), Me > 0 ? ms(TDE) : 0.0, list(TD, Q).c_str());
-  }
+  TRY(tr.finish());
   return GIGA_OK;
 }
 

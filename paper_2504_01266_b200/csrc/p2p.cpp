@@ -196,6 +196,11 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
   const Plan plan = make_plan(M, K, world, true);
   int64_t r0, rows;
   partition_rows(M, world, r, &r0, &rows);
+  Trace tr(d, "p2p_rank");  // $GIGA_TRACE=1: this rank's timeline
+  tr.meta("rank", r);
+  tr.meta("world", world);
+  tr.meta("kchunks", plan.pb);
+  TRY(tr.start(st));
   CK(cudaEventRecord(d.ev_start, st));
   CK(cudaStreamWaitEvent(d.comm, d.ev_start, 0));
   TRY(ws_reserve(d, {{&d.A_lo, lo_bytes(std::max<int64_t>(rows, 1) * K)},
@@ -212,6 +217,7 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
       TRY(write_flag(d.comm, flag_pulled(x.peerF[r - 1], c), s));
     }
     CK(cudaEventRecord(d.ev_kchunk[c], d.comm));
+    TRY(tr.mark("b_chunk", d.comm));
     if (r < world - 1) TRY(write_flag(d.comm, flag_ready(x.peerF[r + 1], c), s));
   }
   // GEMMs over the K-chunks, every tile also stored into the peers' C_full
@@ -232,14 +238,17 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
     TRY(gemm_chunk(A + plan.kb[c], lo_at(d.A_lo, plan.kb[c]), B + plan.kb[c] * N,
                    lo_at(d.B_lo, plan.kb[c] * N), C + r0 * N, rows, N, Kc,
                    chunk_extra(ex, c, plan.pb), st));
+    TRY(tr.mark("gemm", st));
   }
   for (int q = 0; q < world; ++q)
     if (q != r) TRY(write_flag(st, flag_cdone(x.peerF[q], r), s));
   for (int q = 0; q < world; ++q)
     if (q != r) TRY(wait_flag(st, flag_cdone(x.flags, q), s));
+  TRY(tr.mark("all_c", st));
   // the comm stream's last copies are done before the call's work is (join it back)
   CK(cudaEventRecord(d.ev_c, d.comm));
   CK(cudaStreamWaitEvent(st, d.ev_c, 0));
+  TRY(tr.finish());
   return GIGA_OK;
 }
 

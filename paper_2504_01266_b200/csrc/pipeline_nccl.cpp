@@ -115,9 +115,18 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
     ex.max_ctas = std::max(2, nsm - std::max(0, env_int("GIGA_COMM_SMS", 8)));
   }
 
+  std::vector<Trace> tr;  // $GIGA_TRACE=1: per-GPU timeline of the pipeline
+  for (auto &p : parts) {
+    tr.emplace_back(*p.d, "nccl_pipeline");
+    tr.back().meta("rank", p.rank);
+    tr.back().meta("world", world);
+    tr.back().meta("kchunks", pb);
+    tr.back().meta("rchunks", pc);
+  }
   // 0. join the caller's stream, workspace, split A
   for (auto &p : parts) {
     CK(cudaSetDevice(p.d->dev));
+    TRY(tr[&p - &parts[0]].start(p.st));
     CK(cudaEventRecord(p.d->ev_start, p.st));
     CK(cudaStreamWaitEvent(p.d->comm, p.d->ev_start, 0));
     int64_t r0, rows;
@@ -145,6 +154,7 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
     for (auto &p : parts) {
       CK(cudaSetDevice(p.d->dev));
       CK(cudaEventRecord(p.d->ev_kchunk[c], p.d->comm));
+      TRY(tr[&p - &parts[0]].mark("bcast", p.d->comm));
     }
   }
   // 2. compute: K-chunks accumulate into C; the last one in row chunks
@@ -170,6 +180,7 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
       if (c < pb - 1) {
         if (rows > 0)
           TRY(gemm_chunk(p.A + kb[c], at(Alo, kb[c]), Bc, Bloc, Cs, rows, N, Kc, e, p.st));
+        TRY(tr[&p - &parts[0]].mark("gemm", p.st));
         continue;
       }
       for (int q = 0; q < pc; ++q) {
@@ -180,6 +191,7 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
           TRY(gemm_chunk(p.A + q0 * K + kb[c], at(Alo, q0 * K + kb[c]), Bc, Bloc, Cs + q0 * N,
                          brows, N, Kc, e, p.st));
         CK(cudaEventRecord(p.d->ev_rchunk[q], p.st));
+        TRY(tr[&p - &parts[0]].mark("gemm_rows", p.st));
       }
     }
   }
@@ -214,6 +226,10 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
       }
     }
     TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
+    for (auto &p : parts) {
+      CK(cudaSetDevice(p.d->dev));
+      TRY(tr[&p - &parts[0]].mark("gather", p.d->comm));
+    }
   }
   // 4. the caller's stream resumes after the gather
   for (auto &p : parts) {
@@ -221,6 +237,7 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
     CK(cudaEventRecord(p.d->ev_c, p.d->comm));
     CK(cudaStreamWaitEvent(p.st, p.d->ev_c, 0));
   }
+  for (auto &t : tr) TRY(t.finish());
   return GIGA_OK;
 }
 

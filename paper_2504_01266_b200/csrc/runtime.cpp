@@ -377,4 +377,56 @@ int gemm_chunk(const float *A, const float *Alo, const float *B, const float *Bl
   return GIGA_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// timelines ($GIGA_TRACE)
+
+Trace::Trace(DevCtx &d, const char *what) : d_(d), what_(what) {
+  on_ = env_int("GIGA_TRACE", 0) != 0;
+}
+
+int Trace::start(cudaStream_t st) { return on_ ? mark("", st) : GIGA_OK; }
+
+int Trace::mark(const char *series, cudaStream_t st) {
+  if (!on_) return GIGA_OK;
+  if (n_ >= d_.ev_trace.size()) {
+    cudaEvent_t e = nullptr;
+    CK(cudaEventCreate(&e));
+    d_.ev_trace.push_back(e);
+  }
+  CK(cudaEventRecord(d_.ev_trace[n_], st));
+  marks_.push_back({series, n_++});
+  return GIGA_OK;
+}
+
+void Trace::meta(const char *key, double v) {
+  if (!on_) return;
+  char buf[96];
+  snprintf(buf, sizeof buf, "%s\"%s\": %.17g", meta_.empty() ? "" : ", ", key, v);
+  meta_ += buf;
+}
+
+int Trace::finish() {
+  if (!on_ || marks_.empty()) return GIGA_OK;
+  for (auto &m : marks_) CK(cudaEventSynchronize(d_.ev_trace[m.second]));
+  std::map<std::string, std::string> series;
+  for (size_t i = 1; i < marks_.size(); ++i) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, d_.ev_trace[marks_[0].second], d_.ev_trace[marks_[i].second]));
+    std::string &v = series[marks_[i].first];
+    char buf[32];
+    snprintf(buf, sizeof buf, "%s%.4f", v.empty() ? "" : ", ", ms);
+    v += buf;
+  }
+  std::string out = "{\"trace\": \"" + std::string(what_) + "\", \"device\": " +
+                    std::to_string(d_.dev) + ", \"meta\": {" + meta_ + "}, \"ms\": {";
+  bool first = true;
+  for (auto &kv : series) {
+    out += (first ? "\"" : ", \"") + kv.first + "\": [" + kv.second + "]";
+    first = false;
+  }
+  out += "}}\n";
+  fputs(out.c_str(), stderr);
+  return GIGA_OK;
+}
+
 }  // namespace giga

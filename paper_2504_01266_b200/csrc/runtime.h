@@ -61,7 +61,7 @@ struct DevCtx {
   std::vector<cudaEvent_t> ev_kchunk;  // pipeline: B K-chunk c present
   std::vector<cudaEvent_t> ev_rchunk;  // pipeline: C row-chunk q computed
   std::vector<cudaEvent_t> ev_done;    // host pipeline: late row block q computed
-  std::vector<cudaEvent_t> ev_trace;   // host pipeline timeline ($GIGA_HOST_TRACE), timing
+  std::vector<cudaEvent_t> ev_trace;   // timing events of class Trace ($GIGA_TRACE)
   Buf A_lo, B_lo, A_pad, B_pad, C_pad, A_h, B_h, C_h;
   Buf vec_ws;  // dot: kDotMaxBlocks fp64 partials, the fp64 result, the ticket (zeroed once)
 };
@@ -171,6 +171,28 @@ template <class T>
 T *at(T *p, int64_t off) {
   return p ? p + off : nullptr;
 }
+
+// Timeline of one call on one device ($GIGA_TRACE=1): a timing event after each piece of work
+// on each engine, printed as one JSON line on stderr when the call ends ({"trace": what,
+// "device": d, "meta": {...}, "ms": {series: [end times since the call's start]}}). Tracing
+// synchronises the call's streams before printing; it is off unless the variable is set.
+class Trace {
+ public:
+  Trace(DevCtx &d, const char *what);
+  bool on() const { return on_; }
+  int start(cudaStream_t st);                  // the zero of the timeline
+  int mark(const char *series, cudaStream_t st);
+  void meta(const char *key, double v);
+  int finish();                                // waits for the last marks, prints the line
+
+ private:
+  DevCtx &d_;
+  const char *what_;
+  bool on_ = false;
+  size_t n_ = 0;
+  std::vector<std::pair<std::string, size_t>> marks_;
+  std::string meta_;
+};
 
 // ---- runtime.cpp ---------------------------------------------------------------------------
 int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));

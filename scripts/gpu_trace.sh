@@ -11,4 +11,4 @@ Ch = torch.empty((M, N)).pin_memory()
 for _ in range(3):
     giga.matmul(Ah, Bh, Ch, M, N, K, 1)
 PY
-for S in 32768 16384; do GIGA_HOST_TRACE=1 PYTHONPATH=. timeout -s KILL 300 python /tmp/tr.py $S 2> gpurun_out/trace_$S.txt; tail -1 gpurun_out/trace_$S.txt | cut -c1-3000; done
+for S in 32768 16384; do GIGA_TRACE=1 PYTHONPATH=. timeout -s KILL 300 python /tmp/tr.py $S 2> gpurun_out/trace_$S.txt; tail -1 gpurun_out/trace_$S.txt | cut -c1-3000; done

@@ -528,3 +528,35 @@ np.save(sys.argv[1], np.stack([C1.cpu().numpy(), C2]))
         for C in v:
             ok, st = check_close(C, Cref, S)
             assert ok, st
+
+
+def test_trace_timelines(giga, torch_cuda, monkeypatch, capfd):
+    """$GIGA_TRACE=1 prints one JSON timeline per call: the host-buffer schedule (its pieces
+    in plan order) and the N > 1 pipeline (broadcast chunks, GEMM chunks, gather rounds; run
+    at world 1 with GIGA_FORCE_COMM)."""
+    torch = torch_cuda
+    M, N, K = 2048, 1024, 4096
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+    monkeypatch.setenv("GIGA_TRACE", "1")
+    C = np.empty((M, N), np.float32)
+    giga.matmul(A, B, C, M, N, K, 1)
+    monkeypatch.setenv("GIGA_FORCE_COMM", "1")
+    dC = torch.empty((M, N), device="cuda")
+    giga.matmul_sharded([_dev(torch, A)], [_dev(torch, B)], [dC], M, N, K)
+    torch.cuda.synchronize()
+    lines = [json.loads(l) for l in capfd.readouterr().err.splitlines() if l.startswith('{"trace"')]
+    kinds = {l["trace"]: l for l in lines}
+    assert set(kinds) == {"host_pipeline", "nccl_pipeline"}, lines
+    for l in lines:
+        for series, ts in l["ms"].items():
+            assert ts == sorted(ts) and all(t >= 0 for t in ts), (series, ts)
+    h = kinds["host_pipeline"]
+    plan = giga.host_plan(M, N, K)
+    assert len(h["ms"]["h2d_k"]) == len(plan["kb"]) - 1 and h["meta"]["Me"] == plan["Me"]
+    p = kinds["nccl_pipeline"]
+    kb, rc = giga.pipeline_plan(M, N, K, 1)
+    assert len(p["ms"]["bcast"]) == len(kb) - 1 and len(p["ms"]["gather"]) == rc
+    assert len(p["ms"]["gemm_rows"]) == rc
+    Cref, _ = oracle.gemm(A, B)
+    assert check_exact(C, Cref)[0] and check_exact(dC.cpu().numpy(), Cref)[0]
