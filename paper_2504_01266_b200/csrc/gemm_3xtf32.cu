@@ -33,9 +33,13 @@
 //                      accumulators
 //       warps 2..9     epilogue: tcgen05.ld TMEM -> registers, RN fp32 promotion adds,
 //                      swizzled smem staging -> TMA bulk stores (reduce-add when a K-chunked
-//                      pipeline accumulates) into the shard's rows of C.
+//                      pipeline accumulates; load-add-store when the last chunk also writes
+//                      the peers' C) into the shard's rows of C and, fused gather, the peers'.
+//       warp 0 also allocates / frees the TMEM (see the allocation below).
 //     Computing lo on chip halves the L2 -> SM operand traffic and the HBM footprint of the
-//     3xTF32 operands (measured: -11% GEMM time at 32768^3 for the same MMAs).
+//     3xTF32 operands (measured: 11% less GEMM time at 32768^3 for the same MMAs). The peer
+//     CTA publishes its lo tiles to the leader's MMA with an async-proxy bulk signal
+//     (ptx::bulk_signal_leader): a release.cluster arrive per k-block cost 40%.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
