@@ -1,6 +1,7 @@
 """Seeded shape fuzzing: random (M, N, K) from 1 to ~700 (ragged everywhere: K and N not
 multiples of 4 take the padded path, M < tile, tails in every dimension) through every public
-entry point, integer inputs (bit-exact against the oracle), C prefilled with NaN."""
+entry point, integer inputs (bit-exact against the oracle) and non-integer inputs (within the
+1e-5 * sum |A||B| bound), C prefilled with NaN."""
 import numpy as np
 import pytest
 
@@ -54,6 +55,27 @@ def test_fuzz_host_device_sharded(giga, torch_cuda, M, N, K):
     dC.fill_(float("nan"))
     giga.matmul_sharded([dA], [dB], [dC], M, N, K)
     assert check_exact(dC.cpu().numpy(), ref)[0], "sharded"
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES[:8] + [(300, 516, 2056), (1000, 260, 4100)])
+@pytest.mark.parametrize("dist", ["d2", "d4"])
+def test_fuzz_non_integer_within_bound(giga, torch_cuda, M, N, K, dist):
+    """Non-integer inputs (the lo terms are live) through the host and device paths, C within
+    1e-5 * sum |A||B| of the oracle element by element."""
+    from oracle.check import check_close
+    torch = torch_cuda
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, dist)
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
+    ref, S = oracle.gemm(A, B)
+    C = np.full((M, N), np.nan, np.float32)
+    giga.matmul(A, B, C, M, N, K, 1)
+    ok, st = check_close(C, ref, S)
+    assert ok, ("host", st)
+    dC = torch.full((M, N), float("nan"), device="cuda")
+    giga.matmul_sharded([torch.from_numpy(A).cuda()], [torch.from_numpy(B).cuda()], [dC],
+                        M, N, K)
+    ok, st = check_close(dC.cpu().numpy(), ref, S)
+    assert ok, ("sharded", st)
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES[:10])
