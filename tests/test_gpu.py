@@ -560,3 +560,36 @@ def test_trace_timelines(giga, torch_cuda, monkeypatch, capfd):
     assert len(p["ms"]["gemm_rows"]) == rc
     Cref, _ = oracle.gemm(A, B)
     assert check_exact(C, Cref)[0] and check_exact(dC.cpu().numpy(), Cref)[0]
+
+
+def test_concurrent_calls_from_threads_serialise(giga, torch_cuda):
+    """Calls from several host threads at once (include/giga.h: serialised by an internal
+    mutex) each return their own correct result."""
+    import threading
+    shapes = [(300 + 37 * i, 260 + 16 * i, 520 + 64 * i) for i in range(6)]
+    data = []
+    for i, (M, N, K) in enumerate(shapes):
+        A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+        B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+        data.append((A, B, oracle.gemm(A, B)[0]))
+    errors = []
+
+    def work(i):
+        try:
+            A, B, ref = data[i]
+            M, K = A.shape
+            N = B.shape[1]
+            for _ in range(3):
+                C = np.full((M, N), np.nan, np.float32)
+                giga.matmul(A, B, C, M, N, K, 1)
+                if not check_exact(C, ref)[0]:
+                    errors.append(i)
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(shapes))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
