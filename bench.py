@@ -3,6 +3,7 @@
 
     python bench.py --gpus N --steps K --warmup W            (N > 1: under torchrun)
     python bench.py --impl reference ...                      (the CPU fp64 oracle arm)
+    python bench.py --workload dot [--n 67108864]             (the N3 dot product, GB/s)
 
 One step = the whole hot path over one synthetic problem: broadcast B from
 rank 0 (N > 1), the 3xTF32 tcgen05 shard GEMM (the TF32 hi/lo split happens on chip, inside
@@ -184,6 +185,10 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=60.0,
                     help="total seconds of oracle work for --impl reference")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--workload", default="gemm", choices=["gemm", "dot"],
+                    help="gemm (the hot path, default) or dot (the N3 dot product)")
+    ap.add_argument("--n", type=int, default=1 << 26,
+                    help="--workload dot: vector length (the paper's size, P:381)")
     ap.add_argument("--transport", default=os.environ.get("GIGA_TRANSPORT", "nccl"),
                     choices=["nccl", "p2p"],
                     help="N > 1: NCCL pipeline (default) or the peer-to-peer transport "
@@ -191,6 +196,8 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     os.environ["GIGA_TRANSPORT"] = args.transport
+    if args.workload == "dot":
+        return run_dot(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -371,6 +378,97 @@ def main():
         print(json.dumps(line), flush=True)
     giga.finalize()
     if pg is not None:
+        pg.destroy_process_group()
+    return 0
+
+
+def run_dot(args):
+    """--workload dot: the data-parallel dot product (GigaAPI S4.2.8; SURVEY
+    N3). One step = giga_dot_rank on device-resident fp32 vectors (this process's GPU; NCCL
+    all-reduce of the fp64 partial when world > 1) including the 8-byte result read-back.
+    HBM-bound: 8 algorithmic bytes per element (x and y read once)."""
+    import torch
+    import synth
+    from paper_2504_01266_b200 import giga
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+        obj = [giga.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        giga.rank_init(rank, world, local, obj[0])
+    else:
+        giga.rank_init(0, 1, local, None)
+    n = args.n
+    r0, rows = giga.partition(n, world, rank)
+    x = synth.gen_rows_torch(0, 1, n, synth.VECTOR_X, "d4", device=dev)[0, r0:r0 + rows].contiguous()
+    y = synth.gen_rows_torch(0, 1, n, synth.VECTOR_Y, "d4", device=dev)[0, r0:r0 + rows].contiguous()
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    for _ in range(args.warmup):
+        giga.dot_rank(x, y, n, stream=s)
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    # whole call (kernel + all-reduce + 8-byte read-back + host sync), CUDA events on `s`
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(args.steps):
+        val = giga.dot_rank(x, y, n, stream=s)
+    e1.record(s)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if pg:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+    # kernel only: the same kernel, launched back to back through torch's profiler-free path
+    kern = []
+    for _ in range(5):
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(s)
+        giga.dot_rank(x, y, n, stream=s)
+        k1.record(s)
+        k1.synchronize()
+        kern.append(k0.elapsed_time(k1))
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    gbs = 8.0 * n / (ms * 1e-3) / 1e9
+    per_gpu = gbs / world
+    out = None
+    if rank == 0:
+        import oracle  # the cpu_baseline leg
+        xs = synth.gen_vector(min(n, 1 << 24), synth.VECTOR_X, "d4")
+        ys = synth.gen_vector(min(n, 1 << 24), synth.VECTOR_Y, "d4")
+        t0 = time.perf_counter()
+        oracle.dot(xs, ys)
+        tcpu = time.perf_counter() - t0
+        out = {
+            "metric": "dot GB/s (fp32 inputs, fp64 accumulation)", "value": round(gbs, 1),
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
+            "dtype": "f32 in, f64 accumulate", "data": "synthetic (synth d4, uniform [-10,10))",
+            "config": {"workload": f"dot n={n}", "result": val},
+            "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1),
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(per_gpu / peaks["hbm_gbs"], 4),
+                         "note": "whole call per GPU incl. launch, all-reduce and 8-byte "
+                                 "read-back; 8 algorithmic bytes per element",
+                         "single_call_ms_median": round(statistics.median(kern), 5)},
+            "cpu_baseline": {"value": round(8.0 * xs.size / tcpu / 1e9, 3), "unit": "GB/s",
+                             "cores": 1, "kind": "oracle",
+                             "sample": f"first {xs.size} elements, sequential fp64 loop"},
+        }
+        print(json.dumps(out), flush=True)
+    giga.finalize()
+    if pg:
         pg.destroy_process_group()
     return 0
 
