@@ -172,6 +172,37 @@ def run_reference(args):
     return 0
 
 
+def run_reference_dot(args):
+    """--impl reference --workload dot: the fp64 oracle dot product, one host core."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    import synth
+    n = min(args.n, 1 << 26)
+    xs = synth.gen_vector(n, synth.VECTOR_X, "d4")
+    ys = synth.gen_vector(n, synth.VECTOR_Y, "d4")
+    ts = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.dot(xs, ys)
+        if i >= args.warmup:
+            ts.append(time.perf_counter() - t0)
+    sec = statistics.median(ts)
+    gbs = round(8.0 * n / sec / 1e9, 3)
+    print(json.dumps({
+        "impl": "reference", "metric": "dot GB/s (fp32 inputs, fp64 accumulation)",
+        "value": gbs, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"dot n={n}"},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{n} elements, sequential fp64 loop"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -196,10 +227,10 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     os.environ["GIGA_TRANSPORT"] = args.transport
+    if args.impl == "reference":
+        return run_reference_dot(args) if args.workload == "dot" else run_reference(args)
     if args.workload == "dot":
         return run_dot(args)
-    if args.impl == "reference":
-        return run_reference(args)
 
     import torch
     import synth
