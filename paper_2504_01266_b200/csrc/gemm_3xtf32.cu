@@ -46,6 +46,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "kernels.h"
@@ -90,6 +91,10 @@ struct GemmParams {
   int p_kb;       // k-blocks per TMEM accumulation interval (>= 1)
   int n_kb;       // k-blocks per tile
   int m_tiles, n_tiles, num_tiles;
+  // Tail split: tiles [first_split, num_tiles) -- the last, partial wave -- run as two
+  // half-K units each, both TMA reduce-adding into a C region zeroed before the launch
+  // (0 + a + b == a + b in either order: deterministic). num_units = tiles + split tiles.
+  int first_split, num_units;
   int group_m;    // L2 raster: consecutive tiles walk group_m M-tiles before the next N-tile
   unsigned *wave_sync;  // non-null: zeroed counter for the producers' per-wave barrier
   int n_cdst;     // C destinations in CMaps (1 + peers when the gather is fused)
@@ -141,7 +146,8 @@ __device__ __forceinline__ float tf32_lo(float x) {
   return __fsub_rn(x, hi);
 }
 
-__device__ __forceinline__ void tile_coords(int t, const GemmParams &p, int &mb, int &nb) {
+__host__ __device__ __forceinline__ void tile_coords(int t, const GemmParams &p, int &mb,
+                                                    int &nb) {
   const int group_size = p.group_m * p.n_tiles;
   const int g = t / group_size;
   const int first_m = g * p.group_m;
@@ -149,6 +155,23 @@ __device__ __forceinline__ void tile_coords(int t, const GemmParams &p, int &mb,
   const int local = t - g * group_size;
   mb = first_m + local % gm;
   nb = local / gm;
+}
+
+// Work unit u -> tile t and k-block range [kb0, kb1); split units reduce-add their partial.
+__device__ __forceinline__ void unit_coords(int u, const GemmParams &p, int &t, int &kb0,
+                                           int &kb1, bool &split) {
+  if (u < p.first_split) {
+    t = u;
+    kb0 = 0;
+    kb1 = p.n_kb;
+    split = false;
+    return;
+  }
+  const int v = u - p.first_split, mid = p.n_kb / 2;
+  t = p.first_split + (v >> 1);
+  kb0 = (v & 1) ? mid : 0;
+  kb1 = (v & 1) ? p.n_kb : mid;
+  split = true;
 }
 
 template <int CG>
@@ -219,7 +242,6 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int n_int = (p.n_kb + p.p_kb - 1) / p.p_kb;
 
   if (warp == 0) {
     // ======================= TMA producer (both CTAs) =======================
@@ -230,7 +252,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       uint32_t phase = 0;
       int wave = 0;
       uint32_t wave_target = 0;
-      for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++wave) {
+      for (int u = cluster_id; u < p.num_units; u += num_clusters, ++wave) {
         if (p.wave_sync && wave > 0) {
           // Wave barrier among the producers: start loading wave w only when every CTA that
           // has a tile in wave w has issued all loads of wave w-1, so the clusters sharing
@@ -239,7 +261,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
           // 147 -> 35 GB of DRAM reads at 16384^3). A locality hint only, never needed for
           // correctness: the wait gives up after 2 ms, so CTAs kept off the GPU by another
           // kernel cannot deadlock it.
-          const int active = min(num_clusters, p.num_tiles - wave * num_clusters);
+          const int active = min(num_clusters, p.num_units - wave * num_clusters);
           wave_target += uint32_t(active * CG);
           atomicAdd(p.wave_sync, 1u);
           const uint64_t t_start = ptx::globaltimer_ns();
@@ -247,11 +269,13 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
                  ptx::globaltimer_ns() - t_start < 2000000ull)
             __nanosleep(64);
         }
-        int mb, nb;
+        int t, kb0, kb1, mb, nb;
+        bool split;
+        unit_coords(u, p, t, kb0, kb1, split);
         tile_coords(t, p, mb, nb);
         const int m0 = mb * T::TILE_M + int(rank) * BM;
         const int n0 = nb * BN + int(rank) * T::B_COLS;
-        for (int kb = 0; kb < p.n_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *sA = smem + stage * T::STAGE_BYTES;
           uint8_t *sAlo = sA + A_BYTES;
@@ -284,14 +308,17 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
-      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
-        int kb = 0;
+      for (int u = cluster_id; u < p.num_units; u += num_clusters) {
+        int t, kb, kb1;
+        bool split;
+        unit_coords(u, p, t, kb, kb1, split);
+        const int n_int = (kb1 - kb + p.p_kb - 1) / p.p_kb;
         for (int it = 0; it < n_int; ++it, ++acc_iter) {
           const uint32_t buf = acc_iter & 1, use = acc_iter >> 1;
           ptx::mbar_wait(&tempty[buf], (use & 1) ^ 1);
           ptx::tc_fence_after();
           const uint32_t d_tmem = tmem_base + buf * ACC_COLS;
-          const int kb_end = min(kb + p.p_kb, p.n_kb);
+          const int kb_end = min(kb + p.p_kb, kb1);
           uint32_t acc = 0;
           for (; kb < kb_end; ++kb) {
             ptx::mbar_wait(&lofull[stage], phase);
@@ -356,8 +383,11 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     const int xw = warp - XFORM_WARP0;
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
-      for (int kb = 0; kb < p.n_kb; ++kb) {
+    for (int u = cluster_id; u < p.num_units; u += num_clusters) {
+      int t, kb0, kb1;
+      bool split;
+      unit_coords(u, p, t, kb0, kb1, split);
+      for (int kb = kb0; kb < kb1; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         if (do_lo) {
           const uint32_t sA = ptx::smem_u32(smem + stage * T::STAGE_BYTES);
@@ -407,9 +437,12 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     const uint32_t tempty_leader1 = ptx::smem_u32(&tempty[1]) & ptx::kPeerBitMask;
     uint32_t acc_iter = 0;
     uint32_t cphase = 0;  // parity of this warp's C-load barrier
-    for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
-      int mb, nb;
+    for (int u = cluster_id; u < p.num_units; u += num_clusters) {
+      int t, kb0, kb1, mb, nb;
+      bool split;
+      unit_coords(u, p, t, kb0, kb1, split);
       tile_coords(t, p, mb, nb);
+      const int n_int = (kb1 - kb0 + p.p_kb - 1) / p.p_kb;
       float sum[128];  // fp32 running sum of the promoted partials (0 + p == p exactly)
 #pragma unroll
       for (int j = 0; j < 128; ++j) sum[j] = 0.0f;
@@ -480,7 +513,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
           // every destination C buffer (this GPU's, then the peers' when the gather is fused
           // into the epilogue: the same rows land in every GPU's C_full over NVLink)
           for (int dst = 0; dst < p.n_cdst; ++dst) {
-            if (p.accumulate)
+            if (p.accumulate || split)
               ptx::tma_store_add_2d(&cmaps.m[dst], epi_stage + e * EPI_STAGE_BYTES,
                                     ccol0 + 32 * c, crow0);
             else
@@ -725,11 +758,46 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.group_m = group_env ? group_env : GROUP_M;
   p.wave_sync = nullptr;
   p.n_cdst = 1 + ex->n_peer_c;
+  const int nclu = cg == 2 ? num_sms / 2 : num_sms;  // concurrent tiles
+  // Tail split ($GIGA_TAIL_SPLIT=0 disables): when the last wave is at most half full, its
+  // tiles run as two half-K units each, so that wave takes half as long -- e.g. 4096^3:
+  // 256 tiles on 74 pairs = 3 waves + 34 tiles, 4 -> 3.5 wave times. Plain stores only
+  // (no accumulate / load_c / peers: two addends onto zero are order-independent, three are
+  // not), and each half must hold at least one promotion interval.
+  static const bool split_env = [] {
+    const char *e = getenv("GIGA_TAIL_SPLIT");
+    return !(e && *e == '0');
+  }();
+  const int tail = p.num_tiles % nclu;
+  p.first_split = p.num_tiles;
+  p.num_units = p.num_tiles;
+  if (split_env && tail > 0 && 2 * tail <= nclu && !p.accumulate && !p.load_c &&
+      ex->n_peer_c == 0 && p.n_kb >= 2 * p.p_kb) {
+    p.first_split = p.num_tiles - tail;
+    p.num_units = p.num_tiles + tail;
+    // zero the split tiles' bounding rectangle of C (tiles inside it that are not split are
+    // stored over later in the same launch)
+    int mlo = INT32_MAX, mhi = -1, nlo = INT32_MAX, nhi = -1;
+    for (int t = p.first_split; t < p.num_tiles; ++t) {
+      int mb, nb;
+      tile_coords(t, p, mb, nb);
+      mlo = std::min(mlo, mb);
+      mhi = std::max(mhi, mb);
+      nlo = std::min(nlo, nb);
+      nhi = std::max(nhi, nb);
+    }
+    const int64_t r0 = int64_t(mlo) * tile_m;
+    const int64_t r1 = std::min<int64_t>(M, int64_t(mhi + 1) * tile_m);
+    const int64_t c0 = int64_t(nlo) * BN, c1 = std::min<int64_t>(N, int64_t(nhi + 1) * BN);
+    cudaError_t e = cudaMemset2DAsync(C + r0 * ldc + c0, size_t(ldc) * 4, 0,
+                                      size_t(c1 - c0) * 4, size_t(r1 - r0), st);
+    if (e != cudaSuccess) return e;
+  }
   static const bool wave_env = [] {  // producers' per-wave barrier; $GIGA_WAVE_SYNC=0 disables
     const char *e = getenv("GIGA_WAVE_SYNC");
     return !(e && *e == '0');
   }();
-  if (wave_env && p.num_tiles > (cg == 2 ? num_sms / 2 : num_sms)) {
+  if (wave_env && p.num_units > nclu) {
     // one counter per device, zeroed on the launch stream before each launch
     static std::mutex wmu;
     static unsigned *wbuf[64] = {nullptr};
@@ -748,7 +816,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   if (cg == 1) {
     cudaError_t e = ensure_smem_attr<1>();
     if (e != cudaSuccess) return e;
-    const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
+    const int grid = p.num_units < num_sms ? p.num_units : num_sms;
     gemm_3xtf32_kernel<1><<<grid, NUM_THREADS, Tile<1>::SMEM_BYTES, st>>>(tA, tAlo, tB, tBlo,
                                                                           tC, p);
     return cudaGetLastError();
@@ -756,7 +824,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   cudaError_t e = ensure_smem_attr<2>();
   if (e != cudaSuccess) return e;
   const int pairs = num_sms / 2;
-  const int clusters = p.num_tiles < pairs ? p.num_tiles : pairs;
+  const int clusters = p.num_units < pairs ? p.num_units : pairs;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(unsigned(2 * clusters));
   lc.blockDim = dim3(NUM_THREADS);

@@ -593,3 +593,28 @@ def test_concurrent_calls_from_threads_serialise(giga, torch_cuda):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("dist", ["d2", "d3"])
+def test_tail_split_exact_deterministic(giga, torch_cuda, monkeypatch, dist):
+    """2304 x 2304 (81 tiles of 256 x 256 on 74 CTA pairs: the last 7 tiles run as two half-K
+    units that reduce-add into a zeroed C). Within the bound / bit-exact on integers, the same
+    bits on every launch, and the same value set as with the split disabled in a child."""
+    torch = torch_cuda
+    M = N = 2304
+    K = 1040
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, dist)
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
+    dA, dB = _dev(torch, A), _dev(torch, B)
+    outs = []
+    for _ in range(3):
+        dC = torch.full((M, N), float("nan"), device="cuda")
+        giga.gemm_3xtf32(dA, None, dB, None, dC, M, N, K, cta_group=2)
+        outs.append(dC)
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int32), outs[0].view(torch.int32))
+    Cref, S = oracle.gemm(A, B)
+    C = outs[0].cpu().numpy()
+    ok, st = check_exact(C, Cref) if dist == "d3" else check_close(C, Cref, S)
+    assert ok, st
