@@ -463,8 +463,7 @@ int giga_dot(const float *x, const float *y, int64_t n, int ngpus, double *resul
     DevCtx &d = g.devs[i];
     CK(cudaSetDevice(d.dev));
     double part = 0.0;
-    CK(cudaMemcpyAsync(&part, vec_out(d), sizeof(double), cudaMemcpyDeviceToHost, d.compute));
-    CK(cudaStreamSynchronize(d.compute));
+    TRY(read_result(d, d.compute, &part));
     total += part;
   }
   *result = total;
@@ -498,9 +497,7 @@ int giga_dot_rank(const float *x_shard, const float *y_shard, int64_t n, double 
                                   st),
                    "ncclAllReduce(dot)"));
   }
-  CK(cudaMemcpyAsync(result, vec_out(d), sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  return GIGA_OK;
+  return read_result(d, st, result);
 }
 
 // ---- rank-mode peer-to-peer registration (CUDA IPC) ---------------------------------------

@@ -264,12 +264,12 @@ int p2p_dot_allreduce(DevCtx &d, cudaStream_t st, double *result) {
     TRY(write_flag(st, flag_dotdone(page, g.rank), s));
   }
   for (int q = 0; q < g.world; ++q) TRY(wait_flag(st, flag_dotdone(x.flags, q), s));
-  std::vector<double> parts(g.world);
-  CK(cudaMemcpyAsync(parts.data(), dot_part(x.flags, 0, s), sizeof(double) * g.world,
+  // the partials in rank order into the pinned slot (room for 8 = kMaxCDst ranks)
+  CK(cudaMemcpyAsync(d.res_pinned, dot_part(x.flags, 0, s), sizeof(double) * g.world,
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   double tot = 0.0;
-  for (double v : parts) tot += v;
+  for (int q = 0; q < g.world; ++q) tot += d.res_pinned[q];
   *result = tot;
   return GIGA_OK;
 }

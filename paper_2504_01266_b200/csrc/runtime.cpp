@@ -124,6 +124,7 @@ void ctx_destroy(DevCtx &d) {
   if (d.d2h) cudaStreamDestroy(d.d2h);
   for (cudaEvent_t e : {d.ev_b, d.ev_c, d.ev_start, d.ev_last})
     if (e) cudaEventDestroy(e);
+  if (d.res_pinned) cudaFreeHost(d.res_pinned);
   for (auto *v : {&d.ev_kchunk, &d.ev_rchunk, &d.ev_done, &d.ev_trace})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
@@ -269,6 +270,7 @@ constexpr size_t kVecWsBytes = size_t(kDotMaxBlocks) * 8 + 64;
 
 int vec_ws(DevCtx &d) {
   if (d.vec_ws.p) return GIGA_OK;
+  if (!d.res_pinned) CK(cudaMallocHost(reinterpret_cast<void **>(&d.res_pinned), 64));
   TRY(ws_reserve(d, {{&d.vec_ws, kVecWsBytes}}));
   CK(cudaMemset(d.vec_ws.p, 0, kVecWsBytes));  // ticket starts at zero
   return GIGA_OK;
@@ -276,6 +278,15 @@ int vec_ws(DevCtx &d) {
 double *vec_partials(DevCtx &d) { return static_cast<double *>(d.vec_ws.p); }
 double *vec_out(DevCtx &d) { return vec_partials(d) + kDotMaxBlocks; }
 unsigned *vec_ticket(DevCtx &d) { return reinterpret_cast<unsigned *>(vec_out(d) + 1); }
+
+// The fp64 result on the host: an 8-byte copy into the pinned slot (a pageable destination
+// would be staged by the driver), then the stream is awaited.
+int read_result(DevCtx &d, cudaStream_t st, double *out) {
+  CK(cudaMemcpyAsync(d.res_pinned, vec_out(d), sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *out = *d.res_pinned;
+  return GIGA_OK;
+}
 
 int dot_partial(DevCtx &d, const float *x, const float *y, int64_t n, cudaStream_t st) {
   TRY(vec_ws(d));

@@ -64,6 +64,7 @@ struct DevCtx {
   std::vector<cudaEvent_t> ev_trace;   // timing events of class Trace ($GIGA_TRACE)
   Buf A_lo, B_lo, A_pad, B_pad, C_pad, A_h, B_h, C_h;
   Buf vec_ws;  // dot: kDotMaxBlocks fp64 partials, the fp64 result, the ticket (zeroed once)
+  double *res_pinned = nullptr;  // dot: pinned host landing slot of the fp64 result
 };
 
 // Rank-mode peer-to-peer state: this rank's registered B / C_full, its flag page, and the
@@ -228,6 +229,7 @@ double *vec_partials(DevCtx &d);
 double *vec_out(DevCtx &d);
 unsigned *vec_ticket(DevCtx &d);
 int dot_partial(DevCtx &d, const float *x, const float *y, int64_t n, cudaStream_t st);
+int read_result(DevCtx &d, cudaStream_t st, double *out);  // after dot_partial (+ reduction)
 int env_int(const char *name, int dflt);
 bool force_comm();
 Plan make_plan(int64_t M, int64_t K, int world, bool aligned);

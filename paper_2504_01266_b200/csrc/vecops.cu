@@ -7,7 +7,7 @@
 // (P:303). Here: 16-byte vector loads with four in flight per thread (the op is HBM-bound:
 // 8 bytes per element), products of two fp32 values formed exactly in fp64 and summed in
 // fp64, warp-shuffle + shared-memory block reduction, and the per-block partials summed in
-// block order by the last block to finish (an atomic ticket), so one launch returns the
+// a fixed order by the last block to finish (an atomic ticket), so one launch returns the
 // result in device memory and the result is bit-reproducible for a given grid.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -81,14 +81,23 @@ __global__ void __launch_bounds__(kDotThreads) dot_kernel(const float *__restric
   }
   __syncthreads();
   if (!last) return;
-  // the last block sums the partials in block order: deterministic for a given grid
+  // The last block sums the partials in a fixed order (thread t: partials t, t + 256, ... in
+  // sequence; then the same shuffle / shared-memory tree as above): deterministic for a given
+  // grid, and ~5 dependent loads per thread instead of one thread walking all of them.
   __threadfence();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    volatile const double *vp = partials;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += vp[b];
-    *out = s;
-    *ticket = 0;  // ready for the next launch on this workspace
+  double s = 0.0;
+  volatile const double *vp = partials;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += kDotThreads) s += vp[b];
+  s = warp_sum(s);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  if (warp == 0) {
+    double v = lane < kDotThreads / 32 ? red[lane] : 0.0;
+    v = warp_sum(v);
+    if (lane == 0) {
+      *out = v;
+      *ticket = 0;  // ready for the next launch on this workspace
+    }
   }
 }
 
