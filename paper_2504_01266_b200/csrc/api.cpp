@@ -15,6 +15,19 @@
 namespace giga {
 namespace {
 
+// Failure detection for the rank API (stream-ordered calls never wait for NCCL): a
+// communicator that has already failed asynchronously (a peer died, a network error) makes
+// the next call fail fast with GIGA_ERR_COMM instead of queueing work behind it.
+int rank_comm_healthy() {
+  if (!g.rank_comm) return GIGA_OK;
+  const NcclApi *api = nccl_api(nullptr);
+  ncclResult_t ar = ncclSuccess;
+  if (api && api->CommGetAsyncError(g.rank_comm, &ar) == ncclSuccess && ar != ncclSuccess &&
+      ar != ncclInProgress)
+    return nccl_check(ar, "NCCL communicator (asynchronous error from an earlier call)");
+  return GIGA_OK;
+}
+
 int sharded_locked(const float *const *A_shard, float *const *B_buf, float *const *C_full,
                    int64_t M, int64_t N, int64_t K, int ngpus) {
   if (ngpus == 1 && !force_comm()) {
@@ -394,6 +407,7 @@ int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, i
     return fail(GIGA_ERR_INVALID_ARG, "giga_matmul_rank: NULL pointer");
   DevCtx &d = g.devs[0];
   CK(cudaSetDevice(d.dev));
+  TRY(rank_comm_healthy());
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.compute;
   // calls share the rank's workspace: a call starts after the previous one, whatever the
   // caller's streams
@@ -488,6 +502,7 @@ int giga_dot_rank(const float *x_shard, const float *y_shard, int64_t n, double 
     return fail(GIGA_ERR_INVALID_ARG, "giga_dot_rank: NULL pointer");
   DevCtx &d = g.devs[0];
   CK(cudaSetDevice(d.dev));
+  TRY(rank_comm_healthy());
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.compute;
   TRY(dot_partial(d, x_shard, y_shard, rows, st));
   if (g.p2p.ready && g.world > 1) return p2p_dot_allreduce(d, st, result);
