@@ -100,13 +100,15 @@ def test_dot_over_virtual_gpus(giga_virtual, torch_cuda, world):
 
 # ---- rank API (one process per rank) with the peer-to-peer transport ----------------------
 
-def _rank_worker(rank, world, port, M, N, K, q):
+def _rank_worker(rank, world, port, M, N, K, q, transport="p2p", own_device=False,
+                 extra_env=None):
     import os
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
-    os.environ.update({"GIGA_TRANSPORT": "p2p", "GIGA_BCAST_CHUNKS": "3",
+    os.environ.update({"GIGA_TRANSPORT": transport, "GIGA_BCAST_CHUNKS": "3",
                        "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    os.environ.update(extra_env or {})
     try:
         import torch
         import torch.distributed as dist
@@ -114,8 +116,14 @@ def _rank_worker(rank, world, port, M, N, K, q):
         import synth
         from paper_2504_01266_b200 import giga
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        torch.cuda.set_device(0)
-        giga.rank_init(rank, world, 0, None)
+        dev = rank if own_device else 0
+        torch.cuda.set_device(dev)
+        if transport == "nccl":  # the NCCL id travels over the gloo group (plumbing)
+            obj = [giga.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            giga.rank_init(rank, world, dev, obj[0])
+        else:
+            giga.rank_init(rank, world, dev, None)
         r0, rows = giga.partition(M, world, rank)
         A = synth.gen_rows(r0, rows, K, synth.MATRIX_A, "d3")
         Bn = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
@@ -123,10 +131,11 @@ def _rank_worker(rank, world, port, M, N, K, q):
         dB = torch.from_numpy(Bn).cuda() if rank == 0 else torch.full((K, N), float("nan"),
                                                                       device="cuda")
         dC = torch.full((M, N), float("nan"), device="cuda")
-        blob = giga.p2p_export(dB, dC)
-        blobs = [None] * world
-        dist.all_gather_object(blobs, blob)
-        giga.p2p_import(blobs)
+        if transport == "p2p":
+            blob = giga.p2p_export(dB, dC)
+            blobs = [None] * world
+            dist.all_gather_object(blobs, blob)
+            giga.p2p_import(blobs)
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         for _ in range(3):  # repeated calls: flag call numbers and back-pressure
@@ -214,3 +223,124 @@ def test_host_buffers_p2p_virtual(giga_virtual, torch_cuda, monkeypatch, world, 
     Cref, _ = oracle.gemm(A, B)
     ok, st = check_exact(C, Cref)
     assert ok, st
+
+
+def test_rank_worker_nccl_world1(torch_cuda):
+    """The NCCL branch of the rank worker the physical-GPU tests use (unique id over gloo,
+    rank_init with the id, pipeline with a communicator: GIGA_FORCE_COMM) at world size 1."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_rank_worker, args=(0, 1, port, 1000, 520, 2064, q, "nccl", True,
+                                               {"GIGA_FORCE_COMM": "1"}))
+    p.start()
+    try:
+        rank, ok_c, ok_b, ok_d, err = q.get(timeout=240)
+    finally:
+        p.join(timeout=30)
+        if p.is_alive():
+            p.kill()
+    assert ok_c and ok_b and ok_d, err
+
+
+# ---- physical GPUs (skipped on a one-GPU box; run as they are on a multi-GPU one) ----------
+
+def _ngpus():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+multi = pytest.mark.skipif(_ngpus() < 2, reason="needs at least two physical GPUs")
+
+
+@multi
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_rank_api_physical_gpus(torch_cuda, transport):
+    """One process per GPU on distinct devices: NCCL pipeline or p2p transport (IPC, TMA
+    stores into peer memory), repeated calls, B distribution, C gather, dot all-reduce."""
+    import socket
+    import torch.multiprocessing as mp
+    world = min(4, _ngpus())
+    M, N, K = 1000 * world + 7, 520, 2064
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_worker, args=(r, world, port, M, N, K, q, transport, True))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        res = sorted(q.get(timeout=300) for _ in range(world))
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for rank, ok_c, ok_b, ok_d, err in res:
+        assert ok_c and ok_b and ok_d, (rank, ok_c, ok_b, ok_d, err)
+
+
+@multi
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_single_process_physical_gpus(torch_cuda, monkeypatch, transport):
+    """giga_init(g) over g distinct devices, device-resident shards: every GPU ends with all of
+    C, bit-exact on integer inputs."""
+    torch = torch_cuda
+    from paper_2504_01266_b200 import giga
+    monkeypatch.setenv("GIGA_TRANSPORT", transport)
+    world = min(4, _ngpus())
+    M, N, K = 777 * world, 516, 1040
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+    giga.finalize()
+    giga.init(world)
+    try:
+        shards, Bs, Cs = [], [], []
+        for r in range(world):
+            r0, rows = giga.partition(M, world, r)
+            dev = torch.device("cuda", r)
+            shards.append(torch.from_numpy(np.ascontiguousarray(A[r0:r0 + rows])).to(dev))
+            Bs.append(torch.from_numpy(B).to(dev) if r == 0 else
+                      torch.full((K, N), float("nan"), device=dev))
+            Cs.append(torch.full((M, N), float("nan"), device=dev))
+        giga.matmul_sharded(shards, Bs, Cs, M, N, K)
+        Cref, _ = oracle.gemm(A, B)
+        for r in range(world):
+            assert check_exact(Cs[r].cpu().numpy(), Cref)[0], r
+        C = np.empty((M, N), np.float32)
+        giga.matmul(A, B, C, M, N, K, world)  # host buffers over the same GPUs
+        assert check_exact(C, Cref)[0]
+    finally:
+        giga.finalize()
+
+
+@multi
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_bench_physical_gpus(torch_cuda, transport):
+    """bench.py under torchrun on two distinct GPUs: one JSON line, max-over-ranks timing."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+         "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+         "--steps", "3", "--warmup", "3", "--config", "c2_4096", "--no-cpu-baseline",
+         "--e2e-steps", "1", "--transport", transport], cwd=root, capture_output=True,
+        text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["transport"] == transport and d["value"] > 0
