@@ -32,9 +32,29 @@
  *
  * Ownership: the caller owns every pointer passed in; the library never keeps a caller
  * pointer after returning. The library owns its streams, events, communicators and
- * workspace (TF32 low-part buffers, padded copies), freed in giga_finalize().
+ * workspace (padded copies, host-path staging buffers, the pre-split low parts in that
+ * comparison mode), freed in giga_finalize().
  *
  * Threading: calls are serialised by an internal mutex (one call at a time per process).
+ *
+ * Determinism: for a given shape, device count and environment every call returns the same
+ * bits (fixed reduction orders everywhere; no atomics decide an order of additions).
+ *
+ * Environment (read at call time unless noted; defaults in brackets):
+ *   GIGA_TRANSPORT       nccl | p2p: the N > 1 exchange (NCCL collectives, or copy engines for
+ *                        B and the gather fused into the GEMM epilogue) [nccl]
+ *   GIGA_BCAST_CHUNKS, GIGA_GATHER_CHUNKS  chunk counts of the N > 1 plans [6 / 16 p2p, 4]
+ *   GIGA_COMM_SMS, GIGA_NCCL_MAX_CTAS      SMs left to NCCL beside the GEMM [8, = COMM_SMS]
+ *   GIGA_FORCE_COMM      1: run the NCCL pipeline even at one GPU (testing) [0]
+ *   GIGA_TRACE           1: print a JSON timeline of each pipelined call on stderr [0]
+ *   GIGA_HOST_H2D_GBS, GIGA_HOST_D2H_GBS, GIGA_HOST_GEMM_TFLOPS  rates of the host-path
+ *                        schedule model [50, 50, 255]
+ *   GIGA_LO_PRESPLIT     1: 3xTF32 low parts split in HBM (comparison mode; once) [0]
+ *   GIGA_PROMOTE_KBLOCKS TMEM accumulation interval in 16-deep k-blocks (once) [8]
+ *   GIGA_CTA_GROUP       1 | 2: force the GEMM tile variant (once) [by shape]
+ *   GIGA_WAVE_SYNC, GIGA_TAIL_SPLIT  0 disables the GEMM's wave barrier / tail split (once) [1]
+ *   GIGA_GROUP_M, GIGA_L2_PROMO      raster group, TMA L2 promotion (once) [8, 2 = 128 B]
+ *   GIGA_NCCL_PATH       libnccl.so.2 to dlopen if the default lookup fails
  */
 #ifndef GIGA_H_
 #define GIGA_H_
