@@ -486,6 +486,44 @@ def test_rank_api_world1_on_torch_stream(torch_cuda):
         g.init(1)
 
 
+@pytest.mark.parametrize("config", ["c3_16384", "c5_32768"])
+def test_bench_launch_configuration_full_size(torch_cuda, config):
+    """bench.py's exact path at full size: rank_init(0, 1), device-resident synthetic d2
+    inputs generated on the GPU as bench.py does, giga_matmul_rank on a side stream, repeated
+    (warm workspace); sampled rows of C against the oracle."""
+    torch = torch_cuda
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    M, N, K = bench.CONFIGS[config]
+    from paper_2504_01266_b200 import giga as g
+    g.finalize()
+    g.rank_init(0, 1, 0, None)
+    try:
+        A = synth.gen_rows_torch(0, M, K, synth.MATRIX_A, "d2", device="cuda")
+        B = synth.gen_rows_torch(0, K, N, synth.MATRIX_B, "d2", device="cuda")
+        C = torch.full((M, N), float("nan"), device="cuda")
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        for _ in range(2):
+            g.matmul_rank(A, B, C, M, N, K, stream=s)
+        s.synchronize()
+        rows = _sampled_rows(M, np.random.default_rng(7), extra=6)
+        Cs = C[torch.from_numpy(rows).cuda()].cpu().numpy()
+        del A, B, C
+        torch.cuda.empty_cache()
+        Ar = synth.gen_rows_index(rows, K, synth.MATRIX_A, "d2")
+        Bn = synth.gen_rows_torch(0, K, N, synth.MATRIX_B, "d2", device="cpu").numpy()
+        Cref, S = oracle.gemm(Ar, Bn)
+        ok, st = check_close(Cs, Cref, S)
+        assert ok, st
+    finally:
+        g.finalize()
+        g.init(1)
+
+
 def test_presplit_comparison_mode_end_to_end(torch_cuda, tmp_path):
     """GIGA_LO_PRESPLIT=1 (lo arrays split in HBM, the earlier design kept for comparison)
     through the public calls -- device shards, host buffers, the forced-NCCL pipeline -- gives
