@@ -406,7 +406,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": vs_base,
             "wall_ms_per_step": round(wall_ms / args.steps, 4),
-            "dtype": "f32 (3xTF32 tensor, fp32-accurate)", "data": "synthetic",
+            "dtype": "f32", "arithmetic": "3xTF32 tcgen05 MMAs + fp32 RN promotion "
+                                          "(fp32-accurate: <= 1e-5 sum|A||B|)",
+            "data": "synthetic",
             "config": {"workload": f"{args.config} M={M} N={N} K={K}", "dist": args.dist,
                        "parallelism": f"row-split x{world}",
                        "transport": args.transport if world > 1 else "none (1 GPU)",
@@ -495,7 +497,8 @@ def run_dot(args):
             "metric": "dot GB/s (fp32 inputs, fp64 accumulation)", "value": round(gbs, 1),
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
-            "dtype": "f32 in, f64 accumulate", "data": "synthetic (synth d4, uniform [-10,10))",
+            "dtype": "f64", "arithmetic": "f32 inputs, exact products, f64 accumulation",
+            "data": "synthetic (synth d4, uniform [-10,10))",
             "config": {"workload": f"dot n={n}", "result": val},
             "roofline": {"bound": "hbm", "achieved": round(per_gpu, 1),
                          "peak": peaks["hbm_gbs"], "unit": "GB/s",
