@@ -73,7 +73,8 @@ HostRates host_rates_default() {
   return r;
 }
 
-double host_plan_model(const HostPlan &p, int64_t M, int64_t N, int64_t K, const HostRates &r) {
+double host_plan_model(const HostPlan &p, int64_t /*M: rows are in p.rb*/, int64_t N, int64_t K,
+                       const HostRates &r) {
   double th = 0, tc = 0, td = 0;
   double arrive_k[kHostMaxChunks], arrive_r[kHostMaxChunks];
   for (int c = 0; c < p.P; ++c) {

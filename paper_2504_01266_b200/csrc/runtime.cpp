@@ -60,7 +60,8 @@ cudaEvent_t pool_event(int dev) {
 // workspace: grow-only per-GPU buffers, reserved transactionally so a failed call leaves the
 // device memory footprint exactly as it found it.
 
-int ws_reserve(DevCtx &d, std::initializer_list<std::pair<Buf *, size_t>> req) {
+int ws_reserve(DevCtx & /*d: the buffers carry their device*/,
+               std::initializer_list<std::pair<Buf *, size_t>> req) {
   std::vector<std::pair<Buf *, void *>> fresh;
   for (auto &r : req) {
     if (r.first->bytes >= r.second) continue;
