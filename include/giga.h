@@ -252,6 +252,20 @@ int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const
                         float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, int terms,
                         int promote_kblocks, int cta_group, void *stream);
 
+/* The work schedule of one giga_gemm_3xtf32 launch (C stored, default promotion interval)
+ * over an M x N x K product on `num_sms` SMs (<= 0: 148), computed on the host exactly as
+ * the launch computes it (no GPU needed). out must hold 8 values:
+ * out[0] = CTA-group size (1: 128 x 256 tiles, 2: 256 x 256 tiles on CTA pairs),
+ * out[1] = tiles, out[2] = concurrent tiles (clusters), out[3] = k-blocks (16 deep) per tile,
+ * out[4] = first_split: tiles [0, first_split) run whole, out[5] = s: every later tile runs
+ * as s units over consecutive k-block ranges [n_kb*q/s, n_kb*(q+1)/s), out[6] = work units,
+ * out[7] = how the parts combine, both deterministic (the same bits on every launch of the
+ * shape): 0 no split, 1 two halves TMA reduce-add into a C region zeroed before the launch
+ * (0 + a + b is order-independent), 2 the parts' fp32 partials are added in the order
+ * q = 0, 1, ..., s-1 by the part that finishes last (grids under one wave only).
+ * $GIGA_TAIL_SPLIT=0 disables the k-split (s = 1). Errors: INVALID_ARG. */
+int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *out);
+
 /* ------------------------------------------------------------------------------------ */
 /* Kernel timing (bench.py's roofline): when enabled, CUDA events bracket every GEMM and
  * split launch on the stream it is launched on; giga_timing_read synchronises on the

@@ -269,6 +269,7 @@ int giga_finalize(void) {
   g.rank_comm = nullptr;
   if (!g.devs.empty()) cudaSetDevice(g.devs[0].dev);
   p2p_release();
+  release_gemm_caches();
   for (auto &d : g.devs) ctx_destroy(d);
   g.devs.clear();
   {
@@ -663,6 +664,19 @@ int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const
     return launch_gemm_3xtf32(A, A_lo, B, B_lo, C, M, N, K, ldc, terms, promote_kblocks, st,
                               cta_group);
   }));
+  return GIGA_OK;
+}
+
+int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *out) {
+  if (!out) return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_schedule: NULL out");
+  TRY(check_dims(M, N, K));
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+    return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_schedule: dimension above 2^31 - 1");
+  const GemmSchedule s = gemm_schedule(M, N, K, num_sms > 0 ? num_sms : 148, 0, true,
+                                       default_promote_kblocks());
+  const int64_t v[8] = {s.cg,          s.num_tiles, s.nclu,      s.n_kb,
+                        s.first_split, s.s,         s.num_units, s.mode};
+  for (int i = 0; i < 8; ++i) out[i] = v[i];
   return GIGA_OK;
 }
 

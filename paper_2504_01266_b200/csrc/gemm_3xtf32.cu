@@ -48,6 +48,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -70,6 +71,7 @@ constexpr int GROUP_M = 8;                       // L2 raster: default M-tiles p
 constexpr size_t SMEM_RING = 192 * 1024;         // operand ring per CTA
 constexpr uint32_t EPI_STAGE_BYTES = 32 * 32 * 4;  // per epilogue warp: 32 rows x 32 fp32
 constexpr uint32_t EPI_BYTES = NUM_EPI_WARPS * EPI_STAGE_BYTES;  // 32 KiB C staging
+constexpr size_t EPI_SLOT_BYTES = 32 * 128 * 4;  // K-split partial of one epilogue warp
 }  // namespace cfg
 
 template <int CG>
@@ -91,10 +93,17 @@ struct GemmParams {
   int p_kb;       // k-blocks per TMEM accumulation interval (>= 1)
   int n_kb;       // k-blocks per tile
   int m_tiles, n_tiles, num_tiles;
-  // Tail split: tiles [first_split, num_tiles) -- the last, partial wave -- run as two
-  // half-K units each, both TMA reduce-adding into a C region zeroed before the launch
-  // (0 + a + b == a + b in either order: deterministic). num_units = tiles + split tiles.
-  int first_split, num_units;
+  // K-split units (deterministic; plan_ksplit): tiles [0, first_split) run whole; each tile
+  // t >= first_split runs as `split_s` units over consecutive k-block ranges, combined by
+  // split_mode. kSplitWorkspace: a part's epilogue writes its fp32 partial to the workspace
+  // slot of (tile, part) and counts itself in; the last part to arrive sums the tile's parts
+  // in part order (p0 + p1 + ...: the same bits whichever part arrives last) and stores the
+  // tile like a whole one. num_units = first_split + (num_tiles - first_split) * split_s.
+  int first_split, split_s, num_units;
+  int split_mode;   // kSplitReduce: parts TMA reduce-add into C zeroed before the launch
+                    // (s = 2: 0 + a + b is order-independent); kSplitWorkspace: as above
+  float *sk_ws;     // (num_tiles - first_split) * split_s * CG * 8 slots of 32 x 128 fp32
+  unsigned *sk_cnt; // (num_tiles - first_split) * CG * 8 arrival counters, 0 between launches
   int group_m;    // L2 raster: consecutive tiles walk group_m M-tiles before the next N-tile
   unsigned *wave_sync;  // non-null: zeroed counter for the producers' per-wave barrier
   int n_cdst;     // C destinations in CMaps (1 + peers when the gather is fused)
@@ -157,21 +166,22 @@ __host__ __device__ __forceinline__ void tile_coords(int t, const GemmParams &p,
   nb = local / gm;
 }
 
-// Work unit u -> tile t and k-block range [kb0, kb1); split units reduce-add their partial.
-__device__ __forceinline__ void unit_coords(int u, const GemmParams &p, int &t, int &kb0,
-                                           int &kb1, bool &split) {
+// Work unit u -> tile t and k-block range [kb0, kb1); part = -1 for a whole tile, else the
+// unit's index among its tile's split_s parts (consecutive units: they run side by side).
+__host__ __device__ __forceinline__ void unit_coords(int u, const GemmParams &p, int &t,
+                                                    int &kb0, int &kb1, int &part) {
   if (u < p.first_split) {
     t = u;
     kb0 = 0;
     kb1 = p.n_kb;
-    split = false;
+    part = -1;
     return;
   }
-  const int v = u - p.first_split, mid = p.n_kb / 2;
-  t = p.first_split + (v >> 1);
-  kb0 = (v & 1) ? mid : 0;
-  kb1 = (v & 1) ? p.n_kb : mid;
-  split = true;
+  const int v = u - p.first_split;
+  t = p.first_split + v / p.split_s;
+  part = v % p.split_s;
+  kb0 = int(int64_t(p.n_kb) * part / p.split_s);
+  kb1 = int(int64_t(p.n_kb) * (part + 1) / p.split_s);
 }
 
 template <int CG>
@@ -269,9 +279,8 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
                  ptx::globaltimer_ns() - t_start < 2000000ull)
             __nanosleep(64);
         }
-        int t, kb0, kb1, mb, nb;
-        bool split;
-        unit_coords(u, p, t, kb0, kb1, split);
+        int t, kb0, kb1, mb, nb, part;
+        unit_coords(u, p, t, kb0, kb1, part);
         tile_coords(t, p, mb, nb);
         const int m0 = mb * T::TILE_M + int(rank) * BM;
         const int n0 = nb * BN + int(rank) * T::B_COLS;
@@ -309,9 +318,8 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
       for (int u = cluster_id; u < p.num_units; u += num_clusters) {
-        int t, kb, kb1;
-        bool split;
-        unit_coords(u, p, t, kb, kb1, split);
+        int t, kb, kb1, part;
+        unit_coords(u, p, t, kb, kb1, part);
         const int n_int = (kb1 - kb + p.p_kb - 1) / p.p_kb;
         for (int it = 0; it < n_int; ++it, ++acc_iter) {
           const uint32_t buf = acc_iter & 1, use = acc_iter >> 1;
@@ -384,9 +392,8 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int u = cluster_id; u < p.num_units; u += num_clusters) {
-      int t, kb0, kb1;
-      bool split;
-      unit_coords(u, p, t, kb0, kb1, split);
+      int t, kb0, kb1, part;
+      unit_coords(u, p, t, kb0, kb1, part);
       for (int kb = kb0; kb < kb1; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         if (do_lo) {
@@ -438,9 +445,8 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     uint32_t acc_iter = 0;
     uint32_t cphase = 0;  // parity of this warp's C-load barrier
     for (int u = cluster_id; u < p.num_units; u += num_clusters) {
-      int t, kb0, kb1, mb, nb;
-      bool split;
-      unit_coords(u, p, t, kb0, kb1, split);
+      int t, kb0, kb1, mb, nb, part;
+      unit_coords(u, p, t, kb0, kb1, part);
       tile_coords(t, p, mb, nb);
       const int n_int = (kb1 - kb0 + p.p_kb - 1) / p.p_kb;
       float sum[128];  // fp32 running sum of the promoted partials (0 + p == p exactly)
@@ -468,11 +474,49 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
             ptx::mbar_arrive_cluster(buf ? tempty_leader1 : tempty_leader0);
         }
       }
+      if (part >= 0 && p.split_mode == kSplitWorkspace) {
+        // K-split part: publish this warp's 32 x 128 partial (lane-interleaved float4s: one
+        // coalesced 512-byte row of the slot per store), count in; the last of the tile's
+        // parts adds all of them in part order and carries on as a whole tile.
+        const int st_idx = ((t - p.first_split) * CG + int(rank)) * NUM_EPI_WARPS + e;
+        const float4 *slot0 = reinterpret_cast<const float4 *>(p.sk_ws) +
+                        size_t(st_idx) * p.split_s * (32 * 32) + lane;  // this lane's column
+        float4 *mine = const_cast<float4 *>(slot0) + part * (32 * 32);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          __stcg(mine + j * 32,
+                 make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]));
+        __threadfence();
+        __syncwarp();
+        unsigned arrived = 0;
+        if (lane == 0) arrived = atomicAdd(&p.sk_cnt[st_idx], 1u);
+        arrived = __shfl_sync(0xffffffffu, arrived, 0);
+        if (arrived != unsigned(p.split_s - 1)) continue;  // another part finishes the tile
+        if (lane == 0) p.sk_cnt[st_idx] = 0;  // every part has counted in: reset for next launch
+        __threadfence();
+        // the ordered sum reads every part from memory, own slot included (this thread wrote it)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float4 tot = __ldcg(slot0 + j * 32);
+          for (int q = 1; q < p.split_s; ++q) {
+            const float4 v = __ldcg(slot0 + q * (32 * 32) + j * 32);
+            tot.x = __fadd_rn(tot.x, v.x);
+            tot.y = __fadd_rn(tot.y, v.y);
+            tot.z = __fadd_rn(tot.z, v.z);
+            tot.w = __fadd_rn(tot.w, v.w);
+          }
+          sum[4 * j] = tot.x;
+          sum[4 * j + 1] = tot.y;
+          sum[4 * j + 2] = tot.z;
+          sum[4 * j + 3] = tot.w;
+        }
+      }
       // C: this warp's 32 rows x 128 columns go out as four 32 x 32 TMA bulk stores through
       // its 4 KiB staging tile (128B-swizzled rows: 16-byte chunk j of row r sits at chunk
       // j ^ (r & 7), so each 8-lane phase of a v4 store covers all 32 banks). The TMA unit
       // writes whole 128-byte row segments and clips rows >= M / columns >= N. Accumulate
       // mode (K-chunked pipelines) uses the TMA reduce-add: C += partial in fp32.
+      const bool reduce_store = p.accumulate || (part >= 0 && p.split_mode == kSplitReduce);
       const uint32_t stg = ptx::smem_u32(epi_stage + e * EPI_STAGE_BYTES);
       const int crow0 = mb * T::TILE_M + int(rank) * BM + quad * 32;
       const int ccol0 = nb * BN + half * 128;
@@ -513,7 +557,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
           // every destination C buffer (this GPU's, then the peers' when the gather is fused
           // into the epilogue: the same rows land in every GPU's C_full over NVLink)
           for (int dst = 0; dst < p.n_cdst; ++dst) {
-            if (p.accumulate || split)
+            if (reduce_store)
               ptx::tma_store_add_2d(&cmaps.m[dst], epi_stage + e * EPI_STAGE_BYTES,
                                     ccol0 + 32 * c, crow0);
             else
@@ -639,6 +683,148 @@ static int num_sms_current() {
   return n > 0 ? n : 148;
 }
 
+// ---- K-split plan and workspace ------------------------------------------------------------
+// Persistent clusters take units round-robin, so T tiles on `nclu` concurrent clusters last
+// ceil(T / nclu) tile times. Two ways to cut tiles into k-parts, both deterministic:
+//   * kSplitReduce (s = 2, plain-store launches only): the two halves TMA reduce-add into a
+//     C region zeroed before the launch; 0 + a + b == a + b in either order. Used for the
+//     last wave of a multi-wave launch when it is at most half full (4096^3: 256 tiles on 74
+//     pairs = 3 waves + 34 tiles -> 3.5 wave times, measured -11%), and for s = 2 below.
+//   * kSplitWorkspace (any s, any epilogue mode): parts write fp32 partials to a workspace,
+//     the last part of a tile to finish adds them in part order. Only for grids that fill
+//     less than one wave (tiles < nclu), e.g. 24 tiles of 512 x 1536 x 2048 on 148 SMs:
+//     measured -41% with 4 parts. Cost model (k-block times; fitted to scripts/ksplit_sweep.py
+//     on B200): ceil(n_kb / s) + 14 + 5 s against n_kb, one part wave (tiles * s <= nclu);
+//     the 14 + 5 s is the partial write, the arrival count and the latency-bound ordered read
+//     of s partials. Cutting the tail of a multi-wave launch into more than two parts measured
+//     slower than whole tiles (the tensor pipe ran 84% busy in part waves against 93%), so it
+//     is not planned.
+// The workspace is capped at kKSplitMaxSlots 16 KiB slots. $GIGA_KSPLIT_S forces s for
+// under-filled grids (experiments).
+constexpr int kKSplitMaxS = 32;
+constexpr int64_t kKSplitMaxSlots = 8192;  // 128 MiB
+
+KSplitPlan plan_ksplit(int num_tiles, int nclu, int n_kb, int cg, bool plain, int p_kb) {
+  KSplitPlan whole{num_tiles, 1, kSplitNone};
+  if (num_tiles < 1 || nclu < 1 || n_kb < 2) return whole;
+  if (num_tiles >= nclu) {
+    const int tail = num_tiles % nclu;
+    if (plain && tail > 0 && 2 * tail <= nclu && n_kb >= 2 * p_kb)
+      return KSplitPlan{num_tiles - tail, 2, kSplitReduce};
+    return whole;
+  }
+  static const int forced_s = [] {
+    const char *e = getenv("GIGA_KSPLIT_S");
+    return (e && atoi(e) > 0) ? atoi(e) : 0;
+  }();
+  KSplitPlan best = whole;
+  double best_cost = forced_s ? 1e300 : 0.97 * n_kb;
+  for (int s = 2; s <= std::min(n_kb, kKSplitMaxS); ++s) {
+    if (int64_t(num_tiles) * s > nclu && !forced_s) break;  // one part wave
+    if (int64_t(num_tiles) * s * cg * cfg::NUM_EPI_WARPS > kKSplitMaxSlots) break;
+    if (forced_s && s != forced_s) continue;
+    const bool reduce = plain && s == 2;
+    const double cost = double((n_kb + s - 1) / s) * double((int64_t(num_tiles) * s + nclu - 1) / nclu) +
+                        (reduce ? 4.0 : 14.0 + 5.0 * s);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = KSplitPlan{0, s, reduce ? kSplitReduce : kSplitWorkspace};
+    }
+  }
+  return best;
+}
+
+// One workspace per (device, stream): launches on one stream are ordered, so they can share
+// it; launches on different streams (virtual GPUs sharing a device, concurrent callers) get
+// their own. Grow-only; growth waits for the stream's earlier launches (they may still read
+// the old slots). The counters start at zero and every launch leaves them at zero.
+struct KSplitWs {
+  float *ws = nullptr;
+  unsigned *cnt = nullptr;
+  size_t ws_bytes = 0, cnt_n = 0;
+  int dev = 0;
+};
+static std::mutex g_ksplit_mu;
+static std::vector<std::pair<cudaStream_t, KSplitWs>> g_ksplit;
+
+bool ksplit_workspace(cudaStream_t st, size_t ws_bytes, size_t cnt_n, float **ws,
+                      unsigned **cnt) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lk(g_ksplit_mu);
+  KSplitWs *w = nullptr;
+  for (auto &e : g_ksplit)
+    if (e.first == st && e.second.dev == dev) w = &e.second;
+  if (!w || w->ws_bytes < ws_bytes || w->cnt_n < cnt_n) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return false;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return false;
+    KSplitWs fresh;
+    fresh.dev = dev;
+    fresh.ws_bytes = std::max(ws_bytes, w ? w->ws_bytes : 0);
+    fresh.cnt_n = std::max(cnt_n, w ? w->cnt_n : 0);
+    if (cudaMalloc(&fresh.ws, fresh.ws_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (cudaMalloc(&fresh.cnt, fresh.cnt_n * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemsetAsync(fresh.cnt, 0, fresh.cnt_n * sizeof(unsigned), st) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(fresh.ws);
+      if (fresh.cnt) cudaFree(fresh.cnt);
+      return false;
+    }
+    if (w) {
+      cudaFree(w->ws);
+      cudaFree(w->cnt);
+      *w = fresh;
+    } else {
+      g_ksplit.push_back({st, fresh});
+      w = &g_ksplit.back().second;
+    }
+  }
+  *ws = w->ws;
+  *cnt = w->cnt;
+  return true;
+}
+
+void release_gemm_caches() {
+  std::lock_guard<std::mutex> lk(g_ksplit_mu);
+  for (auto &e : g_ksplit) {
+    cudaSetDevice(e.second.dev);
+    cudaDeviceSynchronize();
+    cudaFree(e.second.ws);
+    cudaFree(e.second.cnt);
+  }
+  g_ksplit.clear();
+}
+
+GemmSchedule gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int cta_group,
+                           bool plain, int p_kb) {
+  GemmSchedule s;
+  s.cg = (cta_group == 1 || cta_group == 2) ? cta_group : choose_cta_group(M, N, num_sms);
+  const int tile_m = cfg::BM * s.cg;
+  s.m_tiles = int((M + tile_m - 1) / tile_m);
+  s.n_tiles = int((N + cfg::BN - 1) / cfg::BN);
+  s.num_tiles = s.m_tiles * s.n_tiles;
+  s.nclu = s.cg == 2 ? num_sms / 2 : num_sms;
+  s.n_kb = int((K + cfg::BK - 1) / cfg::BK);
+  if (p_kb <= 0 || p_kb > s.n_kb) p_kb = s.n_kb;
+  // $GIGA_TAIL_SPLIT=0 disables the k-split
+  static const bool split_env = [] {
+    const char *e = getenv("GIGA_TAIL_SPLIT");
+    return !(e && *e == '0');
+  }();
+  const KSplitPlan kp = split_env ? plan_ksplit(s.num_tiles, s.nclu, s.n_kb, s.cg, plain, p_kb)
+                                  : KSplitPlan{s.num_tiles, 1, kSplitNone};
+  s.first_split = kp.first_split;
+  s.s = kp.s;
+  s.mode = kp.mode;
+  s.num_units = s.first_split + (s.num_tiles - s.first_split) * s.s;
+  return s;
+}
+
 cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t n4 = (n + 3) / 4;
@@ -747,10 +933,11 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.n_kb = int((K + BK - 1) / BK);
   int pk = promote_kblocks < 0 ? default_promote_kblocks() : promote_kblocks;
   p.p_kb = (pk == 0 || pk > p.n_kb) ? p.n_kb : pk;
-  const int tile_m = BM * cg;
-  p.m_tiles = int((M + tile_m - 1) / tile_m);
-  p.n_tiles = int((N + BN - 1) / BN);
-  p.num_tiles = p.m_tiles * p.n_tiles;
+  const bool plain = !p.accumulate && !p.load_c && ex->n_peer_c == 0;
+  const GemmSchedule sch = gemm_schedule(M, N, K, num_sms, cg, plain, p.p_kb);
+  p.m_tiles = sch.m_tiles;
+  p.n_tiles = sch.n_tiles;
+  p.num_tiles = sch.num_tiles;
   static int group_env = [] {
     const char *e = getenv("GIGA_GROUP_M");
     return (e && atoi(e) > 0) ? atoi(e) : 0;
@@ -758,23 +945,22 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.group_m = group_env ? group_env : GROUP_M;
   p.wave_sync = nullptr;
   p.n_cdst = 1 + ex->n_peer_c;
-  const int nclu = cg == 2 ? num_sms / 2 : num_sms;  // concurrent tiles
-  // Tail split ($GIGA_TAIL_SPLIT=0 disables): when the last wave is at most half full, its
-  // tiles run as two half-K units each, so that wave takes half as long -- e.g. 4096^3:
-  // 256 tiles on 74 pairs = 3 waves + 34 tiles, 4 -> 3.5 wave times. Plain stores only
-  // (no accumulate / load_c / peers: two addends onto zero are order-independent, three are
-  // not), and each half must hold at least one promotion interval.
-  static const bool split_env = [] {
-    const char *e = getenv("GIGA_TAIL_SPLIT");
-    return !(e && *e == '0');
-  }();
-  const int tail = p.num_tiles % nclu;
-  p.first_split = p.num_tiles;
-  p.num_units = p.num_tiles;
-  if (split_env && tail > 0 && 2 * tail <= nclu && !p.accumulate && !p.load_c &&
-      ex->n_peer_c == 0 && p.n_kb >= 2 * p.p_kb) {
-    p.first_split = p.num_tiles - tail;
-    p.num_units = p.num_tiles + tail;
+  const int nclu = sch.nclu;
+  // K-split (gemm_schedule): kSplitReduce halves reduce-add into C zeroed here; kSplitWorkspace
+  // partials go through a workspace owned by this stream (ksplit_workspace).
+  p.first_split = sch.first_split;
+  p.split_s = sch.s;
+  p.split_mode = sch.mode;
+  p.sk_ws = nullptr;
+  p.sk_cnt = nullptr;
+  if (sch.mode == kSplitWorkspace) {
+    const size_t slots = size_t(p.num_tiles - sch.first_split) * cg * NUM_EPI_WARPS;
+    if (!ksplit_workspace(st, slots * sch.s * EPI_SLOT_BYTES, slots, &p.sk_ws, &p.sk_cnt)) {
+      p.first_split = p.num_tiles;  // no workspace (capture, OOM): whole tiles
+      p.split_s = 1;
+      p.split_mode = kSplitNone;
+    }
+  } else if (sch.mode == kSplitReduce) {
     // zero the split tiles' bounding rectangle of C (tiles inside it that are not split are
     // stored over later in the same launch)
     int mlo = INT32_MAX, mhi = -1, nlo = INT32_MAX, nhi = -1;
@@ -786,6 +972,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
       nlo = std::min(nlo, nb);
       nhi = std::max(nhi, nb);
     }
+    const int tile_m = BM * cg;
     const int64_t r0 = int64_t(mlo) * tile_m;
     const int64_t r1 = std::min<int64_t>(M, int64_t(mhi + 1) * tile_m);
     const int64_t c0 = int64_t(nlo) * BN, c1 = std::min<int64_t>(N, int64_t(nhi + 1) * BN);
@@ -793,6 +980,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
                                       size_t(c1 - c0) * 4, size_t(r1 - r0), st);
     if (e != cudaSuccess) return e;
   }
+  p.num_units = p.first_split + (p.num_tiles - p.first_split) * p.split_s;
   static const bool wave_env = [] {  // producers' per-wave barrier; $GIGA_WAVE_SYNC=0 disables
     const char *e = getenv("GIGA_WAVE_SYNC");
     return !(e && *e == '0');

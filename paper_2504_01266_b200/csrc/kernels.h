@@ -53,6 +53,30 @@ constexpr int kDotMaxBlocks = 2048;
 cudaError_t launch_dot(const float *x, const float *y, int64_t n, double *partials,
                        unsigned *ticket, double *out, cudaStream_t st);
 
+// K-split plan of a launch (gemm_3xtf32.cu): tiles [0, first_split) run whole, the rest as s
+// k-parts each, combined deterministically: kSplitReduce = two halves TMA reduce-add into a
+// zeroed C (plain-store launches), kSplitWorkspace = partials summed in part order by the
+// last part to finish.
+enum { kSplitNone = 0, kSplitReduce = 1, kSplitWorkspace = 2 };
+struct KSplitPlan {
+  int first_split, s, mode;
+};
+KSplitPlan plan_ksplit(int num_tiles, int nclu, int n_kb, int cg, bool plain, int p_kb);
+// The launch's tiling and unit schedule for an M x N x K product on num_sms SMs (cta_group 0:
+// chosen from the shape; plain: C = A*B stored, no accumulate / load_c / peers; p_kb: the
+// promotion interval in k-blocks), as launch_gemm_3xtf32 computes it.
+struct GemmSchedule {
+  int cg, m_tiles, n_tiles, num_tiles, nclu, n_kb, first_split, s, mode, num_units;
+};
+GemmSchedule gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int cta_group,
+                           bool plain, int p_kb);
+// Workspace of the K-split partials for launches on `st` (current device); false when it
+// cannot be had (stream capture, out of memory): the launch then runs whole tiles.
+bool ksplit_workspace(cudaStream_t st, size_t ws_bytes, size_t cnt_n, float **ws,
+                      unsigned **cnt);
+// Frees the K-split workspaces of every device (giga_finalize).
+void release_gemm_caches();
+
 // Resolves cuTensorMapEncodeTiled through the runtime (no libcuda link). 0 on success.
 int ensure_tma_encoder();
 

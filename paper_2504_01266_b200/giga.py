@@ -27,7 +27,7 @@ EXPORTS = (
     "giga_matmul_rank", "giga_split_lo", "giga_gemm_3xtf32", "giga_gemm_3xtf32_ex",
     "giga_timing_enable", "giga_timing_reset", "giga_timing_read", "giga_pipeline_plan",
     "giga_plan_block", "giga_dot", "giga_l2norm", "giga_dot_rank", "giga_init_devices",
-    "giga_rank_p2p_export", "giga_rank_p2p_import", "giga_host_plan",
+    "giga_rank_p2p_export", "giga_rank_p2p_import", "giga_host_plan", "giga_gemm_schedule",
 )
 P2P_BLOB_BYTES = 256
 
@@ -82,6 +82,7 @@ def _load():
         "giga_host_plan": ([i64, i64, i64, i32, P64, ctypes.POINTER(ctypes.c_int), P64,
                             ctypes.POINTER(ctypes.c_int), P64,
                             ctypes.POINTER(ctypes.c_double)], i32),
+        "giga_gemm_schedule": ([i64, i64, i64, i32, P64], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -233,6 +234,14 @@ def plan_block(M: int, world: int, rchunks: int, owner: int, q: int):
     r0, rows = ctypes.c_int64(), ctypes.c_int64()
     _check(lib.giga_plan_block(M, world, rchunks, owner, q, ctypes.byref(r0), ctypes.byref(rows)))
     return r0.value, rows.value
+
+
+def gemm_schedule(M: int, N: int, K: int, num_sms: int = 148) -> dict:
+    """The tiling and k-split unit schedule of one GEMM launch (see include/giga.h)."""
+    out = (ctypes.c_int64 * 8)()
+    _check(lib.giga_gemm_schedule(M, N, K, num_sms, out))
+    keys = ("cta_group", "tiles", "clusters", "n_kb", "first_split", "s", "units", "mode")
+    return dict(zip(keys, list(out)))
 
 
 def host_plan(M: int, N: int, K: int, num_sms: int = 148):

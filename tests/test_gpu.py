@@ -635,12 +635,13 @@ def test_concurrent_calls_from_threads_serialise(giga, torch_cuda):
 
 @pytest.mark.parametrize("dist", ["d2", "d3"])
 def test_tail_split_exact_deterministic(giga, torch_cuda, monkeypatch, dist):
-    """2304 x 2304 (81 tiles of 256 x 256 on 74 CTA pairs: the last 7 tiles run as two half-K
-    units that reduce-add into a zeroed C). Within the bound / bit-exact on integers, the same
-    bits on every launch, and the same value set as with the split disabled in a child."""
+    """2304 x 2304 x 1040 (81 tiles of 256 x 256 on 74 CTA pairs: the last 7 tiles run as
+    k-parts whose partials the last-finishing part adds in part order). Within the bound /
+    bit-exact on integers and the same bits on every launch."""
     torch = torch_cuda
     M = N = 2304
     K = 1040
+    assert giga.gemm_schedule(M, N, K)["s"] > 1
     A = synth.gen_matrix(M, K, synth.MATRIX_A, dist)
     B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
     dA, dB = _dev(torch, A), _dev(torch, B)
@@ -656,3 +657,112 @@ def test_tail_split_exact_deterministic(giga, torch_cuda, monkeypatch, dist):
     C = outs[0].cpu().numpy()
     ok, st = check_exact(C, Cref) if dist == "d3" else check_close(C, Cref, S)
     assert ok, st
+
+
+# shapes whose schedule splits: 512^3 (8 tiles, CG=1: halves onto a zeroed C), 24 and 48
+# tiles on 148 SMs and a single tile (parts through the workspace, ragged M / N / K tails)
+KSPLIT_SHAPES = [(512, 512, 512), (512, 1536, 2048), (1000, 1284, 3000), (96, 200, 4000)]
+
+
+@pytest.mark.parametrize("M,N,K", KSPLIT_SHAPES)
+@pytest.mark.parametrize("dist", ["d1", "d3"])
+def test_ksplit_parity_and_determinism(giga, torch_cuda, M, N, K, dist):
+    """K-split units (deterministic stream-K): every split tile is the ordered sum of its
+    parts. Bit-exact on integers, within 1e-5 sum|A||B| on all-positive data (the worst case
+    for the accumulation), identical bits over repeated launches, no NaN sentinel left."""
+    torch = torch_cuda
+    sch = giga.gemm_schedule(M, N, K)
+    assert sch["s"] > 1, sch
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, dist)
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
+    dA, dB = _dev(torch, A), _dev(torch, B)
+    outs = []
+    for _ in range(3):
+        dC = torch.full((M, N), float("nan"), device="cuda")
+        giga.gemm_3xtf32(dA, None, dB, None, dC, M, N, K)
+        outs.append(dC)
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int32), outs[0].view(torch.int32))
+    Cref, S = oracle.gemm(A, B)
+    C = outs[0].cpu().numpy()
+    ok, st = check_exact(C, Cref) if dist == "d3" else check_close(C, Cref, S)
+    assert ok, st
+
+
+def test_ksplit_forced_part_counts(giga, torch_cuda, tmp_path):
+    """$GIGA_KSPLIT_S forces the number of parts (read once per process: child processes):
+    2 (halves onto a zeroed C) and 3 .. 32 (workspace partials) parts give results within
+    the bound, bit-exact on integers, and on integer data the bits of the whole-tile
+    launch."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    M, N, K = 512, 1536, 2048  # 24 tiles of 128 x 256 (CG = 1) on 148 SMs
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+import synth
+from paper_2504_01266_b200 import giga
+M, N, K = 512, 1536, 2048
+out = []
+for dist in ("d2", "d3"):
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, dist); B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    C = torch.full((M, N), float("nan"), device="cuda")
+    giga.gemm_3xtf32(dA, None, dB, None, C, M, N, K)
+    out.append(C.cpu().numpy())
+print(giga.gemm_schedule(M, N, K)["s"])
+np.save(sys.argv[1], np.stack(out))
+'''
+    res = {}
+    for s in ("0", "2", "3", "7", "16", "32"):
+        f = str(tmp_path / f"c_{s}.npy")
+        env = dict(os.environ)
+        if s == "0":
+            env["GIGA_TAIL_SPLIT"] = "0"
+        else:
+            env["GIGA_KSPLIT_S"] = s
+        r = subprocess.run([sys.executable, "-c", code, f], cwd=root, env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        got_s = int(r.stdout.split()[-1])
+        assert got_s == (1 if s == "0" else int(s)), (s, got_s)
+        res[s] = np.load(f)
+    for dist, i in (("d2", 0), ("d3", 1)):
+        A = synth.gen_matrix(M, K, synth.MATRIX_A, dist)
+        B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
+        Cref, S = oracle.gemm(A, B)
+        for s, v in res.items():
+            ok, st = check_exact(v[i], Cref) if dist == "d3" else check_close(v[i], Cref, S)
+            assert ok, (s, st)
+    for s, v in res.items():
+        assert np.array_equal(v[1], res["0"][1]), s
+
+
+def test_ksplit_concurrent_streams(giga, torch_cuda):
+    """Launches on different streams of one device get their own k-split workspaces: two
+    streams running split GEMMs at the same time give the bits each gives alone."""
+    torch = torch_cuda
+    M, N, K = 1000, 1284, 3000
+    assert giga.gemm_schedule(M, N, K)["mode"] == 2
+    ins = []
+    for seed_dist in ("d2", "d1"):
+        A = synth.gen_matrix(M, K, synth.MATRIX_A, seed_dist)
+        B = synth.gen_matrix(K, N, synth.MATRIX_B, seed_dist)
+        ins.append((_dev(torch, A), _dev(torch, B)))
+    ref = []
+    for dA, dB in ins:
+        C = torch.empty((M, N), device="cuda")
+        giga.gemm_3xtf32(dA, None, dB, None, C, M, N, K)
+        ref.append(C)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [[torch.full((M, N), float("nan"), device="cuda") for _ in range(4)] for _ in ins]
+    for r in range(4):
+        for i, ((dA, dB), st) in enumerate(zip(ins, streams)):
+            giga.gemm_3xtf32(dA, None, dB, None, outs[i][r], M, N, K, stream=st)
+    torch.cuda.synchronize()
+    for i in range(2):
+        for o in outs[i]:
+            assert torch.equal(o.view(torch.int32), ref[i].view(torch.int32))
