@@ -252,6 +252,18 @@ int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const
                         float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, int terms,
                         int promote_kblocks, int cta_group, void *stream);
 
+/* Measurement tool for the N > 1 pipeline on a single GPU: enqueues on `stream` (current
+ * device) exactly the GEMM launches rank `rank` of `world` issues in giga_matmul_rank /
+ * giga_matmul_sharded over NCCL -- the K-chunks of giga_pipeline_plan accumulating into the
+ * rank's rows of C_full, the last K-chunk in its row chunks, on all SMs but $GIGA_COMM_SMS --
+ * with no communication: B is read as if it had arrived. world = 1 is the single-GPU GEMM.
+ * Timing it bounds the per-GPU compute time of the N-GPU step from below
+ * (scripts/project_scaling.py). A_shard: the rank's giga_partition rows x K; B: K x N; C_full: M x N (the
+ * rank's rows are written). K % 4 == N % 4 == 0, 16-byte aligned pointers. Does not need
+ * giga_init. Errors: INVALID_ARG, UNSUPPORTED (GIGA_LO_PRESPLIT=1), CUDA. */
+int giga_rank_compute_only(const float *A_shard, const float *B, float *C_full, int64_t M,
+                           int64_t N, int64_t K, int world, int rank, void *stream);
+
 /* The work schedule of one giga_gemm_3xtf32 launch (C stored, default promotion interval)
  * over an M x N x K product on `num_sms` SMs (<= 0: 148), computed on the host exactly as
  * the launch computes it (no GPU needed). out must hold 8 values:

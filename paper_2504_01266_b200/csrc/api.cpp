@@ -667,6 +667,38 @@ int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const
   return GIGA_OK;
 }
 
+int giga_rank_compute_only(const float *A_shard, const float *B, float *C_full, int64_t M,
+                           int64_t N, int64_t K, int world, int rank, void *stream) {
+  if (!A_shard || !B || !C_full)
+    return fail(GIGA_ERR_INVALID_ARG, "giga_rank_compute_only: NULL pointer");
+  TRY(check_dims(M, N, K));
+  if (world < 1 || world > 4096 || rank < 0 || rank >= world)
+    return fail(GIGA_ERR_INVALID_ARG, "giga_rank_compute_only: rank %d of world %d", rank, world);
+  if ((K & 3) || (N & 3) || !aligned16(A_shard) || !aligned16(B) || !aligned16(C_full))
+    return fail(GIGA_ERR_INVALID_ARG,
+                "giga_rank_compute_only: needs K %% 4 == N %% 4 == 0 and 16-byte aligned pointers");
+  if (lo_presplit())
+    return fail(GIGA_ERR_UNSUPPORTED, "giga_rank_compute_only: not with GIGA_LO_PRESPLIT=1");
+  if (ensure_tma_encoder() != 0) return fail(GIGA_ERR_CUDA, "TMA encoder unavailable");
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const Plan plan = make_plan(M, K, world, true);
+  GemmExtra ex;
+  ex.lda = K;
+  ex.ldb = N;
+  ex.max_ctas = world > 1 ? pipeline_max_ctas(dev) : 0;
+  auto none = [](int) { return int(GIGA_OK); };
+  if (world == 1) {  // the single-GPU path: one whole GEMM on all SMs
+    CK(timed(0, static_cast<cudaStream_t>(stream), [&] {
+      return launch_gemm_3xtf32(A_shard, nullptr, B, nullptr, C_full, M, N, K, N, 3, -1,
+                                static_cast<cudaStream_t>(stream));
+    }));
+    return GIGA_OK;
+  }
+  return rank_gemms(plan, ex, M, N, K, world, rank, A_shard, nullptr, B, nullptr, C_full,
+                    static_cast<cudaStream_t>(stream), none, none);
+}
+
 int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *out) {
   if (!out) return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_schedule: NULL out");
   TRY(check_dims(M, N, K));

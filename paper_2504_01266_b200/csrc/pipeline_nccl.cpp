@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <functional>
 
 namespace giga {
 
@@ -81,6 +82,50 @@ int gather_rows(const NcclApi *api, ncclComm_t comm, cudaStream_t st, float *C_f
   return GIGA_OK;
 }
 
+// The GEMM launches of rank `rank` in the pipeline (compute stream `st`): K-chunk c accumulates
+// into the rank's rows of C_full (c > 0: C += A_c B_c); the last K-chunk runs in the plan's row
+// chunks. before_chunk(c) runs before chunk c's GEMM is enqueued (wait for B chunk c); after(q)
+// after row chunk q's GEMM (q = -1: after an earlier, whole K-chunk).
+int rank_gemms(const Plan &plan, const GemmExtra &ex, int64_t M, int64_t N, int64_t K, int world,
+               int rank, const float *A, const float *Alo, const float *B, const float *Blo,
+               float *C_full, cudaStream_t st, const std::function<int(int)> &before_chunk,
+               const std::function<int(int)> &after) {
+  int64_t r0, rows;
+  partition_rows(M, world, rank, &r0, &rows);
+  float *Cs = C_full + r0 * N;
+  const int64_t *kb = plan.kb;
+  for (int c = 0; c < plan.pb; ++c) {
+    const int64_t Kc = kb[c + 1] - kb[c];
+    TRY(before_chunk(c));
+    GemmExtra e = ex;
+    e.accumulate = c > 0;
+    const float *Bc = B + kb[c] * N, *Bloc = at(Blo, kb[c] * N);
+    if (c < plan.pb - 1) {
+      if (rows > 0)
+        TRY(gemm_chunk(A + kb[c], at(Alo, kb[c]), Bc, Bloc, Cs, rows, N, Kc, e, st));
+      TRY(after(-1));
+      continue;
+    }
+    for (int q = 0; q < plan.pc; ++q) {
+      int64_t b0, brows;
+      plan_block(M, world, plan.pc, rank, q, &b0, &brows);
+      const int64_t q0 = b0 - r0;  // offset inside this rank's shard
+      if (brows > 0)
+        TRY(gemm_chunk(A + q0 * K + kb[c], at(Alo, q0 * K + kb[c]), Bc, Bloc, Cs + q0 * N, brows,
+                       N, Kc, e, st));
+      TRY(after(q));
+    }
+  }
+  return GIGA_OK;
+}
+
+// The SMs the pipeline's GEMMs may use: all but $GIGA_COMM_SMS (8), left to NCCL's kernels.
+int pipeline_max_ctas(int dev) {
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return std::max(2, nsm - std::max(0, env_int("GIGA_COMM_SMS", 8)));
+}
+
 // ---------------------------------------------------------------------------------------
 // The multi-GPU pipeline (SURVEY.md 8(a) a3-a7 with 8(e) overlap). Per participant (one per
 // GPU in single-process mode; this process's GPU in rank mode):
@@ -109,11 +154,7 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
   GemmExtra ex;
   ex.lda = K;
   ex.ldb = N;
-  {
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, parts[0].d->dev);
-    ex.max_ctas = std::max(2, nsm - std::max(0, env_int("GIGA_COMM_SMS", 8)));
-  }
+  ex.max_ctas = pipeline_max_ctas(parts[0].d->dev);
 
   std::vector<Trace> tr;  // $GIGA_TRACE=1: per-GPU timeline of the pipeline
   for (auto &p : parts) {
@@ -170,30 +211,18 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
     }
     const float *Alo = lo_at(p.d->A_lo);
     float *Blo = lo_at(p.d->B_lo);
-    for (int c = 0; c < pb; ++c) {
-      const int64_t Kc = kb[c + 1] - kb[c];
-      CK(cudaStreamWaitEvent(p.st, p.d->ev_kchunk[c], 0));
-      TRY(split(p.B + kb[c] * N, at(Blo, kb[c] * N), Kc * N, p.st));
-      GemmExtra e = ex;
-      e.accumulate = c > 0;
-      const float *Bc = p.B + kb[c] * N, *Bloc = at(Blo, kb[c] * N);
-      if (c < pb - 1) {
-        if (rows > 0)
-          TRY(gemm_chunk(p.A + kb[c], at(Alo, kb[c]), Bc, Bloc, Cs, rows, N, Kc, e, p.st));
-        TRY(tr[&p - &parts[0]].mark("gemm", p.st));
-        continue;
-      }
-      for (int q = 0; q < pc; ++q) {
-        int64_t b0, brows;
-        plan_block(M, world, pc, p.rank, q, &b0, &brows);
-        const int64_t q0 = b0 - r0;  // offset inside this rank's shard
-        if (brows > 0)
-          TRY(gemm_chunk(p.A + q0 * K + kb[c], at(Alo, q0 * K + kb[c]), Bc, Bloc, Cs + q0 * N,
-                         brows, N, Kc, e, p.st));
-        CK(cudaEventRecord(p.d->ev_rchunk[q], p.st));
-        TRY(tr[&p - &parts[0]].mark("gemm_rows", p.st));
-      }
-    }
+    Trace &t = tr[&p - &parts[0]];
+    TRY(rank_gemms(plan, ex, M, N, K, world, p.rank, p.A, Alo, p.B, Blo, p.C, p.st,
+                   [&](int c) -> int {
+                     CK(cudaStreamWaitEvent(p.st, p.d->ev_kchunk[c], 0));
+                     return split(p.B + kb[c] * N, at(Blo, kb[c] * N), (kb[c + 1] - kb[c]) * N,
+                                  p.st);
+                   },
+                   [&](int q) -> int {
+                     if (q < 0) return t.mark("gemm", p.st);
+                     CK(cudaEventRecord(p.d->ev_rchunk[q], p.st));
+                     return t.mark("gemm_rows", p.st);
+                   }));
   }
   // 3. gather C row chunk by row chunk: one broadcast per owner, grouped
   for (int q = 0; q < pc; ++q) {

@@ -15,6 +15,7 @@
 #include <mutex>
 #include <string>
 #include <utility>
+#include <functional>
 #include <vector>
 
 #include "kernels.h"
@@ -242,6 +243,11 @@ int get_comms(int ngpus, std::vector<ncclComm_t> **out);
 int gather_rows(const NcclApi *api, ncclComm_t comm, cudaStream_t st, float *C_full, int64_t M,
                 int64_t N, int world, int rank);
 int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int64_t K);
+int rank_gemms(const Plan &plan, const GemmExtra &ex, int64_t M, int64_t N, int64_t K, int world,
+               int rank, const float *A, const float *Alo, const float *B, const float *Blo,
+               float *C_full, cudaStream_t st, const std::function<int(int)> &before_chunk,
+               const std::function<int(int)> &after);
+int pipeline_max_ctas(int dev);
 
 // ---- p2p.cpp -------------------------------------------------------------------------------
 bool transport_p2p();

@@ -28,6 +28,7 @@ EXPORTS = (
     "giga_timing_enable", "giga_timing_reset", "giga_timing_read", "giga_pipeline_plan",
     "giga_plan_block", "giga_dot", "giga_l2norm", "giga_dot_rank", "giga_init_devices",
     "giga_rank_p2p_export", "giga_rank_p2p_import", "giga_host_plan", "giga_gemm_schedule",
+    "giga_rank_compute_only",
 )
 P2P_BLOB_BYTES = 256
 
@@ -83,6 +84,7 @@ def _load():
                             ctypes.POINTER(ctypes.c_int), P64,
                             ctypes.POINTER(ctypes.c_double)], i32),
         "giga_gemm_schedule": ([i64, i64, i64, i32, P64], i32),
+        "giga_rank_compute_only": ([p, p, p, i64, i64, i64, i32, i32, p], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -234,6 +236,13 @@ def plan_block(M: int, world: int, rchunks: int, owner: int, q: int):
     r0, rows = ctypes.c_int64(), ctypes.c_int64()
     _check(lib.giga_plan_block(M, world, rchunks, owner, q, ctypes.byref(r0), ctypes.byref(rows)))
     return r0.value, rows.value
+
+
+def rank_compute_only(A_shard, B, C_full, M: int, N: int, K: int, world: int, rank: int,
+                      stream=None):
+    """Rank `rank`'s GEMM launches of the world-`world` pipeline, without communication."""
+    _check(lib.giga_rank_compute_only(_ptr(A_shard), _ptr(B), _ptr(C_full), M, N, K, world,
+                                      rank, _stream(stream)))
 
 
 def gemm_schedule(M: int, N: int, K: int, num_sms: int = 148) -> dict:

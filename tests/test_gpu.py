@@ -766,3 +766,28 @@ def test_ksplit_concurrent_streams(giga, torch_cuda):
     for i in range(2):
         for o in outs[i]:
             assert torch.equal(o.view(torch.int32), ref[i].view(torch.int32))
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("dist", ["d2", "d3"])
+def test_rank_compute_only_is_the_pipeline_arithmetic(giga, torch_cuda, world, dist):
+    """giga_rank_compute_only (the single-GPU stand-in for a rank's GEMMs, timed by
+    scripts/project_scaling.py) computes every rank's rows of C: K-chunks accumulating, the
+    last chunk in row chunks. All ranks together give C within the bound, bit-exact on
+    integers, with no NaN sentinel left."""
+    torch = torch_cuda
+    M, N, K = 1000, 516, 2056
+    kb, rc = giga.pipeline_plan(M, N, K, world)
+    assert len(kb) > 2 and rc > 1  # several K-chunks and row chunks are exercised
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, dist)
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
+    dB = _dev(torch, B)
+    dC = torch.full((M, N), float("nan"), device="cuda")
+    for r in range(world):
+        r0, rows = giga.partition(M, world, r)
+        giga.rank_compute_only(_dev(torch, A[r0:r0 + rows]), dB, dC, M, N, K, world, r)
+    torch.cuda.synchronize()
+    Cref, S = oracle.gemm(A, B)
+    C = dC.cpu().numpy()
+    ok, st = check_exact(C, Cref) if dist == "d3" else check_close(C, Cref, S)
+    assert ok, st
