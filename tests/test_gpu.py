@@ -783,9 +783,11 @@ def test_rank_compute_only_is_the_pipeline_arithmetic(giga, torch_cuda, world, d
     B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
     dB = _dev(torch, B)
     dC = torch.full((M, N), float("nan"), device="cuda")
+    shards = []  # kept alive until the asynchronous launches have read them
     for r in range(world):
         r0, rows = giga.partition(M, world, r)
-        giga.rank_compute_only(_dev(torch, A[r0:r0 + rows]), dB, dC, M, N, K, world, r)
+        shards.append(_dev(torch, A[r0:r0 + rows]))
+        giga.rank_compute_only(shards[-1], dB, dC, M, N, K, world, r)
     torch.cuda.synchronize()
     Cref, S = oracle.gemm(A, B)
     C = dC.cpu().numpy()
