@@ -185,8 +185,10 @@ int giga_dot_rank(const float *x_shard, const float *y_shard, int64_t n, double 
  * needs room for 17 entries), growing geometrically so the GEMM starts after a small first
  * chunk; the shard GEMM accumulates chunk by chunk, and the C row blocks are gathered in
  * *rchunks rounds; in round q owner o broadcasts the rows returned by
- * giga_plan_block(M, world, rchunks, o, q) (largest first). Knobs: $GIGA_BCAST_CHUNKS
- * (default 6 with NCCL, 16 with $GIGA_TRANSPORT=p2p), $GIGA_GATHER_CHUNKS (default 4).
+ * giga_plan_block(M, world, rchunks, o, q) (largest first). The counts (at most 6 K-chunks
+ * with NCCL, 16 with $GIGA_TRANSPORT=p2p; at most 4 row chunks) minimise a model of the
+ * exposed first transfer and last gather plus ~20 us per extra GEMM launch ($GIGA_LAUNCH_US);
+ * $GIGA_BCAST_CHUNKS and $GIGA_GATHER_CHUNKS force them.
  * Errors: INVALID_ARG. */
 int giga_pipeline_plan(int64_t M, int64_t N, int64_t K, int world, int *kchunks,
                        int64_t *kbounds, int *rchunks);

@@ -606,7 +606,7 @@ int giga_pipeline_plan(int64_t M, int64_t N, int64_t K, int world, int *kchunks,
                        int64_t *kbounds, int *rchunks) {
   if (M < 1 || N < 1 || K < 1 || world < 1 || !kchunks || !kbounds || !rchunks)
     return fail(GIGA_ERR_INVALID_ARG, "giga_pipeline_plan: bad arguments");
-  const Plan pl = make_plan(M, K, world, (K % 4 == 0) && (N % 4 == 0));
+  const Plan pl = make_plan(M, N, K, world, (K % 4 == 0) && (N % 4 == 0));
   *kchunks = pl.pb;
   *rchunks = pl.pc;
   for (int c = 0; c <= pl.pb; ++c) kbounds[c] = pl.kb[c];
@@ -682,7 +682,7 @@ int giga_rank_compute_only(const float *A_shard, const float *B, float *C_full, 
   if (ensure_tma_encoder() != 0) return fail(GIGA_ERR_CUDA, "TMA encoder unavailable");
   int dev = 0;
   CK(cudaGetDevice(&dev));
-  const Plan plan = make_plan(M, K, world, true);
+  const Plan plan = make_plan(M, N, K, world, true);
   GemmExtra ex;
   ex.lda = K;
   ex.ldb = N;

@@ -58,7 +58,7 @@ int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K, bool gath
               aligned16(gather ? p.C : p.C_rows);
   if (!aligned)
     return fail(GIGA_ERR_UNSUPPORTED, "p2p transport needs K %% 4 == N %% 4 == 0, aligned");
-  const Plan plan = make_plan(M, K, world, true);
+  const Plan plan = make_plan(M, N, K, world, true);
   // 0. join the callers' streams, workspace, split A
   for (auto &p : parts) {
     CK(cudaSetDevice(p.d->dev));
@@ -193,7 +193,7 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
   if ((K % 4) || (N % 4) || !aligned16(A) || !aligned16(B) || !aligned16(C))
     return fail(GIGA_ERR_UNSUPPORTED, "p2p transport needs K %% 4 == N %% 4 == 0, aligned");
   const uint32_t s = ++x.step;
-  const Plan plan = make_plan(M, K, world, true);
+  const Plan plan = make_plan(M, N, K, world, true);
   int64_t r0, rows;
   partition_rows(M, world, r, &r0, &rows);
   Trace tr(d, "p2p_rank");  // $GIGA_TRACE=1: this rank's timeline

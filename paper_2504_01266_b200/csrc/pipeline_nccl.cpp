@@ -148,7 +148,7 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
   if (!api) return fail(GIGA_ERR_COMM, "NCCL unavailable: %s", why ? why : "?");
   bool aligned = (K % 4 == 0) && (N % 4 == 0);
   for (auto &p : parts) aligned = aligned && aligned16(p.A) && aligned16(p.B) && aligned16(p.C);
-  const Plan plan = make_plan(M, K, world, aligned);
+  const Plan plan = make_plan(M, N, K, world, aligned);
   const int pb = plan.pb, pc = plan.pc;
   const int64_t *kb = plan.kb;
   GemmExtra ex;

@@ -335,9 +335,18 @@ static bool geometric_bounds(int64_t total, int n, double ratio, int64_t align,
 // chunk has landed, and each later chunk's transfer hides behind the previous chunk's GEMM as
 // long as the growth r stays below (GEMM time per K-row) / (transfer time per K-row)
 // = (2 rows_max / R) / (4 / BW) = rows_max BW / (2 R), R ~ 255 TFLOP/s, BW ~ 600 GB/s (NCCL
-// broadcast) or 770 GB/s (a copy-engine hop). r = 0.8 of that, at most 4, lowered until every
-// chunk is >= 256 deep. E.g. 32768^3 on 8 GPUs (NCCL): 555, 1094, 2155, 4245, 8364, 16479.
-Plan make_plan(int64_t M, int64_t K, int world, bool aligned) {
+// broadcast) or 770 GB/s (a copy-engine hop); r = 0.8 of that, at most 4, lowered until every
+// chunk is >= 256 deep. The number of chunks pb (<= 6 with NCCL, <= 16 with p2p) minimises
+//   startup + pb O,  startup = hops x (first chunk's transfer), hops = 1 (NCCL pipelines its
+//   broadcast) or world - 1 (the p2p chain forwards whole chunks),
+// O ~ 20 us per extra GEMM launch (launch gap and the partial last wave; measured with
+// scripts/project_scaling.py: a 2048 x 4096^2 shard in 6 + 3 launches took 0.45 ms against
+// 0.24 ms of work). The row chunks pc (<= 4) of the last K-chunk minimise the end of the last
+// gather in a simulation of the two streams (GEMM of row chunk q, then its gather after the
+// previous gather): big shards keep 4 chunks, small ones (c2 on 2 GPUs) take fewer launches.
+// $GIGA_BCAST_CHUNKS / $GIGA_GATHER_CHUNKS force the counts; $GIGA_LAUNCH_US sets O.
+// E.g. 32768^3 on 8 GPUs (NCCL): 6 chunks, 4 row chunks; 4096^3 on 2 GPUs: 3 and 2.
+Plan make_plan(int64_t M, int64_t N, int64_t K, int world, bool aligned) {
   Plan pl;
   int64_t rows_max = 0;
   for (int r = 0; r < world; ++r) {
@@ -348,20 +357,51 @@ Plan make_plan(int64_t M, int64_t K, int world, bool aligned) {
   pl.kb[0] = 0;
   pl.kb[1] = K;
   if (!aligned) return pl;
-  // NCCL pipelines a broadcast internally; the p2p chain forwards whole chunks GPU to GPU, so
-  // the last of g GPUs waits (g - 1) hops of the first chunks: more, smaller chunks there.
   const bool p2p = transport_p2p();
-  pl.pb = std::min(std::max(env_int("GIGA_BCAST_CHUNKS", p2p ? kMaxChunks : 6), 1), kMaxChunks);
-  pl.pb = int(std::min<int64_t>(pl.pb, std::max<int64_t>(1, K / 256)));
   const double bw = p2p ? 770e9 : 600e9, R = 255e12;
-  double r = std::min(4.0, std::max(1.0, 0.8 * double(rows_max) * bw / (2.0 * R)));
-  while (r > 1.0 && !geometric_bounds(K, pl.pb, r, 16, 256, pl.kb)) r = std::max(1.0, r * 0.9);
-  if (r <= 1.0 && !geometric_bounds(K, pl.pb, 1.0, 16, 256, pl.kb)) {
-    for (int c = 0; c < pl.pb; ++c) pl.kb[c] = (K * c / pl.pb) / 16 * 16;
-    pl.kb[pl.pb] = K;
+  const double O = std::max(0, env_int("GIGA_LAUNCH_US", 20)) * 1e-6;
+  const double r_max = std::min(4.0, std::max(1.0, 0.8 * double(rows_max) * bw / (2.0 * R)));
+  const int hops = p2p ? std::max(1, world - 1) : 1;
+  const int pb_env = env_int("GIGA_BCAST_CHUNKS", 0);
+  const int pb_cap = int(std::min<int64_t>(
+      pb_env > 0 ? std::min(pb_env, kMaxChunks) : (p2p ? kMaxChunks : 6),
+      std::max<int64_t>(1, K / 256)));
+  double best = 1e300;
+  for (int pb = pb_env > 0 ? pb_cap : 1; pb <= pb_cap; ++pb) {
+    int64_t b[kMaxChunks + 1];
+    double r = r_max;
+    while (r > 1.0 && !geometric_bounds(K, pb, r, 16, 256, b)) r = std::max(1.0, r * 0.9);
+    if (r <= 1.0 && !geometric_bounds(K, pb, 1.0, 16, 256, b)) {
+      for (int c = 0; c < pb; ++c) b[c] = (K * c / pb) / 16 * 16;
+      b[pb] = K;
+    }
+    const double cost = hops * 4.0 * double(b[1]) * double(N) / bw + O * pb;
+    if (cost < best) {
+      best = cost;
+      pl.pb = pb;
+      for (int c = 0; c <= pb; ++c) pl.kb[c] = b[c];
+    }
   }
-  pl.pc = std::min(std::max(env_int("GIGA_GATHER_CHUNKS", 4), 1), kMaxChunks);
-  pl.pc = int(std::min<int64_t>(pl.pc, std::max<int64_t>(1, rows_max / 256)));
+  const int64_t Kc = K - pl.kb[pl.pb - 1];
+  const int pc_env = env_int("GIGA_GATHER_CHUNKS", 0);
+  const int pc_cap = int(std::min<int64_t>(pc_env > 0 ? std::min(pc_env, kMaxChunks) : 4,
+                                           std::max<int64_t>(1, rows_max / 256)));
+  best = 1e300;
+  for (int pc = pc_env > 0 ? pc_cap : 1; pc <= pc_cap; ++pc) {
+    int64_t b[kMaxChunks + 1];
+    if (!geometric_bounds(rows_max, pc, 0.7, 256, 256, b))
+      for (int i = 0; i <= pc; ++i) b[i] = rows_max * i / pc;
+    double g_end = 0, x_end = 0;  // GEMM stream, gather stream
+    for (int q = 0; q < pc; ++q) {
+      const double rq = double(b[q + 1] - b[q]);
+      g_end += 2.0 * rq * double(N) * double(Kc) / R + O;
+      x_end = std::max(g_end, x_end) + 4.0 * rq * double(N) * double(world - 1) / bw;
+    }
+    if (x_end < best) {
+      best = x_end;
+      pl.pc = pc;
+    }
+  }
   return pl;
 }
 

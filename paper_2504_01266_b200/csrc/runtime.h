@@ -145,8 +145,9 @@ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 // The chunk plan (runtime.cpp make_plan / plan_block): B is distributed in pb K-chunks
 // [kb[c], kb[c+1]) growing geometrically (multiples of 16, at least 256 deep); the last
 // K-chunk's GEMM and the C gather run in pc row chunks per owner, shrinking geometrically.
-// Knobs: $GIGA_BCAST_CHUNKS (6 with NCCL, 16 with p2p), $GIGA_GATHER_CHUNKS (4); unaligned
-// shapes use one chunk of each.
+// The counts (at most 6 / 16 K-chunks with NCCL / p2p, 4 row chunks) trade the exposed first
+// transfer and last gather against ~20 us per extra GEMM launch; $GIGA_BCAST_CHUNKS and
+// $GIGA_GATHER_CHUNKS force them. Unaligned shapes use one chunk of each.
 struct Plan {
   int pb = 1, pc = 1;
   int64_t kb[kMaxChunks + 1] = {0};
@@ -233,7 +234,7 @@ int dot_partial(DevCtx &d, const float *x, const float *y, int64_t n, cudaStream
 int read_result(DevCtx &d, cudaStream_t st, double *out);  // after dot_partial (+ reduction)
 int env_int(const char *name, int dflt);
 bool force_comm();
-Plan make_plan(int64_t M, int64_t K, int world, bool aligned);
+Plan make_plan(int64_t M, int64_t N, int64_t K, int world, bool aligned);
 void plan_block(int64_t M, int world, int pc, int owner, int q, int64_t *row0, int64_t *rows);
 
 // ---- pipeline_nccl.cpp ---------------------------------------------------------------------
