@@ -244,7 +244,10 @@ int giga_gemm_3xtf32(const float *A, const float *A_lo, const float *B, const fl
                      float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, void *stream);
 
 /* As giga_gemm_3xtf32 with the numerics and tiling knobs exposed (tests and probes):
- * terms = 3 (3xTF32) or 1 (plain TF32: a_hi*b_hi only; A_lo/B_lo ignored);
+ * terms = 3 (3xTF32), 2 (TF32 + BF16: a_hi*b_hi as one TF32 MMA, a_lo*b + a_hi*b_lo as one
+ * K=16 BF16 MMA per k8 step, split error <= 2^-18 |a||b| per product with the default RN hi,
+ * $GIGA_HI_RN=0 truncates (2^-17); A_lo and B_lo must be NULL) or 1 (plain TF32: a_hi*b_hi
+ * only; A_lo/B_lo ignored). The product path uses 3 unless $GIGA_SCHEME=tf32bf16;
  * promote_kblocks = number of 16-wide k-blocks accumulated in TMEM before the partial sum
  * is added into the fp32 register sum; 0 = never promote (one TMEM accumulation over K);
  * -1 = the library default;

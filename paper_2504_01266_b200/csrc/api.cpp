@@ -651,7 +651,8 @@ int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const
                         int promote_kblocks, int cta_group, void *stream) {
   if (cta_group < 0 || cta_group > 2)
     return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_3xtf32_ex: cta_group must be 0, 1 or 2");
-  if (!A || !B || !C || (!A_lo) != (!B_lo) || (terms != 1 && terms != 3))
+  if (!A || !B || !C || (!A_lo) != (!B_lo) || (terms != 1 && terms != 2 && terms != 3) ||
+      (terms == 2 && A_lo))
     return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_3xtf32: bad pointers/terms");
   TRY(check_dims(M, N, K));
   if ((K & 3) || (N & 3) || (ldc & 3) || ldc < N || !aligned16(A) || !aligned16(B) ||
@@ -690,7 +691,8 @@ int giga_rank_compute_only(const float *A_shard, const float *B, float *C_full, 
   auto none = [](int) { return int(GIGA_OK); };
   if (world == 1) {  // the single-GPU path: one whole GEMM on all SMs
     CK(timed(0, static_cast<cudaStream_t>(stream), [&] {
-      return launch_gemm_3xtf32(A_shard, nullptr, B, nullptr, C_full, M, N, K, N, 3, -1,
+      return launch_gemm_3xtf32(A_shard, nullptr, B, nullptr, C_full, M, N, K, N,
+                                product_terms(nullptr), -1,
                                 static_cast<cudaStream_t>(stream));
     }));
     return GIGA_OK;

@@ -45,6 +45,7 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <mutex>
@@ -89,7 +90,7 @@ struct GemmParams {
   int M, N, K, ldc;
   int accumulate; // 1: C += A*B (K-chunked pipelines), 0: C = A*B
   int load_c;     // 1: epilogue adds the block's current C before storing (see GemmExtra)
-  int terms;      // 3 = 3xTF32, 1 = TF32 (hi*hi only)
+  int terms;      // 3 = 3xTF32, 2 = TF32 hi*hi + one BF16 correction MMA, 1 = TF32 hi*hi only
   int p_kb;       // k-blocks per TMEM accumulation interval (>= 1)
   int n_kb;       // k-blocks per tile
   int m_tiles, n_tiles, num_tiles;
@@ -108,6 +109,7 @@ struct GemmParams {
   unsigned *wave_sync;  // non-null: zeroed counter for the producers' per-wave barrier
   int n_cdst;     // C destinations in CMaps (1 + peers when the gather is fused)
   int lo_smem;    // 1: lo tiles computed in smem from the raw tiles; 0: TMA-loaded (A_lo, B_lo)
+  int hi_rn;      // terms == 2: hi = RN tf32(x) written over the raw tile (else hi = trunc)
 };
 
 // C tensor maps: [0] this GPU's C, [1..] the same rows of the peers' C_full buffers.
@@ -142,6 +144,12 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
 // [24,29) M >> 4.
 __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+         (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+// Instruction descriptor, kind::f16 with BF16 A and B (format 1), F32 D; A K-major, B
+// MN-major (the correction tiles of the TF32 + BF16 scheme, below).
+__host__ __device__ constexpr uint32_t make_idesc_bf16(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
          (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
@@ -182,6 +190,111 @@ __host__ __device__ __forceinline__ void unit_coords(int u, const GemmParams &p,
   part = v % p.split_s;
   kb0 = int(int64_t(p.n_kb) * part / p.split_s);
   kb1 = int(int64_t(p.n_kb) * (part + 1) / p.split_s);
+}
+
+// ---- TF32 + BF16 scheme (terms == 2) -------------------------------------------------------
+// x = hi + lo with hi = tf32(x) (RN, written over the raw tile when hi_rn, else the MMA's own
+// truncation) and lo = x - hi exact. a*b = a_hi*b_hi + a_lo*b + a_hi*b_lo exactly; the first
+// product is one kind::tf32 MMA (exact products), the two corrections, each ~2^-11 of a*b,
+// are ONE kind::f16 MMA with K = 16 over bf16 operands concatenated along K:
+//   A' row  = [bf16(a_lo[k0..k7]) | bf16(a_hi[k0..k7])]           (K-major, SW64, 64 B rows)
+//   B' rows = [bf16(b[k0..k7][n]) ; bf16(b_lo[k0..k7][n])]         (MN-major, SW128)
+// bf16 keeps 8 significant bits, so each correction carries <= 2 * 2^-9 of itself:
+// |error| <= 2^-18 |a||b| per product with RN hi (|lo| <= 2^-11 |x|), 2^-17 with truncation,
+// against the 1e-5 = 2^-16.6 bound. A bf16 K16 MMA takes the time of a tf32 K8 MMA, so a
+// k8 step costs 2 MMA times instead of 3xTF32's 3.
+// Layouts written here (stage = [A raw | A' | B raw | B']):
+//   A raw: TMA SW64, 128 rows x 64 B, 16-B chunk c of row r at r*64 + ((c ^ (r>>1 & 3)) << 4).
+//     A' has the same geometry: chunk 2h (2h+1) of row r = bf16 lo (hi) of k8 step h.
+//   B raw: TMA 128B_ATOM_32B, 32-column chunks of 16 k-rows x 128 B; the 32-B granule g of
+//     row k sits at k*128 + ((g ^ (k & 3)) << 5).
+//   B': 64-column chunks of 32 rows x 128 B (k8 step j: rows 16j..16j+7 = bf16(b[k]),
+//     16j+8.. = bf16(b_lo[k])); 16-B chunk c (8 columns) of row q at q*128 + ((c ^ (q&7)) << 4).
+// Thread mapping keeps every 8-lane phase of each 16-B access on distinct bank groups.
+__device__ __forceinline__ float tf32_hi(float x, int rn) {
+  return rn ? ptx::tf32_rna(x) : __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+template <int CG>
+__device__ __forceinline__ void xform_tf32_bf16(uint32_t sA, int xt, int rn) {
+  using namespace cfg;
+  using T = Tile<CG>;
+  constexpr int NT = NUM_XFORM_WARPS * 32;
+  const uint32_t sAx = sA + A_BYTES, sB = sA + 2 * A_BYTES, sBx = sB + T::B_BYTES;
+  // A: units (row r, k8 step h); lanes of a warp take 32 consecutive rows
+  constexpr int UA = 2 * BM / NT;  // 4
+  float4 xa[UA][2];
+#pragma unroll
+  for (int i = 0; i < UA; ++i) {
+    const int u = i * NT + xt, r = u & (BM - 1), h = u / BM;
+    const uint32_t sw = uint32_t(r >> 1) & 3, row = sA + uint32_t(r) * 64;
+    xa[i][0] = ptx::ld_shared_v4(row + ((uint32_t(2 * h) ^ sw) << 4));
+    xa[i][1] = ptx::ld_shared_v4(row + ((uint32_t(2 * h + 1) ^ sw) << 4));
+  }
+  // B: units (k-row k, 8-column granule); 8 consecutive lanes cover 64 columns of one row
+  constexpr int UB = (T::B_COLS / 8) * BK / NT;  // 4 (CG = 2), 8 (CG = 1)
+  float4 xb[UB][2];
+#pragma unroll
+  for (int i = 0; i < UB; ++i) {
+    const int u = i * NT + xt, g8 = u & 7, k = (u >> 3) & (BK - 1), nch = u >> 7;
+    const uint32_t gaddr = sB + uint32_t(2 * nch + (g8 >> 2)) * B_CHUNK_BYTES + uint32_t(k) * 128 +
+                           ((uint32_t(g8 & 3) ^ uint32_t(k & 3)) << 5);
+    // lanes of the second 32-column chunk read their granule's halves in the other order:
+    // the two chunks are 2 KiB apart (same banks)
+    const uint32_t q = uint32_t(g8 >> 2) << 4;
+    const float4 p0 = ptx::ld_shared_v4(gaddr + q), p1 = ptx::ld_shared_v4(gaddr + (q ^ 16));
+    xb[i][0] = q ? p1 : p0;
+    xb[i][1] = q ? p0 : p1;
+  }
+#pragma unroll
+  for (int i = 0; i < UA; ++i) {
+    const int u = i * NT + xt, r = u & (BM - 1), h = u / BM;
+    const uint32_t sw = uint32_t(r >> 1) & 3;
+    const uint32_t o0 = uint32_t(r) * 64 + ((uint32_t(2 * h) ^ sw) << 4);
+    const uint32_t o1 = uint32_t(r) * 64 + ((uint32_t(2 * h + 1) ^ sw) << 4);
+    const float v[8] = {xa[i][0].x, xa[i][0].y, xa[i][0].z, xa[i][0].w,
+                        xa[i][1].x, xa[i][1].y, xa[i][1].z, xa[i][1].w};
+    float hi[8], lo[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      hi[j] = tf32_hi(v[j], rn);
+      lo[j] = __fsub_rn(v[j], hi[j]);
+    }
+    ptx::st_shared_v4_u32(sAx + o0, ptx::pack_bf16x2(lo[0], lo[1]), ptx::pack_bf16x2(lo[2], lo[3]),
+                          ptx::pack_bf16x2(lo[4], lo[5]), ptx::pack_bf16x2(lo[6], lo[7]));
+    ptx::st_shared_v4_u32(sAx + o1, ptx::pack_bf16x2(hi[0], hi[1]), ptx::pack_bf16x2(hi[2], hi[3]),
+                          ptx::pack_bf16x2(hi[4], hi[5]), ptx::pack_bf16x2(hi[6], hi[7]));
+    if (rn) {
+      ptx::st_shared_v4(sA + o0, hi[0], hi[1], hi[2], hi[3]);
+      ptx::st_shared_v4(sA + o1, hi[4], hi[5], hi[6], hi[7]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < UB; ++i) {
+    const int u = i * NT + xt, g8 = u & 7, k = (u >> 3) & (BK - 1), nch = u >> 7;
+    const float v[8] = {xb[i][0].x, xb[i][0].y, xb[i][0].z, xb[i][0].w,
+                        xb[i][1].x, xb[i][1].y, xb[i][1].z, xb[i][1].w};
+    float hi[8], lo[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      hi[j] = tf32_hi(v[j], rn);
+      lo[j] = __fsub_rn(v[j], hi[j]);
+    }
+    const uint32_t kk = uint32_t(k & 7), chunk = (uint32_t(g8) ^ kk) << 4;
+    const uint32_t base = sBx + uint32_t(nch) * 4096 + uint32_t(k >> 3) * 2048;
+    ptx::st_shared_v4_u32(base + kk * 128 + chunk, ptx::pack_bf16x2(v[0], v[1]),
+                          ptx::pack_bf16x2(v[2], v[3]), ptx::pack_bf16x2(v[4], v[5]),
+                          ptx::pack_bf16x2(v[6], v[7]));
+    ptx::st_shared_v4_u32(base + (8 + kk) * 128 + chunk, ptx::pack_bf16x2(lo[0], lo[1]),
+                          ptx::pack_bf16x2(lo[2], lo[3]), ptx::pack_bf16x2(lo[4], lo[5]),
+                          ptx::pack_bf16x2(lo[6], lo[7]));
+    if (rn) {
+      const uint32_t gaddr = sB + uint32_t(2 * nch + (g8 >> 2)) * B_CHUNK_BYTES +
+                             uint32_t(k) * 128 + ((uint32_t(g8 & 3) ^ uint32_t(k & 3)) << 5);
+      ptx::st_shared_v4(gaddr, hi[0], hi[1], hi[2], hi[3]);
+      ptx::st_shared_v4(gaddr + 16, hi[4], hi[5], hi[6], hi[7]);
+    }
+  }
 }
 
 template <int CG>
@@ -314,6 +427,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     // ======================= MMA issuer (leader CTA) =======================
     if (lane == 0 && leader) {
       constexpr uint32_t idesc = make_idesc(BM * CG, BN);
+      constexpr uint32_t idesc2 = make_idesc_bf16(BM * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
@@ -341,7 +455,21 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
               const uint64_t dB = make_sdesc(sB + 1024 * k8, B_CHUNK_BYTES, 512, 1);
               const uint64_t dAlo = make_sdesc(sAlo + 32 * k8, 16, 512, 4);
               const uint64_t dBlo = make_sdesc(sBlo + 1024 * k8, B_CHUNK_BYTES, 512, 1);
-              if (CG == 1) {
+              if (p.terms == 2) {
+                // one K=16 bf16 MMA: [a_lo | a_hi] . [b ; b_lo] = a_lo*b + a_hi*b_lo, then hi*hi
+                // A' K-major SW64 (the lo tile's geometry); B' MN-major SW128: LBO = 4096
+                // between 64-column atoms, SBO = 1024 between 8-row k groups (measured on
+                // B200: the swapped reading gives wrong products)
+                const uint64_t dAx = make_sdesc(sAlo + 32 * k8, 16, 512, 4);
+                const uint64_t dBx = make_sdesc(sBlo + 2048 * k8, 4096, 1024, 2);
+                if (CG == 1) {
+                  ptx::mma_bf16(d_tmem, dAx, dBx, idesc2, acc);
+                  ptx::mma_tf32(d_tmem, dA, dB, idesc, 1u);
+                } else {
+                  ptx::mma_bf16_cg2(d_tmem, dAx, dBx, idesc2, acc);
+                  ptx::mma_tf32_cg2(d_tmem, dA, dB, idesc, 1u);
+                }
+              } else if (CG == 1) {
                 if (p.terms == 3) {
                   ptx::mma_tf32(d_tmem, dAlo, dB, idesc, acc);
                   ptx::mma_tf32(d_tmem, dA, dBlo, idesc, 1u);
@@ -417,6 +545,9 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
                               tf32_lo(vb[i].x), tf32_lo(vb[i].y), tf32_lo(vb[i].z),
                               tf32_lo(vb[i].w));
           ptx::fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
+        } else if (p.terms == 2) {
+          xform_tf32_bf16<CG>(ptx::smem_u32(smem + stage * T::STAGE_BYTES), xt, p.hi_rn);
+          ptx::fence_proxy_async_smem();
         }
         __syncwarp();
         if (lane == 0) {
@@ -626,6 +757,16 @@ int default_promote_kblocks() {
     return kDefaultPromoteKBlocks;
   }();
   return v;
+}
+
+int product_terms(const float *A_lo) {
+  static const int v = [] {
+    const char *e = getenv("GIGA_SCHEME");
+    if (e && strcmp(e, "3xtf32") == 0) return 3;
+    if (e && strcmp(e, "tf32bf16") == 0) return 2;
+    return kDefaultTerms;
+  }();
+  return A_lo ? 3 : v;
 }
 
 // CTA-group size: 2 (CTA pairs) unless the problem has fewer 256-row tiles than SM pairs,
@@ -892,8 +1033,9 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
     return cudaErrorInvalidValue;
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || ldc > INT32_MAX)
     return cudaErrorInvalidValue;
-  if (terms != 1 && terms != 3) return cudaErrorInvalidValue;
+  if (terms != 1 && terms != 2 && terms != 3) return cudaErrorInvalidValue;
   if (terms == 3 && (!A_lo) != (!B_lo)) return cudaErrorInvalidValue;  // both or neither
+  if (terms == 2 && (A_lo || B_lo)) return cudaErrorInvalidValue;     // on chip only
   const bool lo_smem = terms == 3 && !A_lo;
   if (ensure_tma_encoder() != 0) return cudaErrorNotSupported;
 
@@ -930,6 +1072,11 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   if (p.accumulate && p.load_c) return cudaErrorInvalidValue;
   p.terms = terms;
   p.lo_smem = lo_smem ? 1 : 0;
+  static const int hi_rn_env = [] {  // terms == 2: $GIGA_HI_RN=0 keeps the truncated hi
+    const char *e = getenv("GIGA_HI_RN");
+    return (e && *e == '0') ? 0 : 1;
+  }();
+  p.hi_rn = hi_rn_env;
   p.n_kb = int((K + BK - 1) / BK);
   int pk = promote_kblocks < 0 ? default_promote_kblocks() : promote_kblocks;
   p.p_kb = (pk == 0 || pk > p.n_kb) ? p.n_kb : pk;

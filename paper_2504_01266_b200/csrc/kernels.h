@@ -12,6 +12,13 @@ constexpr int kDefaultPromoteKBlocks = 8;
 // The promotion interval in effect (kDefaultPromoteKBlocks or $GIGA_PROMOTE_KBLOCKS).
 int default_promote_kblocks();
 
+// The product path's fp32-accurate scheme: 3 = 3xTF32 (three kind::tf32 MMAs
+// per k8 step), 2 = TF32 + BF16 (hi*hi as kind::tf32, both corrections as one K=16 kind::f16
+// MMA). kDefaultTerms unless $GIGA_SCHEME is "3xtf32" or "tf32bf16". With pre-split lo
+// operands (A_lo != nullptr) the scheme is always 3.
+constexpr int kDefaultTerms = 3;
+int product_terms(const float *A_lo);
+
 // lo = x - tf32(x) over n elements (HBM-bound elementwise split).
 cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t st);
 // The same over a rows x cols block of a row-major matrix with row stride ld (cols, ld % 4 == 0).

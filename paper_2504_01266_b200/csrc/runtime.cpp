@@ -168,7 +168,7 @@ int split(const float *x, float *lo, int64_t n, cudaStream_t st) {
 int gemm(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
          int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st) {
   CK(timed(0, st, [&] {
-    return launch_gemm_3xtf32(A, Alo, B, Blo, C, M, N, K, ldc, 3, -1, st);
+    return launch_gemm_3xtf32(A, Alo, B, Blo, C, M, N, K, ldc, product_terms(Alo), -1, st);
   }));
   return GIGA_OK;
 }
@@ -424,7 +424,8 @@ bool force_comm() { return env_int("GIGA_FORCE_COMM", 0) != 0; }
 int gemm_chunk(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
                int64_t rows, int64_t N, int64_t Kc, const GemmExtra &ex, cudaStream_t st) {
   CK(timed(0, st, [&] {
-    return launch_gemm_3xtf32(A, Alo, B, Blo, C, rows, N, Kc, N, 3, -1, st, 0, &ex);
+    return launch_gemm_3xtf32(A, Alo, B, Blo, C, rows, N, Kc, N, product_terms(Alo), -1, st,
+                              0, &ex);
   }));
   return GIGA_OK;
 }
