@@ -333,8 +333,11 @@ def main():
     tf32_sustained = 0.5 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     tf32_burst = 0.5 * peaks["bf16_tflops"]
     gemm_ms = kt["gemm_ms"] / max(1, kt["gemm_launches"])
-    # algorithmic tensor flops per launch: 3 TF32 MMAs per logical product (3xTF32)
-    tensor_flops = 3 * 2.0 * rows * N * K
+    # algorithmic tensor work per launch in TF32-instruction-equivalent flops: 3xTF32 issues
+    # 3 TF32 MMAs per logical product (6 rows N K); TF32 + BF16 one TF32 MMA plus one BF16 MMA
+    # of twice the depth at twice the rate (2 + 2 = 4 rows N K)
+    terms = giga.product_scheme(rows, N, K)
+    tensor_flops = (3 if terms == 3 else 2) * 2.0 * rows * N * K
     achieved = tensor_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
@@ -355,8 +358,11 @@ def main():
                          f"({peaks['bf16_tflops']}; nominal tf32:bf16 = 1.1:2.25); against the "
                          f"sustained figure ({peaks.get('bf16_tflops_sustained')}) frac = "
                          f"{round(achieved / tf32_sustained, 4) if achieved else None}; "
-                         f"achieved = 3 x 2 x rows x N x K tensor flops per launch / event time",
-            "split_ms_per_step": round(kt["split_ms"] / args.steps, 4)}
+                         f"achieved = {3 if terms == 3 else 2} x 2 x rows x N x K TF32-equivalent "
+                         f"tensor flops per launch / event time",
+            "scheme": "3xTF32" if terms == 3 else "TF32+BF16",
+            "prep_ms_per_step": round(kt["split_ms"] / args.steps, 4),
+            "prep_launches_per_step": round(kt["split_launches"] / args.steps, 2)}
 
     # ---- the north_star's whole-step roofline: T_roof / t with
     #      T_roof = max(2 r_max N K / (P_tf32 / 3), 4 (K N [g > 1] + (M - r_min) N) / BW_nvlink)
@@ -370,6 +376,11 @@ def main():
                  "t_comp_ms": round(t_comp * 1e3, 4), "t_comm_ms": round(t_comm * 1e3, 4),
                  "bound": "tensor" if t_comp >= t_comm else "nvlink",
                  "frac": round(t_roof / (ms_step * 1e-3), 4)}
+    if terms == 2:  # the scheme's own ceiling: 2 TF32-instruction-equivalents per product
+        t_comp2 = 2.0 * max(rows_all) * N * K / (tf32_burst * 1e12 / 2)
+        step_roof["scheme_note"] = ("the north_star's T_comp assumes 3xTF32 (P_tf32/3); the "
+                                    "TF32 + BF16 scheme's ceiling is P_tf32/2")
+        step_roof["frac_scheme"] = round(max(t_comp2, t_comm) / (ms_step * 1e-3), 4)
 
     # ---- end to end: host buffers through the C ABI ----
     e2e = None
@@ -406,8 +417,11 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": vs_base,
             "wall_ms_per_step": round(wall_ms / args.steps, 4),
-            "dtype": "f32", "arithmetic": "3xTF32 tcgen05 MMAs + fp32 RN promotion "
-                                          "(fp32-accurate: <= 1e-5 sum|A||B|)",
+            "dtype": "f32",
+            "arithmetic": ("3xTF32 tcgen05 MMAs" if terms == 3 else
+                           "TF32 + BF16 tcgen05 MMAs (a_hi b_hi in TF32, a_lo b + a_hi b_lo in one "
+                           "K=16 BF16 MMA; operands prepared in HBM per call)")
+                          + " + fp32 RN promotion (fp32-accurate: <= 1e-5 sum|A||B|)",
             "data": "synthetic",
             "config": {"workload": f"{args.config} M={M} N={N} K={K}", "dist": args.dist,
                        "parallelism": f"row-split x{world}",

@@ -18,9 +18,11 @@
  * (row stride K), B is K x N (row stride N), C is M x N (row stride N). No transposes, no
  * alpha/beta.
  *
- * Precision: fp32 in, fp32 out, fp32-accurate: internally each product is formed as
- * 3xTF32 (a_lo*b_hi + a_hi*b_lo + a_hi*b_hi on the tcgen05 tensor cores, partial sums
- * promoted into fp32 registers) so that per element
+ * Precision: fp32 in, fp32 out, fp32-accurate: internally each product is formed from
+ * TF32 hi / lo parts on the tcgen05 tensor cores -- 3xTF32 (a_lo*b_hi + a_hi*b_lo +
+ * a_hi*b_hi) or, for large launches, TF32 + BF16 (a_hi*b_hi in TF32, a_lo*b + a_hi*b_lo in
+ * one BF16 MMA; giga_product_scheme) -- with partial sums promoted into fp32 registers, so
+ * that per element
  *     |C - C_exact| <= 1e-5 * sum_k |A_ik| |B_kj|          (BASELINE.json north_star)
  * and integer-valued inputs whose partial sums stay below 2^24 give bit-exact results.
  * Non-finite inputs: NaN propagates; Inf may turn into NaN (Inf - Inf in the split).
@@ -49,6 +51,9 @@
  *   GIGA_TRACE           1: print a JSON timeline of each pipelined call on stderr [0]
  *   GIGA_HOST_H2D_GBS, GIGA_HOST_D2H_GBS, GIGA_HOST_GEMM_TFLOPS  rates of the host-path
  *                        schedule model [50, 50, 255]
+ *   GIGA_SCHEME          3xtf32 | tf32bf16: force the product scheme (once) [by shape]
+ *   GIGA_HI_RN, GIGA_A_PRE, GIGA_B_PRE  TF32 + BF16: 0 = truncated hi / A' / B' built on chip
+ *                        instead of RN hi / prepared in HBM (measurements; once) [1, 1, 1]
  *   GIGA_LO_PRESPLIT     1: 3xTF32 low parts split in HBM (comparison mode; once) [0]
  *   GIGA_PROMOTE_KBLOCKS TMEM accumulation interval in 16-deep k-blocks (once) [8]
  *   GIGA_CTA_GROUP       1 | 2: force the GEMM tile variant (once) [by shape]
@@ -282,6 +287,15 @@ int giga_rank_compute_only(const float *A_shard, const float *B, float *C_full, 
  * q = 0, 1, ..., s-1 by the part that finishes last (grids under one wave only).
  * $GIGA_TAIL_SPLIT=0 disables the k-split (s = 1). Errors: INVALID_ARG. */
 int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *out);
+
+/* The fp32-accurate scheme the product path uses for one M x N x K GEMM launch (host-only,
+ * DESIGN.md 6.7): *terms = 3 (3xTF32: three kind::tf32 MMAs per k8 step) or 2 (TF32 + BF16:
+ * a_hi*b_hi as one kind::tf32 MMA plus a_lo*b + a_hi*b_lo as one K=16 kind::f16 MMA, with
+ * hi = RN tf32(x); A_hi, A', B_hi, B' prepared once per launch in library-owned HBM scratch
+ * by two elementwise kernels; per-product split error <= 2^-18 |a||b|). 2 when M, N >= 8192,
+ * K >= 2048 and 1/M + 1/N < 1.6e-4 (the preparation is then amortised), else 3;
+ * $GIGA_SCHEME = 3xtf32 | tf32bf16 forces one. Errors: INVALID_ARG. */
+int giga_product_scheme(int64_t M, int64_t N, int64_t K, int *terms);
 
 /* ------------------------------------------------------------------------------------ */
 /* Kernel timing (bench.py's roofline): when enabled, CUDA events bracket every GEMM and

@@ -689,16 +689,18 @@ int giga_rank_compute_only(const float *A_shard, const float *B, float *C_full, 
   ex.ldb = N;
   ex.max_ctas = world > 1 ? pipeline_max_ctas(dev) : 0;
   auto none = [](int) { return int(GIGA_OK); };
-  if (world == 1) {  // the single-GPU path: one whole GEMM on all SMs
-    CK(timed(0, static_cast<cudaStream_t>(stream), [&] {
-      return launch_gemm_3xtf32(A_shard, nullptr, B, nullptr, C_full, M, N, K, N,
-                                product_terms(nullptr), -1,
-                                static_cast<cudaStream_t>(stream));
-    }));
-    return GIGA_OK;
-  }
+  if (world == 1)  // the single-GPU path: one whole GEMM on all SMs
+    return run_gemm(A_shard, nullptr, B, nullptr, C_full, M, N, K, N, GemmExtra(),
+                    static_cast<cudaStream_t>(stream));
   return rank_gemms(plan, ex, M, N, K, world, rank, A_shard, nullptr, B, nullptr, C_full,
                     static_cast<cudaStream_t>(stream), none, none);
+}
+
+int giga_product_scheme(int64_t M, int64_t N, int64_t K, int *terms) {
+  if (!terms) return fail(GIGA_ERR_INVALID_ARG, "giga_product_scheme: NULL terms");
+  TRY(check_dims(M, N, K));
+  *terms = product_terms(lo_presplit() ? reinterpret_cast<const float *>(1) : nullptr, M, N, K);
+  return GIGA_OK;
 }
 
 int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *out) {

@@ -48,6 +48,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <list>
 #include <mutex>
 #include <vector>
 
@@ -110,6 +111,10 @@ struct GemmParams {
   int n_cdst;     // C destinations in CMaps (1 + peers when the gather is fused)
   int lo_smem;    // 1: lo tiles computed in smem from the raw tiles; 0: TMA-loaded (A_lo, B_lo)
   int hi_rn;      // terms == 2: hi = RN tf32(x) written over the raw tile (else hi = trunc)
+  int b_pre;      // terms == 2: B_hi and B' precomputed in HBM by prep_b_kernel (TMA-loaded
+                  // through tmB / tmBlo); the transform warps handle A only
+  int a_pre;      // terms == 2 (with b_pre): A_hi and A' precomputed too (tmA / tmAlo); no
+                  // transform work in the kernel
 };
 
 // C tensor maps: [0] this GPU's C, [1..] the same rows of the peers' C_full buffers.
@@ -220,7 +225,7 @@ __device__ __forceinline__ float tf32_hi(float x, int rn) {
   return __uint_as_float((rn ? b + 0x1000u : b) & 0xFFFFE000u);
 }
 
-template <int CG>
+template <int CG, bool B_PRE>
 __device__ __forceinline__ void xform_tf32_bf16(uint32_t sA, int xt, int rn) {
   using namespace cfg;
   using T = Tile<CG>;
@@ -237,8 +242,8 @@ __device__ __forceinline__ void xform_tf32_bf16(uint32_t sA, int xt, int rn) {
     xa[i][1] = ptx::ld_shared_v4(row + ((uint32_t(2 * h + 1) ^ sw) << 4));
   }
   // B: units (k-row k, 8-column granule); 8 consecutive lanes cover 64 columns of one row
-  constexpr int UB = (T::B_COLS / 8) * BK / NT;  // 4 (CG = 2), 8 (CG = 1)
-  float4 xb[UB][2];
+  constexpr int UB = B_PRE ? 0 : (T::B_COLS / 8) * BK / NT;  // 4 (CG = 2), 8 (CG = 1)
+  float4 xb[UB > 0 ? UB : 1][2];
 #pragma unroll
   for (int i = 0; i < UB; ++i) {
     const int u = i * NT + xt, g8 = u & 7, k = (u >> 3) & (BK - 1), nch = u >> 7;
@@ -375,7 +380,11 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     // ======================= TMA producer (both CTAs) =======================
     if (lane == 0) {
       const bool load_lo = p.terms == 3 && !p.lo_smem;
-      const uint32_t tx_cta = load_lo ? T::STAGE_BYTES : (A_BYTES + T::B_BYTES);
+      const bool load_bx = p.terms == 2 && p.b_pre;
+      const bool load_ax = load_bx && p.a_pre;
+      const uint32_t tx_cta = (load_lo || load_ax) ? T::STAGE_BYTES
+                              : load_bx ? (A_BYTES + 2 * T::B_BYTES)
+                                        : (A_BYTES + T::B_BYTES);
       int stage = 0;
       uint32_t phase = 0;
       int wave = 0;
@@ -415,6 +424,12 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
 #pragma unroll
           for (int c = 0; c < T::B_COLS / 32; ++c)
             ptx::tma_load_2d(sB + c * B_CHUNK_BYTES, &tmB, &full[stage], n0 + 32 * c, k0);
+          if (load_ax) ptx::tma_load_2d(sAlo, &tmAlo, &full[stage], 2 * k0, m0);
+          if (load_bx) {
+#pragma unroll
+            for (int c = 0; c < T::B_COLS / 64; ++c)
+              ptx::tma_load_2d(sBlo + c * 4096, &tmBlo, &full[stage], n0 + 64 * c, 2 * k0);
+          }
           if (load_lo) {
             ptx::tma_load_2d(sAlo, &tmAlo, &full[stage], k0, m0);
 #pragma unroll
@@ -550,8 +565,11 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
                               tf32_lo(vb[i].x), tf32_lo(vb[i].y), tf32_lo(vb[i].z),
                               tf32_lo(vb[i].w));
           ptx::fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
-        } else if (p.terms == 2) {
-          xform_tf32_bf16<CG>(ptx::smem_u32(smem + stage * T::STAGE_BYTES), xt, p.hi_rn);
+        } else if (p.terms == 2 && !p.a_pre) {
+          if (p.b_pre)
+            xform_tf32_bf16<CG, true>(ptx::smem_u32(smem + stage * T::STAGE_BYTES), xt, p.hi_rn);
+          else
+            xform_tf32_bf16<CG, false>(ptx::smem_u32(smem + stage * T::STAGE_BYTES), xt, p.hi_rn);
           ptx::fence_proxy_async_smem();
         }
         __syncwarp();
@@ -749,6 +767,83 @@ __global__ void __launch_bounds__(256) split_lo_kernel(const float *__restrict__
   }
 }
 
+// B operand of the TF32 + BF16 scheme, once per call in HBM (B is read by every M-tile, so the
+// transform warps would redo this per tile): B_hi[k][n] = RN tf32(b) (fp32, the tf32 MMA's
+// operand) and B'[16 (k / 8) + (k % 8)][n] = bf16(b), B'[16 (k / 8) + 8 + (k % 8)][n] =
+// bf16(b - B_hi) (bf16, ldx columns), rows of k >= K zero: the layout one 64 x 32 TMA box
+// (128B swizzle) lands as the MN-major SW128 B' chunk the correction MMA reads. HBM-bound:
+// 4 B read + 8 B written per element. Thread = 4 columns x one k8 block.
+__global__ void __launch_bounds__(256) prep_b_kernel(const float *__restrict__ B, int64_t ldb,
+                                                     int K, int N, float *__restrict__ Bhi,
+                                                     uint16_t *__restrict__ Bx, int64_t ldx) {
+  const int n4 = N >> 2, kb8 = (K + 7) >> 3;
+  const int64_t total = int64_t(kb8) * n4;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int kb = int(i / n4), n = int(i - int64_t(kb) * n4) * 4;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = kb * 8 + j;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < K) v = __ldcs(reinterpret_cast<const float4 *>(B + int64_t(k) * ldb + n));
+      const float h0 = tf32_hi(v.x, 1), h1 = tf32_hi(v.y, 1), h2 = tf32_hi(v.z, 1),
+                  h3 = tf32_hi(v.w, 1);
+      if (k < K)
+        __stcs(reinterpret_cast<float4 *>(Bhi + int64_t(k) * N + n), make_float4(h0, h1, h2, h3));
+      const uint2 big = make_uint2(ptx::pack_bf16x2(v.x, v.y), ptx::pack_bf16x2(v.z, v.w));
+      const uint2 sml = make_uint2(ptx::pack_bf16x2(__fsub_rn(v.x, h0), __fsub_rn(v.y, h1)),
+                                   ptx::pack_bf16x2(__fsub_rn(v.z, h2), __fsub_rn(v.w, h3)));
+      __stcs(reinterpret_cast<uint2 *>(Bx + int64_t(16 * kb + j) * ldx + n), big);
+      __stcs(reinterpret_cast<uint2 *>(Bx + int64_t(16 * kb + 8 + j) * ldx + n), sml);
+    }
+  }
+}
+
+// A operand of the TF32 + BF16 scheme in HBM: A_hi[m][k] = RN tf32(a) (row stride K) and the
+// K-major A'[m][16 (k / 8) + (k % 8)] = bf16(a - A_hi), A'[m][16 (k / 8) + 8 + (k % 8)] =
+// bf16(A_hi) (row stride ldx = 2 * ceil(K / 8) * 8, k >= K zero): a 32 x 128 TMA box with the
+// 64B swizzle lands as the A' tile of a k-block. Thread = one row x one k8 block (32 B out).
+__global__ void __launch_bounds__(256) prep_a_kernel(const float *__restrict__ A, int64_t lda,
+                                                     int M, int K, float *__restrict__ Ahi,
+                                                     uint16_t *__restrict__ Ax, int64_t ldx) {
+  const int kb8 = (K + 7) >> 3;
+  const int64_t total = int64_t(M) * kb8;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t m = i / kb8;
+    const int kb = int(i - m * kb8), k = kb * 8;
+    const float *src = A + m * lda + k;
+    float v[8];
+    if (k + 8 <= K) {
+      const float4 a0 = __ldcs(reinterpret_cast<const float4 *>(src));
+      const float4 a1 = __ldcs(reinterpret_cast<const float4 *>(src + 4));
+      v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w;
+      v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (k + j < K) ? src[j] : 0.f;
+    }
+    float h[8], l[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      h[j] = tf32_hi(v[j], 1);
+      l[j] = __fsub_rn(v[j], h[j]);
+    }
+    float *hd = Ahi + m * K + k;
+    if (k + 8 <= K) {
+      __stcs(reinterpret_cast<float4 *>(hd), make_float4(h[0], h[1], h[2], h[3]));
+      __stcs(reinterpret_cast<float4 *>(hd + 4), make_float4(h[4], h[5], h[6], h[7]));
+    } else {
+      for (int j = 0; j < 8 && k + j < K; ++j) hd[j] = h[j];
+    }
+    uint4 *xd = reinterpret_cast<uint4 *>(Ax + m * ldx + 16 * kb);
+    __stcs(xd, make_uint4(ptx::pack_bf16x2(l[0], l[1]), ptx::pack_bf16x2(l[2], l[3]),
+                          ptx::pack_bf16x2(l[4], l[5]), ptx::pack_bf16x2(l[6], l[7])));
+    __stcs(xd + 1, make_uint4(ptx::pack_bf16x2(h[0], h[1]), ptx::pack_bf16x2(h[2], h[3]),
+                              ptx::pack_bf16x2(h[4], h[5]), ptx::pack_bf16x2(h[6], h[7])));
+  }
+}
+
 // ---- host side ----------------------------------------------------------------------------
 // Promotion interval: kDefaultPromoteKBlocks, overridable once per process with the
 // GIGA_PROMOTE_KBLOCKS environment variable (0 = never promote; tests / sweeps only).
@@ -764,14 +859,18 @@ int default_promote_kblocks() {
   return v;
 }
 
-int product_terms(const float *A_lo) {
-  static const int v = [] {
+int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K) {
+  static const int forced = [] {
     const char *e = getenv("GIGA_SCHEME");
     if (e && strcmp(e, "3xtf32") == 0) return 3;
     if (e && strcmp(e, "tf32bf16") == 0) return 2;
-    return kDefaultTerms;
+    return 0;
   }();
-  return A_lo ? 3 : v;
+  if (A_lo) return 3;
+  if (forced) return forced;
+  return (M >= 8192 && N >= 8192 && K >= 2048 && 1.0 / double(M) + 1.0 / double(N) < 1.6e-4)
+             ? 2
+             : 3;
 }
 
 // CTA-group size: 2 (CTA pairs) unless the problem has fewer 256-row tiles than SM pairs,
@@ -820,6 +919,20 @@ static bool make_map(CUtensorMap *m, const float *ptr, uint64_t cols, uint64_t r
   return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims,
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, promo,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 2-D bf16 map (B' of the TF32 + BF16 scheme), 128B swizzle.
+static bool make_map_bf16(CUtensorMap *m, const uint16_t *ptr, uint64_t cols, uint64_t rows,
+                          uint64_t ld, uint32_t box_cols, uint32_t box_rows,
+                          CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * sizeof(uint16_t)};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t *>(ptr), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
 }
 
 static int num_sms_current() {
@@ -935,8 +1048,53 @@ bool ksplit_workspace(cudaStream_t st, size_t ws_bytes, size_t cnt_n, float **ws
   return true;
 }
 
+// Per-(device, stream) scratch of the TF32 + BF16 scheme's B_hi / B' (grow-only, like the
+// K-split workspace; growth waits for the stream's earlier launches).
+// The B part comes first in the buffer and remembers what it holds (key: B, ldb, K, N of the
+// last preparation), so row chunks of one product can skip re-preparing B.
+struct ScratchBuf {
+  cudaStream_t st;
+  int dev;
+  void *p;
+  size_t bytes;
+  const float *key_b;
+  int64_t key_ldb, key_k, key_n;
+};
+static std::list<ScratchBuf> g_bpre;
+
+static ScratchBuf *bpre_scratch(cudaStream_t st, size_t bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_ksplit_mu);
+  for (auto &b : g_bpre)
+    if (b.st == st && b.dev == dev && b.bytes >= bytes) return &b;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return nullptr;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return nullptr;
+  for (auto it = g_bpre.begin(); it != g_bpre.end(); ++it)
+    if (it->st == st && it->dev == dev) {
+      cudaFree(it->p);
+      g_bpre.erase(it);
+      break;
+    }
+  void *p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  g_bpre.push_back({st, dev, p, bytes, nullptr, 0, 0, 0});
+  return &g_bpre.back();
+}
+
 void release_gemm_caches() {
   std::lock_guard<std::mutex> lk(g_ksplit_mu);
+  for (auto &b : g_bpre) {
+    cudaSetDevice(b.dev);
+    cudaDeviceSynchronize();
+    cudaFree(b.p);
+  }
+  g_bpre.clear();
   for (auto &e : g_ksplit) {
     cudaSetDevice(e.second.dev);
     cudaDeviceSynchronize();
@@ -1025,6 +1183,75 @@ static cudaError_t ensure_smem_attr() {
   return e;
 }
 
+// ---- TF32 + BF16 operand preparation (terms = 2) ---------------------------------------------
+cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, TermsPrep *tp) {
+  *tp = TermsPrep();
+  if (ensure_tma_encoder() != 0) return cudaErrorNotSupported;
+  // $GIGA_B_PRE=0: the transform warps build B' per tile (and A' too); $GIGA_A_PRE=0: A' only
+  static const bool b_pre_env = [] {
+    const char *e = getenv("GIGA_B_PRE");
+    return !(e && *e == '0');
+  }();
+  static const bool a_pre_env = [] {
+    const char *e = getenv("GIGA_A_PRE");
+    return !(e && *e == '0');
+  }();
+  if (!b_pre_env) return cudaSuccess;
+  const int64_t k8 = (K + 7) / 8 * 8, ldx = (N + 7) / 8 * 8;
+  auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t hi_b = up(size_t(K) * size_t(N) * 4), bx_b = up(size_t(2 * k8) * ldx * 2);
+  const size_t hi_a = up(size_t(M) * size_t(K) * 4), ax_b = up(size_t(M) * size_t(2 * k8) * 2);
+  ScratchBuf *sb = bpre_scratch(st, hi_b + bx_b + (a_pre_env ? hi_a + ax_b : 0));
+  if (!sb) return cudaSuccess;  // no scratch (capture, OOM): operands built on chip
+  uint8_t *scr = static_cast<uint8_t *>(sb->p);
+  tp->owner = sb;
+  tp->k8 = k8;
+  tp->ldbx = ldx;
+  tp->Bhi = reinterpret_cast<float *>(scr);
+  tp->Bx = reinterpret_cast<uint16_t *>(scr + hi_b);
+  if (a_pre_env) {
+    tp->Ahi = reinterpret_cast<float *>(scr + hi_b + bx_b);
+    tp->Ax = reinterpret_cast<uint16_t *>(scr + hi_b + bx_b + hi_a);
+  }
+  tp->key_b = sb->key_b;
+  tp->key_ldb = sb->key_ldb;
+  tp->key_k = sb->key_k;
+  tp->key_n = sb->key_n;
+  return cudaSuccess;
+}
+
+bool TermsPrep::b_matches(const float *B, int64_t ldb, int64_t N, int64_t K) const {
+  return Bhi && key_b == B && key_ldb == ldb && key_k == K && key_n == N;
+}
+
+cudaError_t launch_prep_b(const float *B, int64_t ldb, int64_t N, int64_t K, TermsPrep *tp,
+                          cudaStream_t st) {
+  ScratchBuf *sb = static_cast<ScratchBuf *>(tp->owner);
+  const int64_t units = (tp->k8 / 8) * (N / 4);
+  const int64_t blocks = std::min<int64_t>((units + 255) / 256, int64_t(num_sms_current()) * 8);
+  sb->key_b = nullptr;
+  prep_b_kernel<<<unsigned(std::max<int64_t>(blocks, 1)), 256, 0, st>>>(
+      B, ldb, int(K), int(N), const_cast<float *>(tp->Bhi), const_cast<uint16_t *>(tp->Bx),
+      tp->ldbx);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  sb->key_b = tp->key_b = B;
+  sb->key_ldb = tp->key_ldb = ldb;
+  sb->key_k = tp->key_k = K;
+  sb->key_n = tp->key_n = N;
+  return cudaSuccess;
+}
+
+cudaError_t launch_prep_a(const float *A, int64_t lda, int64_t M, int64_t K, TermsPrep *tp,
+                          cudaStream_t st) {
+  const int64_t units = M * (tp->k8 / 8);
+  const int64_t blocks = std::min<int64_t>((units + 255) / 256, int64_t(num_sms_current()) * 8);
+  prep_a_kernel<<<unsigned(std::max<int64_t>(blocks, 1)), 256, 0, st>>>(
+      A, lda, int(M), int(K), const_cast<float *>(tp->Ahi), const_cast<uint16_t *>(tp->Ax),
+      2 * tp->k8);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
                                const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,
                                int64_t ldc, int terms, int promote_kblocks, cudaStream_t st,
@@ -1082,6 +1309,34 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
     return (e && *e == '0') ? 0 : 1;
   }();
   p.hi_rn = hi_rn_env;
+  p.b_pre = 0;
+  p.a_pre = 0;
+  if (terms == 2) {
+    // operands prepared in HBM (the caller's TermsPrep, else here, untimed)
+    TermsPrep local;
+    const TermsPrep *tp = ex->prep;
+    if (!tp) {
+      cudaError_t e = terms_prep_alloc(M, N, K, st, &local);
+      if (e == cudaSuccess && local.Bhi && !(ex->b_prep_reuse && local.b_matches(B, ldb, N, K)))
+        e = launch_prep_b(B, ldb, N, K, &local, st);
+      if (e == cudaSuccess && local.Ahi) e = launch_prep_a(A, lda, M, K, &local, st);
+      if (e != cudaSuccess) return e;
+      tp = &local;
+    }
+    if (tp->Ahi && tp->Bhi) {
+      if (!make_map(&tA, tp->Ahi, K, M, K, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
+          !make_map_bf16(&tAlo, tp->Ax, 2 * tp->k8, M, 2 * tp->k8, 32, BM,
+                         CU_TENSOR_MAP_SWIZZLE_64B))
+        return cudaErrorInvalidValue;
+      p.a_pre = 1;
+    }
+    if (tp->Bhi) {
+      if (!make_map(&tB, tp->Bhi, N, K, N, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+          !make_map_bf16(&tBlo, tp->Bx, N, 2 * tp->k8, tp->ldbx, 64, 32))
+        return cudaErrorInvalidValue;
+      p.b_pre = 1;
+    }
+  }
   p.n_kb = int((K + BK - 1) / BK);
   int pk = promote_kblocks < 0 ? default_promote_kblocks() : promote_kblocks;
   p.p_kb = (pk == 0 || pk > p.n_kb) ? p.n_kb : pk;

@@ -100,8 +100,10 @@ int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M
     CK(cudaStreamWaitEvent(d.compute, d.ev_rchunk[q], 0));
     if (q1 > q0) {
       TRY(split(Ad + q0 * K, at(Alo, q0 * K), (q1 - q0) * K, d.compute));
-      TRY(gemm(Ad + q0 * K, at(Alo, q0 * K), Bd, Blo, Cd + q0 * N, q1 - q0, N, K, N,
-               d.compute));
+      GemmExtra e2;
+      e2.b_prep_reuse = q > 0;  // every late row block multiplies by the same full B
+      TRY(gemm_chunk(Ad + q0 * K, at(Alo, q0 * K), Bd, Blo, Cd + q0 * N, q1 - q0, N, K, e2,
+                     d.compute));
     }
     CK(cudaEventRecord(d.ev_done[q], d.compute));
     TRY(tr.mark("gemm2", d.compute));

@@ -12,12 +12,13 @@ constexpr int kDefaultPromoteKBlocks = 8;
 // The promotion interval in effect (kDefaultPromoteKBlocks or $GIGA_PROMOTE_KBLOCKS).
 int default_promote_kblocks();
 
-// The product path's fp32-accurate scheme: 3 = 3xTF32 (three kind::tf32 MMAs
-// per k8 step), 2 = TF32 + BF16 (hi*hi as kind::tf32, both corrections as one K=16 kind::f16
-// MMA). kDefaultTerms unless $GIGA_SCHEME is "3xtf32" or "tf32bf16". With pre-split lo
-// operands (A_lo != nullptr) the scheme is always 3.
-constexpr int kDefaultTerms = 3;
-int product_terms(const float *A_lo);
+// The product path's fp32-accurate scheme for an M x N x K launch: 3 = 3xTF32
+// (three kind::tf32 MMAs per k8 step), 2 = TF32 + BF16 (hi*hi as kind::tf32, both corrections
+// as one K=16 kind::f16 MMA, operands prepared once per launch in HBM). 2 where the operand
+// preparation (~12 B per element of A and B) is amortised: M, N >= 8192, K >= 2048 and
+// 1/M + 1/N < 1.6e-4; else 3. $GIGA_SCHEME = "3xtf32" / "tf32bf16" forces one. With pre-split
+// lo operands (A_lo != nullptr) the scheme is always 3.
+int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K);
 
 // lo = x - tf32(x) over n elements (HBM-bound elementwise split).
 cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t st);
@@ -40,6 +41,26 @@ cudaError_t launch_split_lo_2d(const float *x, float *lo, int64_t rows, int64_t 
 // bits as accumulate's reduce-add), then stores the sum to C and every peer -- the last chunk
 // of a K-chunked series, so that only final values cross NVLink.
 constexpr int kMaxCDst = 8;
+// Operands of the TF32 + BF16 scheme prepared in HBM (per-stream scratch, library-owned):
+// B_hi = RN tf32(B), B' = bf16 [b ; b_lo] per k8 block (ldbx columns), A_hi = RN tf32(A),
+// A' = bf16 [a_lo | a_hi] per k8 block (2 * k8 columns). Null pointers: that operand is built
+// by the GEMM's transform warps. key_*: what the B part holds now.
+struct TermsPrep {
+  const float *Ahi = nullptr, *Bhi = nullptr;
+  const uint16_t *Ax = nullptr, *Bx = nullptr;
+  int64_t k8 = 0, ldbx = 0;
+  void *owner = nullptr;
+  const float *key_b = nullptr;
+  int64_t key_ldb = 0, key_k = 0, key_n = 0;
+  bool b_matches(const float *B, int64_t ldb, int64_t N, int64_t K) const;
+};
+// Reserve the scratch for an M x N x K product on `st` (pointers stay null when it cannot be
+// had: stream capture, OOM, $GIGA_B_PRE=0), then prepare B and A into it (stream-ordered).
+cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, TermsPrep *tp);
+cudaError_t launch_prep_b(const float *B, int64_t ldb, int64_t N, int64_t K, TermsPrep *tp,
+                          cudaStream_t st);
+cudaError_t launch_prep_a(const float *A, int64_t lda, int64_t M, int64_t K, TermsPrep *tp,
+                          cudaStream_t st);
 struct GemmExtra {
   int64_t lda = 0, ldb = 0;
   int accumulate = 0;
@@ -47,6 +68,10 @@ struct GemmExtra {
   float *const *peer_c = nullptr;
   int n_peer_c = 0;
   int load_c = 0;
+  // TF32 + BF16 scheme: 1 = B (same pointer, ldb, K, N) is unchanged since the previous launch
+  // on this stream (row chunks of one product), so its prepared B_hi / B' are reused
+  int b_prep_reuse = 0;
+  const TermsPrep *prep = nullptr;  // terms = 2: operands already prepared by the caller
 };
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
                                const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,

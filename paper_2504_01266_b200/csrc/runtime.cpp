@@ -165,12 +165,31 @@ int split(const float *x, float *lo, int64_t n, cudaStream_t st) {
   return GIGA_OK;
 }
 
-int gemm(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
-         int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st) {
+// One product GEMM with the scheme product_terms picks; for the TF32 + BF16 scheme its operand
+// preparation launches first, timed as "split" launches (bench.py's roofline separates them).
+int run_gemm(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
+             int64_t M, int64_t N, int64_t K, int64_t ldc, const GemmExtra &ex,
+             cudaStream_t st) {
+  const int terms = product_terms(Alo, M, N, K);
+  GemmExtra e = ex;
+  TermsPrep tp;
+  if (terms == 2) {
+    const int64_t lda = e.lda ? e.lda : K, ldb = e.ldb ? e.ldb : N;
+    CK(terms_prep_alloc(M, N, K, st, &tp));
+    if (tp.Bhi && !(e.b_prep_reuse && tp.b_matches(B, ldb, N, K)))
+      CK(timed(1, st, [&] { return launch_prep_b(B, ldb, N, K, &tp, st); }));
+    if (tp.Ahi) CK(timed(1, st, [&] { return launch_prep_a(A, lda, M, K, &tp, st); }));
+    e.prep = &tp;
+  }
   CK(timed(0, st, [&] {
-    return launch_gemm_3xtf32(A, Alo, B, Blo, C, M, N, K, ldc, product_terms(Alo), -1, st);
+    return launch_gemm_3xtf32(A, Alo, B, Blo, C, M, N, K, ldc, terms, -1, st, 0, &e);
   }));
   return GIGA_OK;
+}
+
+int gemm(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
+         int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st) {
+  return run_gemm(A, Alo, B, Blo, C, M, N, K, ldc, GemmExtra(), st);
 }
 
 int shard_compute(DevCtx &d, cudaStream_t st, const float *A, int64_t rows, const float *B,
@@ -423,11 +442,7 @@ bool force_comm() { return env_int("GIGA_FORCE_COMM", 0) != 0; }
 
 int gemm_chunk(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
                int64_t rows, int64_t N, int64_t Kc, const GemmExtra &ex, cudaStream_t st) {
-  CK(timed(0, st, [&] {
-    return launch_gemm_3xtf32(A, Alo, B, Blo, C, rows, N, Kc, N, product_terms(Alo), -1, st,
-                              0, &ex);
-  }));
-  return GIGA_OK;
+  return run_gemm(A, Alo, B, Blo, C, rows, N, Kc, N, ex, st);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -214,6 +214,9 @@ bool lo_presplit();
 size_t lo_bytes(int64_t elems);
 float *lo_at(Buf &b, int64_t off = 0);
 int split(const float *x, float *lo, int64_t n, cudaStream_t st);
+int run_gemm(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
+             int64_t M, int64_t N, int64_t K, int64_t ldc, const GemmExtra &ex,
+             cudaStream_t st);
 int gemm(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
          int64_t M, int64_t N, int64_t K, int64_t ldc, cudaStream_t st);
 int gemm_chunk(const float *A, const float *Alo, const float *B, const float *Blo, float *C,

@@ -28,7 +28,7 @@ EXPORTS = (
     "giga_timing_enable", "giga_timing_reset", "giga_timing_read", "giga_pipeline_plan",
     "giga_plan_block", "giga_dot", "giga_l2norm", "giga_dot_rank", "giga_init_devices",
     "giga_rank_p2p_export", "giga_rank_p2p_import", "giga_host_plan", "giga_gemm_schedule",
-    "giga_rank_compute_only",
+    "giga_rank_compute_only", "giga_product_scheme",
 )
 P2P_BLOB_BYTES = 256
 
@@ -84,6 +84,7 @@ def _load():
                             ctypes.POINTER(ctypes.c_int), P64,
                             ctypes.POINTER(ctypes.c_double)], i32),
         "giga_gemm_schedule": ([i64, i64, i64, i32, P64], i32),
+        "giga_product_scheme": ([i64, i64, i64, ctypes.POINTER(ctypes.c_int)], i32),
         "giga_rank_compute_only": ([p, p, p, i64, i64, i64, i32, i32, p], i32),
     }
     for name, (args, res) in sig.items():
@@ -251,6 +252,13 @@ def gemm_schedule(M: int, N: int, K: int, num_sms: int = 148) -> dict:
     _check(lib.giga_gemm_schedule(M, N, K, num_sms, out))
     keys = ("cta_group", "tiles", "clusters", "n_kb", "first_split", "s", "units", "mode")
     return dict(zip(keys, list(out)))
+
+
+def product_scheme(M: int, N: int, K: int) -> int:
+    """3 (3xTF32) or 2 (TF32 + BF16): the scheme the product path uses for this launch."""
+    t = ctypes.c_int(0)
+    _check(lib.giga_product_scheme(M, N, K, ctypes.byref(t)))
+    return t.value
 
 
 def host_plan(M: int, N: int, K: int, num_sms: int = 148):

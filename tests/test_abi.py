@@ -81,3 +81,16 @@ def test_init_without_gpu_reports_no_device(giga):
         giga.init(1)
     assert e.value.status == "GIGA_ERR_NO_DEVICE"
     assert giga.num_devices() == 0
+
+
+def test_product_scheme_selection():
+    """giga_product_scheme (host-only): TF32 + BF16 only where its per-launch operand
+    preparation is amortised; 3xTF32 for the small and the skinny configs."""
+    from paper_2504_01266_b200 import giga
+    assert giga.product_scheme(16384, 16384, 16384) == 2
+    assert giga.product_scheme(32768, 32768, 32768) == 2
+    for shape in [(512, 512, 512), (4096, 4096, 4096), (262144, 1024, 1024),
+                  (4096, 32768, 32768), (16384, 16384, 1024)]:
+        assert giga.product_scheme(*shape) == 3, shape
+    with pytest.raises(Exception):
+        giga.product_scheme(0, 4, 4)

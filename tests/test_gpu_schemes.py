@@ -1,9 +1,9 @@
 """GPU parity of the fp32-accurate schemes of the shard GEMM against the CPU fp64 oracle.
 
-terms = 3: 3xTF32 (the product default, BASELINE north_star (3)).
+terms = 3: 3xTF32 (BASELINE north_star (3); the product scheme for small and skinny launches).
 terms = 2: TF32 + BF16 -- a_hi*b_hi as one kind::tf32 MMA plus both corrections as one K=16
 kind::f16 MMA over [bf16(a_lo) | bf16(a_hi)] . [bf16(b) ; bf16(b_lo)] (gemm_3xtf32.cu,
-DESIGN.md 6.7). Its split error is <= 2^-18 |a||b| per product with the RN hi (the library
+DESIGN.md 6.7; the product scheme for large launches, giga_product_scheme). Its split error is <= 2^-18 |a||b| per product with the RN hi (the library
 default), inside the 1e-5 * sum|A||B| bound (R5) with the accumulation error on top.
 """
 import numpy as np
@@ -93,29 +93,45 @@ def test_coherent_worst_case(giga, torch_cuda, terms):
     assert ok, st
 
 
-def test_scheme_is_selectable_for_the_product_path(tmp_path):
-    """GIGA_SCHEME=tf32bf16 routes the product path (giga_matmul_sharded) through terms = 2;
-    checked in a child process because the scheme is read once per process."""
+_CHILD = """
+import os, numpy as np, torch, oracle, synth
+from oracle.check import check_close, check_exact
+from paper_2504_01266_b200 import giga
+giga.init(1)
+M, N, K = 4096, 1040, 2064  # host schedule: 4 late row blocks
+dist = os.environ["CHILD_DIST"]
+A = synth.gen_matrix(M, K, synth.MATRIX_A, dist); B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
+ref, S = oracle.gemm(A, B)
+def check(C, what):
+    ok, st = check_exact(C, ref) if dist == "d3" else check_close(C, ref, S)
+    assert ok, (what, st)
+dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+dC = torch.full((M, N), float("nan"), device="cuda")
+giga.matmul_sharded([dA], [dB], [dC], M, N, K)
+check(dC.cpu().numpy(), "sharded")
+C = np.full((M, N), np.nan, np.float32)
+giga.matmul(A, B, C, M, N, K, 1)  # host buffers: K-chunks, then row blocks reusing B's prep
+check(C, "host")
+giga.finalize()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("dist", ["d1", "d3"])
+@pytest.mark.parametrize("env", [{}, {"GIGA_FORCE_COMM": "1", "GIGA_BCAST_CHUNKS": "3",
+                                      "GIGA_GATHER_CHUNKS": "3"}, {"GIGA_A_PRE": "0"},
+                                 {"GIGA_B_PRE": "0"}])
+def test_scheme_through_the_product_paths(dist, env):
+    """GIGA_SCHEME=tf32bf16 forces terms = 2 on every product launch: the device-resident
+    call, the host-buffer schedule (late row blocks reuse the prepared B: b_prep_reuse) and,
+    with GIGA_FORCE_COMM, the NCCL pipeline at world 1 (K-chunks accumulating, the last in row
+    chunks reusing B's preparation); also with A' / B' built on chip. Child processes: the
+    environment is read once per process."""
+    import os
     import subprocess
     import sys
-    import os
-    code = (
-        "import numpy as np, torch, oracle, synth\n"
-        "from oracle.check import check_close\n"
-        "from paper_2504_01266_b200 import giga\n"
-        "giga.init(1)\n"
-        "M, N, K = 520, 1000, 2000\n"
-        "A = synth.gen_matrix(M, K, synth.MATRIX_A, 'd1'); B = synth.gen_matrix(K, N, synth.MATRIX_B, 'd1')\n"
-        "dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()\n"
-        "dC = torch.full((M, N), float('nan'), device='cuda')\n"
-        "giga.matmul_sharded([dA], [dB], [dC], M, N, K)\n"
-        "ref, S = oracle.gemm(A, B)\n"
-        "ok, st = check_close(dC.cpu().numpy(), ref, S)\n"
-        "assert ok, st\n"
-        "print('ok', st['max_rel_err'])\n"
-        "giga.finalize()\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, GIGA_SCHEME="tf32bf16", PYTHONPATH=root)
-    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+    penv = dict(os.environ, GIGA_SCHEME="tf32bf16", PYTHONPATH=root, CHILD_DIST=dist, **env)
+    r = subprocess.run([sys.executable, "-c", _CHILD], env=penv, cwd=root, capture_output=True,
                        text=True, timeout=300)
-    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
