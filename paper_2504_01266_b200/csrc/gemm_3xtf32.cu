@@ -336,6 +336,8 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x / CG;
   const int num_clusters = gridDim.x / CG;
+  // TF32 + BF16 with both operands prepared in HBM: no transform, the MMA waits on `full`
+  const bool direct = p.terms == 2 && p.a_pre && p.b_pre;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -418,6 +420,37 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
           uint8_t *sB = sA + 2 * A_BYTES;
           uint8_t *sBlo = sB + T::B_BYTES;
           const int k0 = kb * BK;
+          if (direct) {
+            // no transform: every tile lands on the leader's `full` barrier, which the MMA
+            // issuer waits on (cta_group::2 loads complete on the peer's barrier)
+            if (CG == 1) {
+              ptx::mbar_expect_tx(&full[stage], tx_cta);
+              ptx::tma_load_2d(sA, &tmA, &full[stage], k0, m0);
+              ptx::tma_load_2d(sAlo, &tmAlo, &full[stage], 2 * k0, m0);
+#pragma unroll
+              for (int c = 0; c < T::B_COLS / 32; ++c)
+                ptx::tma_load_2d(sB + c * B_CHUNK_BYTES, &tmB, &full[stage], n0 + 32 * c, k0);
+#pragma unroll
+              for (int c = 0; c < T::B_COLS / 64; ++c)
+                ptx::tma_load_2d(sBlo + c * 4096, &tmBlo, &full[stage], n0 + 64 * c, 2 * k0);
+            } else {
+              const uint32_t fb = ptx::smem_u32(&full[stage]) & ptx::kPeerBitMask;
+              if (leader) ptx::mbar_expect_tx(&full[stage], 2 * tx_cta);
+              ptx::tma_load_2d_cg2(sA, &tmA, fb, k0, m0);
+              ptx::tma_load_2d_cg2(sAlo, &tmAlo, fb, 2 * k0, m0);
+#pragma unroll
+              for (int c = 0; c < T::B_COLS / 32; ++c)
+                ptx::tma_load_2d_cg2(sB + c * B_CHUNK_BYTES, &tmB, fb, n0 + 32 * c, k0);
+#pragma unroll
+              for (int c = 0; c < T::B_COLS / 64; ++c)
+                ptx::tma_load_2d_cg2(sBlo + c * 4096, &tmBlo, fb, n0 + 64 * c, 2 * k0);
+            }
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           // every CTA's tiles land on its own `full` barrier (its transform warps wait there)
           ptx::mbar_expect_tx(&full[stage], tx_cta);
           ptx::tma_load_2d(sA, &tmA, &full[stage], k0, m0);
@@ -463,7 +496,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
           const int kb_end = min(kb + p.p_kb, kb1);
           uint32_t acc = 0;
           for (; kb < kb_end; ++kb) {
-            ptx::mbar_wait(&lofull[stage], phase);
+            ptx::mbar_wait(direct ? &full[stage] : &lofull[stage], phase);
             ptx::tc_fence_after();
             const uint32_t sA = ptx::smem_u32(smem + stage * T::STAGE_BYTES);
             const uint32_t sAlo = sA + A_BYTES;
@@ -539,7 +572,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     const int xw = warp - XFORM_WARP0;
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = cluster_id; u < p.num_units; u += num_clusters) {
+    for (int u = direct ? p.num_units : cluster_id; u < p.num_units; u += num_clusters) {
       int t, kb0, kb1, part;
       unit_coords(u, p, t, kb0, kb1, part);
       for (int kb = kb0; kb < kb1; ++kb) {
