@@ -708,8 +708,10 @@ int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *ou
   TRY(check_dims(M, N, K));
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
     return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_schedule: dimension above 2^31 - 1");
+  const int terms =
+      product_terms(lo_presplit() ? reinterpret_cast<const float *>(1) : nullptr, M, N, K);
   const GemmSchedule s = gemm_schedule(M, N, K, num_sms > 0 ? num_sms : 148, 0, true,
-                                       default_promote_kblocks());
+                                       default_promote_kblocks(terms));
   const int64_t v[8] = {s.cg,          s.num_tiles, s.nclu,      s.n_kb,
                         s.first_split, s.s,         s.num_units, s.mode};
   for (int i = 0; i < 8; ++i) out[i] = v[i];

@@ -880,16 +880,17 @@ __global__ void __launch_bounds__(256) prep_a_kernel(const float *__restrict__ A
 // ---- host side ----------------------------------------------------------------------------
 // Promotion interval: kDefaultPromoteKBlocks, overridable once per process with the
 // GIGA_PROMOTE_KBLOCKS environment variable (0 = never promote; tests / sweeps only).
-int default_promote_kblocks() {
+int default_promote_kblocks(int terms) {
   static int v = [] {
     const char *e = getenv("GIGA_PROMOTE_KBLOCKS");
     if (e && *e) {
       const int x = atoi(e);
       if (x >= 0) return x;
     }
-    return kDefaultPromoteKBlocks;
+    return -1;
   }();
-  return v;
+  if (v >= 0) return v;
+  return terms == 2 ? kDefaultPromoteKBlocksT2 : kDefaultPromoteKBlocks;
 }
 
 int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K) {
@@ -1371,7 +1372,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
     }
   }
   p.n_kb = int((K + BK - 1) / BK);
-  int pk = promote_kblocks < 0 ? default_promote_kblocks() : promote_kblocks;
+  int pk = promote_kblocks < 0 ? default_promote_kblocks(terms) : promote_kblocks;
   p.p_kb = (pk == 0 || pk > p.n_kb) ? p.n_kb : pk;
   const bool plain = !p.accumulate && !p.load_c && ex->n_peer_c == 0;
   const GemmSchedule sch = gemm_schedule(M, N, K, num_sms, cg, plain, p.p_kb);

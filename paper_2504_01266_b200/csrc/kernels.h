@@ -7,10 +7,13 @@ namespace giga {
 
 // Default number of 16-wide k-blocks accumulated in TMEM before promotion into the fp32
 // register sum. 8 k-blocks = K 128 = 16 k8 steps.
+// The TF32 + BF16 scheme adds 2 MMAs per k8 step into TMEM instead of 3, so its truncation
+// drift per interval is smaller: 16 k-blocks (measured 32768^3 d1 worst case: DESIGN.md 6.7).
 constexpr int kDefaultPromoteKBlocks = 8;
+constexpr int kDefaultPromoteKBlocksT2 = 16;
 
-// The promotion interval in effect (kDefaultPromoteKBlocks or $GIGA_PROMOTE_KBLOCKS).
-int default_promote_kblocks();
+// The promotion interval in effect for `terms` (the defaults above or $GIGA_PROMOTE_KBLOCKS).
+int default_promote_kblocks(int terms = 3);
 
 // The product path's fp32-accurate scheme for an M x N x K launch: 3 = 3xTF32
 // (three kind::tf32 MMAs per k8 step), 2 = TF32 + BF16 (hi*hi as kind::tf32, both corrections
