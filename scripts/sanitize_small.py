@@ -28,6 +28,18 @@ for cg in (1, 2):
     giga.gemm_3xtf32(dA, dAlo, dB, dBlo, C2, M, N, K, cta_group=cg)
     torch.cuda.synchronize()
     assert torch.equal(C1, C2), cg
+# TF32 + BF16 scheme: operands prepared in HBM (prep kernels; direct TMA -> MMA barrier), and
+# with A' / B' built on chip by the transform warps (GIGA_A_PRE / GIGA_B_PRE are read once,
+# so the on-chip variants run in sanitize_t2_onchip.py); integer inputs give exact results
+M, N, K = 520, 516, 1040
+Ai = synth.gen_matrix(M, K, 1, "d3"); Bi = synth.gen_matrix(K, N, 2, "d3")
+dAi, dBi = torch.from_numpy(Ai).cuda(), torch.from_numpy(Bi).cuda()
+ref = torch.from_numpy(Ai.astype(np.float64) @ Bi.astype(np.float64)).float().cuda()
+for cg in (1, 2):
+    C3 = torch.full((M, N), float("nan"), device="cuda")
+    giga.gemm_3xtf32(dAi, None, dBi, None, C3, M, N, K, terms=2, cta_group=cg)
+    torch.cuda.synchronize()
+    assert torch.equal(C3, ref), ("terms 2", cg)
 x = synth.gen_vector(100003, 3, "d3"); y = synth.gen_vector(100003, 4, "d3")
 print("dot", giga.dot(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()))
 giga.finalize()
