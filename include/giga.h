@@ -292,8 +292,9 @@ int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *ou
  * DESIGN.md 6.7): *terms = 3 (3xTF32: three kind::tf32 MMAs per k8 step) or 2 (TF32 + BF16:
  * a_hi*b_hi as one kind::tf32 MMA plus a_lo*b + a_hi*b_lo as one K=16 kind::f16 MMA, with
  * hi = RN tf32(x); A_hi, A', B_hi, B' prepared once per launch in library-owned HBM scratch
- * by two elementwise kernels; per-product split error <= 2^-18 |a||b|). 2 when M, N >= 8192,
- * K >= 2048 and 1/M + 1/N < 1.6e-4 (the preparation is then amortised), else 3;
+ * by two elementwise kernels; per-product split error <= 2^-18 |a||b|). 2 when M >= 4096,
+ * N >= 8192, K >= 2048 and M N K >= 2^37 (the preparation is then amortised: measured
+ * crossover), else 3;
  * $GIGA_SCHEME = 3xtf32 | tf32bf16 forces one. Errors: INVALID_ARG. */
 int giga_product_scheme(int64_t M, int64_t N, int64_t K, int *terms);
 

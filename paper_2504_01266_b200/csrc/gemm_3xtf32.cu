@@ -902,7 +902,9 @@ int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K) {
   }();
   if (A_lo) return 3;
   if (forced) return forced;
-  return (M >= 8192 && N >= 8192 && K >= 2048 && 1.0 / double(M) + 1.0 / double(N) < 1.6e-4)
+  // measured crossover (profiles/r01_scheme_crossover.jsonl, preparation included): TF32 + BF16
+  // wins 2-11% from 8192 x 8192 x 2048 and 4096 x 32768^2 up, loses 2% at 4096^3
+  return (M >= 4096 && N >= 8192 && K >= 2048 && double(M) * double(N) * double(K) >= 0x1p37)
              ? 2
              : 3;
 }
