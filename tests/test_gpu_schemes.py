@@ -135,3 +135,45 @@ def test_scheme_through_the_product_paths(dist, env):
     r = subprocess.run([sys.executable, "-c", _CHILD], env=penv, cwd=root, capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+_CHILD_P2P = """
+import os, numpy as np, torch, oracle, synth
+from oracle.check import check_close, check_exact
+from paper_2504_01266_b200 import giga
+giga.init_devices([0, 0, 0])
+M, N, K = 1500, 1040, 2064
+dist = os.environ["CHILD_DIST"]
+A = synth.gen_matrix(M, K, synth.MATRIX_A, dist); B = synth.gen_matrix(K, N, synth.MATRIX_B, dist)
+ref, S = oracle.gemm(A, B)
+shards, Bs, Cs = [], [], []
+for g in range(3):
+    r0, rows = giga.partition(M, 3, g)
+    shards.append(torch.from_numpy(A[r0:r0 + rows]).cuda())
+    Bs.append(torch.from_numpy(B).cuda() if g == 0 else torch.empty((K, N), device="cuda"))
+    Cs.append(torch.full((M, N), float("nan"), device="cuda"))
+for rep in range(2):
+    giga.matmul_sharded(shards, Bs, Cs, M, N, K)
+    for g, C in enumerate(Cs):
+        C = C.cpu().numpy()
+        ok, st = check_exact(C, ref) if dist == "d3" else check_close(C, ref, S)
+        assert ok, (rep, g, st)
+giga.finalize()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("dist", ["d1", "d3"])
+def test_scheme_through_the_p2p_transport(dist):
+    """TF32 + BF16 forced on the peer-to-peer transport over 3 virtual GPUs of device 0:
+    K-chunked GEMMs accumulating, the last chunk's epilogue loading the local partial and
+    storing the final rows into every GPU's C_full (the fused gather), twice."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    penv = dict(os.environ, GIGA_SCHEME="tf32bf16", GIGA_TRANSPORT="p2p", PYTHONPATH=root,
+                CHILD_DIST=dist)
+    r = subprocess.run([sys.executable, "-c", _CHILD_P2P], env=penv, cwd=root,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
