@@ -102,6 +102,7 @@ int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M
       TRY(split(Ad + q0 * K, at(Alo, q0 * K), (q1 - q0) * K, d.compute));
       GemmExtra e2;
       e2.b_prep_reuse = q > 0;  // every late row block multiplies by the same full B
+      e2.rows_hint = M - Me;
       TRY(gemm_chunk(Ad + q0 * K, at(Alo, q0 * K), Bd, Blo, Cd + q0 * N, q1 - q0, N, K, e2,
                      d.compute));
     }

@@ -74,6 +74,9 @@ struct GemmExtra {
   // TF32 + BF16 scheme: 1 = B (same pointer, ldb, K, N) is unchanged since the previous launch
   // on this stream (row chunks of one product), so its prepared B_hi / B' are reused
   int b_prep_reuse = 0;
+  // rows that share this B (row blocks / row chunks of one product): the scheme choice
+  // amortises B's preparation over them (0 = this launch's M)
+  int64_t rows_hint = 0;
   const TermsPrep *prep = nullptr;  // terms = 2: operands already prepared by the caller
 };
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,

@@ -111,6 +111,7 @@ int rank_gemms(const Plan &plan, const GemmExtra &ex, int64_t M, int64_t N, int6
       plan_block(M, world, plan.pc, rank, q, &b0, &brows);
       const int64_t q0 = b0 - r0;  // offset inside this rank's shard
       e.b_prep_reuse = q > 0;  // the same B chunk for every row chunk
+      e.rows_hint = rows;
       if (brows > 0)
         TRY(gemm_chunk(A + q0 * K + kb[c], at(Alo, q0 * K + kb[c]), Bc, Bloc, Cs + q0 * N, brows,
                        N, Kc, e, st));

@@ -170,7 +170,7 @@ int split(const float *x, float *lo, int64_t n, cudaStream_t st) {
 int run_gemm(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
              int64_t M, int64_t N, int64_t K, int64_t ldc, const GemmExtra &ex,
              cudaStream_t st) {
-  const int terms = product_terms(Alo, M, N, K);
+  const int terms = product_terms(Alo, std::max(M, ex.rows_hint), N, K);
   GemmExtra e = ex;
   TermsPrep tp;
   if (terms == 2) {
