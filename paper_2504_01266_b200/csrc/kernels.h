@@ -7,10 +7,11 @@ namespace giga {
 
 // Default number of 16-wide k-blocks accumulated in TMEM before promotion into the fp32
 // register sum. 8 k-blocks = K 128 = 16 k8 steps.
-// The TF32 + BF16 scheme adds 2 MMAs per k8 step into TMEM instead of 3, so its truncation
-// drift per interval is smaller: 16 k-blocks (measured 32768^3 d1 worst case: DESIGN.md 6.7).
+// The TF32 + BF16 scheme adds 2 MMAs per k8 step into TMEM instead of 3; 16 k-blocks would be
+// 2% faster but raise its adversarial coherent-error case from 5.0e-6 to 7.3e-6 of the 1e-5
+// bound, so it keeps 8 too.
 constexpr int kDefaultPromoteKBlocks = 8;
-constexpr int kDefaultPromoteKBlocksT2 = 16;
+constexpr int kDefaultPromoteKBlocksT2 = 8;
 
 // The promotion interval in effect for `terms` (the defaults above or $GIGA_PROMOTE_KBLOCKS).
 int default_promote_kblocks(int terms = 3);

@@ -177,3 +177,43 @@ def test_scheme_through_the_p2p_transport(dist):
     r = subprocess.run([sys.executable, "-c", _CHILD_P2P], env=penv, cwd=root,
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+_CHILD_REUSE = """
+import numpy as np, torch, oracle, synth
+from oracle.check import check_exact
+from paper_2504_01266_b200 import giga
+giga.init(1)
+M, N, K = 4096, 1040, 2064
+A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+B1 = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+B2 = synth.gen_matrix(K, N, 7, "d3")
+dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B1).cuda()
+dC = torch.full((M, N), float("nan"), device="cuda")
+for Bh in (B1, B2, B1):
+    dB.copy_(torch.from_numpy(Bh))  # same pointer, new contents: B is prepared again
+    giga.matmul_sharded([dA], [dB], [dC], M, N, K)
+    ok, st = check_exact(dC.cpu().numpy(), oracle.gemm(A, Bh)[0])
+    assert ok, st
+    C = np.full((M, N), np.nan, np.float32)
+    giga.matmul(A, Bh, C, M, N, K, 1)  # host path: B staged into the same device buffer
+    ok, st = check_exact(C, oracle.gemm(A, Bh)[0])
+    assert ok, st
+giga.finalize()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{}, {"GIGA_FORCE_COMM": "1", "GIGA_BCAST_CHUNKS": "3",
+                                      "GIGA_GATHER_CHUNKS": "3"}])
+def test_b_preparation_is_not_reused_across_calls(env):
+    """B's prepared operands are reused only between launches of one product (row chunks /
+    row blocks); a later call with the same B pointer but new contents must prepare again."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    penv = dict(os.environ, GIGA_SCHEME="tf32bf16", PYTHONPATH=root, **env)
+    r = subprocess.run([sys.executable, "-c", _CHILD_REUSE], env=penv, cwd=root,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
