@@ -893,13 +893,20 @@ int default_promote_kblocks(int terms) {
   return terms == 2 ? kDefaultPromoteKBlocksT2 : kDefaultPromoteKBlocks;
 }
 
-int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K) {
+static int forced_scheme() {
   static const int forced = [] {
     const char *e = getenv("GIGA_SCHEME");
     if (e && strcmp(e, "3xtf32") == 0) return 3;
     if (e && strcmp(e, "tf32bf16") == 0) return 2;
     return 0;
   }();
+  return forced;
+}
+
+bool scheme_forced() { return forced_scheme() != 0; }
+
+int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K) {
+  const int forced = forced_scheme();
   if (A_lo) return 3;
   if (forced) return forced;
   // measured crossover (profiles/r01_scheme_crossover.jsonl, preparation included): TF32 + BF16

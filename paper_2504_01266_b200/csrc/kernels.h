@@ -23,6 +23,8 @@ int default_promote_kblocks(int terms = 3);
 // and M N K >= 2^37 (measured crossover); else 3. $GIGA_SCHEME = "3xtf32" / "tf32bf16" forces one. With pre-split
 // lo operands (A_lo != nullptr) the scheme is always 3.
 int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K);
+// true when $GIGA_SCHEME forces the scheme (measurements keep it even without scratch)
+bool scheme_forced();
 
 // lo = x - tf32(x) over n elements (HBM-bound elementwise split).
 cudaError_t launch_split_lo(const float *x, float *lo, int64_t n, cudaStream_t st);

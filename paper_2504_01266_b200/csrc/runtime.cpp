@@ -170,12 +170,18 @@ int split(const float *x, float *lo, int64_t n, cudaStream_t st) {
 int run_gemm(const float *A, const float *Alo, const float *B, const float *Blo, float *C,
              int64_t M, int64_t N, int64_t K, int64_t ldc, const GemmExtra &ex,
              cudaStream_t st) {
-  const int terms = product_terms(Alo, std::max(M, ex.rows_hint), N, K);
+  int terms = product_terms(Alo, std::max(M, ex.rows_hint), N, K);
   GemmExtra e = ex;
   TermsPrep tp;
   if (terms == 2) {
     const int64_t lda = e.lda ? e.lda : K, ldb = e.ldb ? e.ldb : N;
     CK(terms_prep_alloc(M, N, K, st, &tp));
+    // no scratch for the prepared operands (OOM, stream capture): 3xTF32, which builds its
+    // lo operands on chip and beats the on-chip TF32 + BF16 variant
+    if (!tp.Bhi && !scheme_forced()) terms = 3;
+  }
+  if (terms == 2) {
+    const int64_t lda = e.lda ? e.lda : K, ldb = e.ldb ? e.ldb : N;
     if (tp.Bhi && !(e.b_prep_reuse && tp.b_matches(B, ldb, N, K)))
       CK(timed(1, st, [&] { return launch_prep_b(B, ldb, N, K, &tp, st); }));
     if (tp.Ahi) CK(timed(1, st, [&] { return launch_prep_a(A, lda, M, K, &tp, st); }));
