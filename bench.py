@@ -361,6 +361,10 @@ def main():
                          f"achieved = {3 if terms == 3 else 2} x 2 x rows x N x K TF32-equivalent "
                          f"tensor flops per launch / event time",
             "scheme": "3xTF32" if terms == 3 else "TF32+BF16",
+            "limit_note": ("tensor pipe (3 TF32 MMAs per k8 step) at the power-capped clock"
+                           if terms == 3 else
+                           "operand feed (32 KiB of TMA fills per 2-MMA stage) and the power cap, "
+                           "not the MMAs: DESIGN.md 6.7"),
             "prep_ms_per_step": round(kt["split_ms"] / args.steps, 4),
             "prep_launches_per_step": round(kt["split_launches"] / args.steps, 2)}
 
