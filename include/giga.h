@@ -156,8 +156,11 @@ int giga_rank_init(int rank, int world, int device, const uint8_t id[128]);
  * A_shard: rows_r x K block (giga_partition(M, world, rank)); B: K x N (source on rank 0,
  * receive buffer elsewhere); C_full: M x N, holds the full C on return on every rank.
  * Work is enqueued on `stream` (a cudaStream_t, NULL = the library's stream) and the call
- * returns without synchronising the host (stream-ordered). Errors: NOT_INITIALIZED,
- * INVALID_ARG, CUDA, COMM. */
+ * returns without synchronising the host (stream-ordered). The call can be captured into a
+ * CUDA graph on `stream` after one eager call with the same shapes (which sizes the
+ * library's per-stream workspaces); inside a capture it does not order itself against
+ * earlier eager calls -- the graph's stream does. Errors: NOT_INITIALIZED, INVALID_ARG,
+ * CUDA, COMM. */
 int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, int64_t N,
                      int64_t K, void *stream);
 

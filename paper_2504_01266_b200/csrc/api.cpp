@@ -411,8 +411,13 @@ int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, i
   TRY(rank_comm_healthy());
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.compute;
   // calls share the rank's workspace: a call starts after the previous one, whatever the
-  // caller's streams
-  if (d.has_last) CK(cudaStreamWaitEvent(st, d.ev_last, 0));
+  // caller's streams. Inside a CUDA-graph capture an event recorded outside it cannot be
+  // waited on: the graph's stream orders its replays, and the caller orders the graph
+  // against eager calls.
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(st, &cs));
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
+  if (d.has_last && !capturing) CK(cudaStreamWaitEvent(st, d.ev_last, 0));
   int rc;
   if (g.p2p.ready && transport_p2p()) {
     rc = run_p2p_rank(d, st, A_shard, B, C_full, M, N, K);
@@ -423,8 +428,10 @@ int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, i
     rc = run_pipeline(parts, g.world, M, N, K);
   }
   TRY(rc);
-  CK(cudaEventRecord(d.ev_last, st));
-  d.has_last = true;
+  if (!capturing) {
+    CK(cudaEventRecord(d.ev_last, st));
+    d.has_last = true;
+  }
   return GIGA_OK;
 }
 

@@ -217,3 +217,43 @@ def test_b_preparation_is_not_reused_across_calls(env):
     r = subprocess.run([sys.executable, "-c", _CHILD_REUSE], env=penv, cwd=root,
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("M,N,K", [(8192, 8192, 2048), (1536, 1040, 1028)])
+def test_rank_api_in_a_cuda_graph(torch_cuda, M, N, K):
+    """giga_matmul_rank is stream-ordered, so a step can be captured into a CUDA graph and
+    replayed (launch-bound inner loops). One eager call first sizes the library's per-stream
+    workspaces; the captured launches then reuse them (8192 x 8192 x 2048 runs the prepared
+    TF32 + BF16 scheme, 1536 x 1040 x 1028 3xTF32). Replays with new A contents: bit-exact."""
+    torch = torch_cuda
+    from paper_2504_01266_b200 import giga as g
+    g.finalize()
+    g.rank_init(0, 1, 0, None)
+    try:
+        B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+        dB = torch.from_numpy(B).cuda()
+        dA = torch.empty((M, K), device="cuda")
+        dC = torch.full((M, N), float("nan"), device="cuda")
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        A0 = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+        dA.copy_(torch.from_numpy(A0))
+        torch.cuda.synchronize()
+        g.matmul_rank(dA, dB, dC, M, N, K, stream=s)  # eager: workspaces sized
+        s.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            g.matmul_rank(dA, dB, dC, M, N, K, stream=s)
+        rows = np.array(sorted({0, M - 1, M // 2} | set(range(1, M, max(1, M // 61)))))
+        for seed in (3, 5):
+            A = synth.gen_matrix(M, K, seed, "d3")
+            dA.copy_(torch.from_numpy(A))
+            dC.fill_(float("nan"))
+            torch.cuda.synchronize()
+            graph.replay()
+            torch.cuda.synchronize()
+            ok, st = check_exact(dC.cpu().numpy()[rows], oracle.gemm(A[rows], B)[0])
+            assert ok, (seed, st)
+            assert not torch.isnan(dC).any().item()
+    finally:
+        g.finalize()
