@@ -908,6 +908,7 @@ bool scheme_forced() { return forced_scheme() != 0; }
 int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K) {
   const int forced = forced_scheme();
   if (A_lo) return 3;
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return 3;  // the launch rejects these
   if (forced) return forced;
   // measured crossover (profiles/r01_scheme_crossover.jsonl, preparation included): TF32 + BF16
   // wins 2-11% from 8192 x 8192 x 2048 and 4096 x 32768^2 up, loses 2% at 4096^3
