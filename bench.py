@@ -363,7 +363,8 @@ def main():
             "scheme": "3xTF32" if terms == 3 else "TF32+BF16",
             "limit_note": ("tensor pipe (3 TF32 MMAs per k8 step) at the power-capped clock"
                            if terms == 3 else
-                           "operand feed (32 KiB of TMA fills per 2-MMA stage) and the power cap, "
+                           "operand feed: 32 KiB of TMA fills per CTA per 2-MMA stage against the "
+                           "measured per-SM TMA fill ceiling (roofline.feed), and the power cap; "
                            "not the MMAs: DESIGN.md 6.7"),
             "prep_ms_per_step": round(kt["split_ms"] / args.steps, 4),
             "prep_launches_per_step": round(kt["split_launches"] / args.steps, 2)}
@@ -380,6 +381,31 @@ def main():
                  "t_comp_ms": round(t_comp * 1e3, 4), "t_comm_ms": round(t_comm * 1e3, 4),
                  "bound": "tensor" if t_comp >= t_comm else "nvlink",
                  "frac": round(t_roof / (ms_step * 1e-3), 4)}
+    if terms == 2:
+        # the prepared TF32 + BF16 kernel is bound by its TMA operand feed: 64 KiB of fills
+        # per 256 x 256 pair tile and 16-deep k-block = rows N K / 16 bytes per launch, against
+        # the measured L2 -> SM TMA fill ceiling (scripts/tma_box_bench.cu: 10.7 TB/s on a
+        # 148-SM B200 for every box shape; profiles/r01_tma_box_bench.jsonl)
+        feed_bytes = rows * N * K / 16.0
+        feed_ach = feed_bytes / (gemm_ms * 1e-3) / 1e9 if gemm_ms > 0 else None
+        roof["feed"] = {"bound": "l2_to_smem_tma", "achieved": round(feed_ach, 1) if feed_ach else None,
+                        "peak": 10714.0, "unit": "GB/s",
+                        "frac": round(feed_ach / 10714.0, 4) if feed_ach else None,
+                        "bytes_per_launch": feed_bytes,
+                        "peak_source": "measured TMA fill ceiling, scripts/tma_box_bench.cu"}
+    if terms == 2:
+        # the prepared TF32 + BF16 kernel is bound by its TMA operand feed: 64 KiB of fills
+        # per 256 x 256 pair tile and 16-deep k-block = rows N K / 16 bytes per launch, against
+        # the measured L2 -> SM TMA fill ceiling (scripts/tma_box_bench.cu: 10.7 TB/s on a
+        # 148-SM B200 for every box shape; profiles/r01_tma_box_bench.jsonl)
+        feed_bytes = rows * N * K / 16.0
+        feed_ach = feed_bytes / (gemm_ms * 1e-3) / 1e9 if gemm_ms > 0 else None
+        roof["feed"] = {"bound": "l2_to_smem_tma",
+                        "achieved": round(feed_ach, 1) if feed_ach else None,
+                        "peak": 10714.0, "unit": "GB/s",
+                        "frac": round(feed_ach / 10714.0, 4) if feed_ach else None,
+                        "bytes_per_launch": feed_bytes,
+                        "peak_source": "measured TMA fill ceiling, scripts/tma_box_bench.cu"}
     if terms == 2:  # the scheme's own ceiling: 2 TF32-instruction-equivalents per product
         t_comp2 = 2.0 * max(rows_all) * N * K / (tf32_burst * 1e12 / 2)
         step_roof["scheme_note"] = ("the north_star's T_comp assumes 3xTF32 (P_tf32/3); the "
