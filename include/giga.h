@@ -296,8 +296,8 @@ int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *ou
  * a_hi*b_hi as one kind::tf32 MMA plus a_lo*b + a_hi*b_lo as one K=16 kind::f16 MMA, with
  * hi = RN tf32(x); A_hi, A', B_hi, B' prepared once per launch in library-owned HBM scratch
  * by two elementwise kernels; per-product split error <= 2^-18 |a||b|). 2 when M >= 4096,
- * N >= 8192, K >= 2048 and M N K >= 2^37 (the preparation is then amortised: measured
- * crossover), else 3;
+ * N >= 8192 and either K >= 2048 with M N K >= 2^37 or K >= 512 with M N K >= 2^38 (the
+ * preparation is then amortised: measured crossover), else 3;
  * $GIGA_SCHEME = 3xtf32 | tf32bf16 forces one. Errors: INVALID_ARG. */
 int giga_product_scheme(int64_t M, int64_t N, int64_t K, int *terms);
 

@@ -910,9 +910,13 @@ int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K) {
   if (A_lo) return 3;
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return 3;  // the launch rejects these
   if (forced) return forced;
-  // measured crossover (profiles/r01_scheme_crossover.jsonl, preparation included): TF32 + BF16
-  // wins 2-11% from 8192 x 8192 x 2048 and 4096 x 32768^2 up, loses 2% at 4096^3
-  return (M >= 4096 && N >= 8192 && K >= 2048 && double(M) * double(N) * double(K) >= 0x1p37)
+  // measured crossover (profiles/r01_scheme_crossover.jsonl, r01_kchunk_crossover.jsonl;
+  // preparation included): TF32 + BF16 wins 2-11% from 8192 x 8192 x 2048 and 4096 x 32768^2
+  // up and 3-10% on 16384 x 32768 x (576..1792) (the host schedule's K-chunks); it ties at
+  // 8192 x 16384 x 1024 and loses 2-5% at 4096^3 and 4096 x 32768 x 768
+  const double mnk = double(M) * double(N) * double(K);
+  return (M >= 4096 && N >= 8192 &&
+          ((K >= 2048 && mnk >= 0x1p37) || (K >= 512 && mnk >= 0x1p38)))
              ? 2
              : 3;
 }

@@ -19,8 +19,8 @@ int default_promote_kblocks(int terms = 3);
 // The product path's fp32-accurate scheme for an M x N x K launch: 3 = 3xTF32
 // (three kind::tf32 MMAs per k8 step), 2 = TF32 + BF16 (hi*hi as kind::tf32, both corrections
 // as one K=16 kind::f16 MMA, operands prepared once per launch in HBM). 2 where the operand
-// preparation (~12 B per element of A and B) is amortised: M >= 4096, N >= 8192, K >= 2048
-// and M N K >= 2^37 (measured crossover); else 3. $GIGA_SCHEME = "3xtf32" / "tf32bf16" forces one. With pre-split
+// preparation (~12 B per element of A and B) is amortised: M >= 4096, N >= 8192 and either
+// K >= 2048 with M N K >= 2^37 or K >= 512 with M N K >= 2^38 (measured crossover); else 3. $GIGA_SCHEME = "3xtf32" / "tf32bf16" forces one. With pre-split
 // lo operands (A_lo != nullptr) the scheme is always 3.
 int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K);
 // true when $GIGA_SCHEME forces the scheme (measurements keep it even without scratch)

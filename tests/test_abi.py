@@ -88,10 +88,11 @@ def test_product_scheme_selection():
     preparation is amortised; 3xTF32 for the small and the skinny configs."""
     from paper_2504_01266_b200 import giga
     for shape in [(16384, 16384, 16384), (32768, 32768, 32768), (4096, 32768, 32768),
-                  (8192, 8192, 2048)]:
+                  (8192, 8192, 2048), (16384, 32768, 576)]:
         assert giga.product_scheme(*shape) == 2, shape
     for shape in [(512, 512, 512), (4096, 4096, 4096), (262144, 1024, 1024),
-                  (2048, 16384, 16384), (16384, 16384, 1024), (65536, 4096, 4096)]:
+                  (2048, 16384, 16384), (16384, 16384, 256), (65536, 4096, 4096),
+                  (8192, 16384, 1024), (4096, 32768, 768)]:
         assert giga.product_scheme(*shape) == 3, shape
     with pytest.raises(Exception):
         giga.product_scheme(0, 4, 4)
