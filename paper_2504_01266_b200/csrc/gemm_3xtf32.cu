@@ -13,6 +13,12 @@
 //     tcgen05.mma.kind::tf32 are issued into one TMEM accumulator, small terms first:
 //     a_lo*b_hi, a_hi*b_lo, a_hi*b_hi (a_lo*b_lo, ~2^-20 relative, is dropped). hi is never
 //     materialised: the MMA is fed the raw fp32 tile and reads only its TF32 part.
+//   * terms = 2, TF32 + BF16 (the product scheme for large launches): hi = RN
+//     tf32(x); a_hi*b_hi is one kind::tf32 MMA and a_lo*b + a_hi*b_lo ONE K=16 kind::f16 MMA
+//     over bf16 operands concatenated along K (2 MMA times per k8 step instead of 3). The
+//     operands come prepared from HBM (prep_b_kernel / prep_a_kernel, once per launch) and the
+//     MMA waits on the TMA barrier directly ("direct" mode, no transform work); the on-chip
+//     variants (xform_tf32_bf16) remain for measurements and the no-scratch case.
 //   * Accumulator promotion: the tensor core's fp32 accumulation truncates (measured,
 //     tests/test_gpu.py::test_probe_accumulation_rounding), so every `p_kb` k-blocks the
 //     MMA issuer switches to the other of two TMEM accumulators and the epilogue warps add
