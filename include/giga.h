@@ -34,8 +34,8 @@
  *
  * Ownership: the caller owns every pointer passed in; the library never keeps a caller
  * pointer after returning. The library owns its streams, events, communicators and
- * workspace (padded copies, host-path staging buffers, the pre-split low parts in that
- * comparison mode), freed in giga_finalize().
+ * workspace (padded copies, host-path staging buffers, the TF32 + BF16 prepared operands,
+ * the pre-split low parts in that comparison mode), freed in giga_finalize().
  *
  * Threading: calls are serialised by an internal mutex (one call at a time per process).
  *
