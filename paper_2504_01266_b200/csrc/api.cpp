@@ -282,6 +282,9 @@ int giga_finalize(void) {
     for (auto &p : g_tpool) cudaEventDestroy(p.second);
     g_tpool.clear();
   }
+  g.rank_p2p = false;
+  g.rank = 0;
+  g.world = 1;
   g.mode = 0;
   return GIGA_OK;
 }
@@ -393,6 +396,7 @@ int giga_rank_init(int rank, int world, int device, const uint8_t id[128]) {
   }
   g.rank = rank;
   g.world = world;
+  g.rank_p2p = transport_p2p() && world > 1;
   g.mode = 2;
   return GIGA_OK;
 }
@@ -417,9 +421,24 @@ int giga_matmul_rank(const float *A_shard, float *B, float *C_full, int64_t M, i
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   CK(cudaStreamIsCapturing(st, &cs));
   const bool capturing = cs != cudaStreamCaptureStatusNone;
+  // the transport was fixed at giga_rank_init; a world > 1 without a communicator or a p2p
+  // registration would silently compute only this rank's rows
+  if (g.world > 1 && !g.rank_comm && !(g.rank_p2p && g.p2p.ready))
+    return g.rank_p2p ? fail(GIGA_ERR_NOT_INITIALIZED,
+                             "giga_matmul_rank: p2p transport needs giga_rank_p2p_export/import")
+                      : fail(GIGA_ERR_NOT_INITIALIZED,
+                             "giga_matmul_rank: no communicator for world %d", g.world);
+  if (capturing) {
+    // the p2p flag protocol bakes the call number into the captured waits and writes, so
+    // replays would not order themselves across processes
+    if (g.rank_p2p)
+      return fail(GIGA_ERR_UNSUPPORTED,
+                  "giga_matmul_rank: CUDA-graph capture is not supported with the p2p transport");
+    keep_superseded_buffers();  // the graph keeps workspace pointers: never free them early
+  }
   if (d.has_last && !capturing) CK(cudaStreamWaitEvent(st, d.ev_last, 0));
   int rc;
-  if (g.p2p.ready && transport_p2p()) {
+  if (g.rank_p2p) {
     rc = run_p2p_rank(d, st, A_shard, B, C_full, M, N, K);
   } else if (!g.rank_comm) {
     rc = shard_compute(d, st, A_shard, rows, B, C_full + r0 * N, N, N, K, nullptr);
@@ -512,8 +531,11 @@ int giga_dot_rank(const float *x_shard, const float *y_shard, int64_t n, double 
   CK(cudaSetDevice(d.dev));
   TRY(rank_comm_healthy());
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.compute;
+  if (g.world > 1 && !g.rank_comm && !(g.rank_p2p && g.p2p.ready))
+    return fail(GIGA_ERR_NOT_INITIALIZED, "giga_dot_rank: no communicator / p2p registration "
+                "for world %d", g.world);
   TRY(dot_partial(d, x_shard, y_shard, rows, st));
-  if (g.p2p.ready && g.world > 1) return p2p_dot_allreduce(d, st, result);
+  if (g.rank_p2p) return p2p_dot_allreduce(d, st, result);
   if (g.rank_comm) {  // every rank gets the sum of the partials
     const NcclApi *api = nccl_api(nullptr);
     TRY(nccl_check(api->AllReduce(vec_out(d), vec_out(d), 1, ncclFloat64, ncclSum, g.rank_comm,

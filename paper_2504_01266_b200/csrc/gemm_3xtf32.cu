@@ -1060,6 +1060,28 @@ struct KSplitWs {
 static std::mutex g_ksplit_mu;
 static std::vector<std::pair<cudaStream_t, KSplitWs>> g_ksplit;
 
+// Superseded buffers kept alive for captured graphs (retire_buffer).
+static std::mutex g_retire_mu;
+static bool g_keep_superseded = false;
+static std::vector<std::pair<int, void *>> g_retired;
+
+void keep_superseded_buffers() {
+  std::lock_guard<std::mutex> lk(g_retire_mu);
+  g_keep_superseded = true;
+}
+
+void retire_buffer(void *p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_retire_mu);
+  if (!g_keep_superseded) {
+    cudaFree(p);
+    return;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  g_retired.push_back({dev, p});
+}
+
 bool ksplit_workspace(cudaStream_t st, size_t ws_bytes, size_t cnt_n, float **ws,
                       unsigned **cnt) {
   int dev = 0;
@@ -1089,8 +1111,8 @@ bool ksplit_workspace(cudaStream_t st, size_t ws_bytes, size_t cnt_n, float **ws
       return false;
     }
     if (w) {
-      cudaFree(w->ws);
-      cudaFree(w->cnt);
+      retire_buffer(w->ws);
+      retire_buffer(w->cnt);
       *w = fresh;
     } else {
       g_ksplit.push_back({st, fresh});
@@ -1128,7 +1150,7 @@ static ScratchBuf *bpre_scratch(cudaStream_t st, size_t bytes) {
   if (cudaStreamSynchronize(st) != cudaSuccess) return nullptr;
   for (auto it = g_bpre.begin(); it != g_bpre.end(); ++it)
     if (it->st == st && it->dev == dev) {
-      cudaFree(it->p);
+      retire_buffer(it->p);
       g_bpre.erase(it);
       break;
     }
@@ -1156,6 +1178,14 @@ void release_gemm_caches() {
     cudaFree(e.second.cnt);
   }
   g_ksplit.clear();
+  std::lock_guard<std::mutex> lr(g_retire_mu);
+  for (auto &r : g_retired) {
+    cudaSetDevice(r.first);
+    cudaDeviceSynchronize();
+    cudaFree(r.second);
+  }
+  g_retired.clear();
+  g_keep_superseded = false;
 }
 
 GemmSchedule gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int cta_group,

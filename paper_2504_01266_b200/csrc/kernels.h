@@ -117,6 +117,11 @@ bool ksplit_workspace(cudaStream_t st, size_t ws_bytes, size_t cnt_n, float **ws
                       unsigned **cnt);
 // Frees the K-split workspaces of every device (giga_finalize).
 void release_gemm_caches();
+// A library buffer superseded by a larger one (workspace growth): freed at once, unless a
+// CUDA graph has captured library work (keep_superseded_buffers()), in which case it stays
+// allocated until giga_finalize -- an earlier graph may still reference it.
+void retire_buffer(void *p);
+void keep_superseded_buffers();
 
 // Resolves cuTensorMapEncodeTiled through the runtime (no libcuda link). 0 on success.
 int ensure_tma_encoder();

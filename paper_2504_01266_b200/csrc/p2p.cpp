@@ -130,8 +130,12 @@ int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K, bool gath
 //             overwriting its own chunk c, pulled[c] >= s-1 (downstream finished reading it in
 //             call s-1); copies the chunk from upstream's B; marks upstream's pulled[c] = s and
 //             downstream's ready[c] = s.
-//   C:        the GEMM epilogue writes this rank's rows into every peer's C_full; then
-//             cdone[r] = s in every peer's page, and this rank waits cdone[q] >= s for all q.
+//   C:        at the start of call s every rank writes started[r] = s into every peer's
+//             page on its own stream -- ordered after whatever the caller queued there before
+//             the call, i.e. after its consumers of call s-1's C_full. The GEMM that stores
+//             into the peers' C_full (the last K-chunk's) first waits started[q] >= s for
+//             every peer q, so no rank overwrites a C_full its owner may still be reading.
+//             Then cdone[r] = s in every peer's page, and this rank waits cdone[q] >= s.
 
 const DrvApi *drv_api() {
   static DrvApi api;
@@ -159,6 +163,7 @@ uint32_t *flag_ready(uint32_t *page, int c) { return page + c; }
 uint32_t *flag_pulled(uint32_t *page, int c) { return page + 16 + c; }
 uint32_t *flag_cdone(uint32_t *page, int q) { return page + 32 + q; }
 uint32_t *flag_dotdone(uint32_t *page, int q) { return page + 96 + q; }
+uint32_t *flag_started(uint32_t *page, int q) { return page + 160 + q; }
 // two slot sets by call parity: a peer can run at most one call ahead of this rank
 double *dot_part(uint32_t *page, int q, uint32_t s) {
   return reinterpret_cast<double *>(page + 256) + (s & 1) * 64 + q;
@@ -201,6 +206,9 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
   tr.meta("world", world);
   tr.meta("kchunks", plan.pb);
   TRY(tr.start(st));
+  // "my C_full is free for call s": after the caller's earlier work on st
+  for (int q = 0; q < world; ++q)
+    if (q != r) TRY(write_flag(st, flag_started(x.peerF[q], r), s));
   CK(cudaEventRecord(d.ev_start, st));
   CK(cudaStreamWaitEvent(d.comm, d.ev_start, 0));
   TRY(ws_reserve(d, {{&d.A_lo, lo_bytes(std::max<int64_t>(rows, 1) * K)},
@@ -235,6 +243,9 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
     CK(cudaStreamWaitEvent(st, d.ev_kchunk[c], 0));
     TRY(split(B + plan.kb[c] * N, lo_at(d.B_lo, plan.kb[c] * N), Kc * N, st));
     if (rows == 0) continue;
+    if (c == plan.pb - 1)  // this GEMM writes into the peers' C_full: they must have started s
+      for (int q = 0; q < world; ++q)
+        if (q != r) TRY(wait_flag(st, flag_started(x.flags, q), s));
     TRY(gemm_chunk(A + plan.kb[c], lo_at(d.A_lo, plan.kb[c]), B + plan.kb[c] * N,
                    lo_at(d.B_lo, plan.kb[c] * N), C + r0 * N, rows, N, Kc,
                    chunk_extra(ex, c, plan.pb), st));

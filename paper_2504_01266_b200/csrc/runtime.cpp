@@ -80,7 +80,7 @@ int ws_reserve(DevCtx & /*d: the buffers carry their device*/,
     size_t want = 0;
     for (auto &r : req)
       if (r.first == f.first) want = std::max(want, r.second);
-    if (f.first->p) cudaFree(f.first->p);
+    retire_buffer(f.first->p);  // freed now, or at finalize once a graph has captured work
     f.first->p = f.second;
     f.first->bytes = want;
   }

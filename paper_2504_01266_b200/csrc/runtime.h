@@ -72,7 +72,8 @@ struct DevCtx {
 // peers' buffers and flag pages mapped through CUDA IPC (index = rank).
 // Flag page (device memory, u32 unless noted): ready[c] @0 (upstream has B chunk c),
 // pulled[c] @64 (downstream finished reading my chunk c), cdone[q] @128 (rank q wrote its C
-// rows into my C_full), dotdone[q] @384, dot partials (fp64) @1024. Values are call numbers.
+// rows into my C_full), dotdone[q] @384, started[q] @640 (rank q began call s: its C_full may
+// be written), dot partials (fp64) @1024. Values are call numbers.
 constexpr size_t kFlagBytes = 4096;
 struct RankP2P {
   bool ready = false;
@@ -91,6 +92,7 @@ struct State {
   std::map<int, std::vector<ncclComm_t>> comms;  // single-process: ngpus -> comms
   ncclComm_t rank_comm = nullptr;
   int rank = 0, world = 1;
+  bool rank_p2p = false;  // rank mode: $GIGA_TRANSPORT=p2p when giga_rank_init ran (fixed then)
   RankP2P p2p;
 };
 extern State g;
@@ -261,6 +263,7 @@ uint32_t *flag_ready(uint32_t *page, int c);
 uint32_t *flag_pulled(uint32_t *page, int c);
 uint32_t *flag_cdone(uint32_t *page, int q);
 uint32_t *flag_dotdone(uint32_t *page, int q);
+uint32_t *flag_started(uint32_t *page, int q);
 double *dot_part(uint32_t *page, int q, uint32_t s);
 int wait_flag(cudaStream_t st, uint32_t *addr, uint32_t v);
 int write_flag(cudaStream_t st, uint32_t *addr, uint32_t v);

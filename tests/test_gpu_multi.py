@@ -184,6 +184,114 @@ def test_rank_p2p_across_processes(torch_cuda, world, M, N, K):
         assert ok_c and ok_b and ok_d, (rank, ok_c, ok_b, ok_d, err)
 
 
+def _rank_worker_changing(rank, world, port, M, N, K, q):
+    """Inputs change on every call and each rank reads its C_full between calls on its own
+    stream; rank 1 reads late (a long sleep first). Without the started[] flags of the p2p
+    transport, rank 0's next call writes its rows into rank 1's C_full before rank 1 has read
+    the previous result."""
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ.update({"GIGA_TRANSPORT": "p2p", "GIGA_BCAST_CHUNKS": "3",
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    try:
+        import torch
+        import torch.distributed as dist
+        import oracle
+        import synth
+        from paper_2504_01266_b200 import giga
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        giga.rank_init(rank, world, 0, None)
+        r0, rows = giga.partition(M, world, rank)
+        dA = torch.empty((max(rows, 1), K), device="cuda")
+        dB = torch.full((K, N), float("nan"), device="cuda")
+        dC = torch.full((M, N), float("nan"), device="cuda")
+        blobs = [None] * world
+        dist.all_gather_object(blobs, giga.p2p_export(dB, dC))
+        giga.p2p_import(blobs)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        calls = 4
+        As = [synth.gen_matrix(M, K, 10 + c, "d3") for c in range(calls)]
+        Bs = [synth.gen_matrix(K, N, 20 + c, "d3") for c in range(calls)]
+        snaps = []
+        with torch.cuda.stream(s):
+            for c in range(calls):
+                dA[:rows].copy_(torch.from_numpy(As[c][r0:r0 + rows]))
+                if rank == 0:
+                    dB.copy_(torch.from_numpy(Bs[c]))
+                giga.matmul_rank(dA, dB, dC, M, N, K, stream=s)
+                if rank == 1:
+                    torch.cuda._sleep(200_000_000)  # a slow consumer of call c's C_full
+                snaps.append(dC.clone())
+        s.synchronize()
+        ok = []
+        for c in range(calls):
+            Cref, _ = oracle.gemm(As[c], Bs[c])
+            ok.append(bool(np.array_equal(snaps[c].cpu().numpy().astype(np.float64), Cref)))
+        dist.barrier()
+        giga.finalize()
+        q.put((rank, all(ok), str(ok)))
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, False, repr(e)))
+
+
+def test_rank_p2p_changing_inputs_slow_consumer(torch_cuda):
+    import socket
+    import torch.multiprocessing as mp
+    world, M, N, K = 2, 1024, 512, 1040
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_worker_changing, args=(r, world, port, M, N, K, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        res = sorted(q.get(timeout=240) for _ in range(world))
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for rank, ok, detail in res:
+        assert ok, (rank, detail)
+
+
+def test_rank_p2p_without_registration_refuses(torch_cuda, monkeypatch):
+    """world > 1 over the p2p transport but no giga_rank_p2p_export / import: the call must
+    fail, not compute only this rank's rows; the dot likewise."""
+    torch = torch_cuda
+    from paper_2504_01266_b200 import giga
+    monkeypatch.setenv("GIGA_TRANSPORT", "p2p")
+    giga.finalize()
+    giga.rank_init(0, 2, 0, None)
+    try:
+        M, N, K = 512, 256, 256
+        dA = torch.ones((256, K), device="cuda")
+        dB = torch.ones((K, N), device="cuda")
+        dC = torch.zeros((M, N), device="cuda")
+        with pytest.raises(giga.GigaError) as e:
+            giga.matmul_rank(dA, dB, dC, M, N, K)
+        assert e.value.status == "GIGA_ERR_NOT_INITIALIZED"
+        x = torch.ones(100, device="cuda")
+        with pytest.raises(giga.GigaError) as e:
+            giga.dot_rank(x, x, 200)
+        assert e.value.status == "GIGA_ERR_NOT_INITIALIZED"
+        # the transport is fixed at rank_init: changing the variable later changes nothing
+        monkeypatch.setenv("GIGA_TRANSPORT", "nccl")
+        with pytest.raises(giga.GigaError) as e:
+            giga.matmul_rank(dA, dB, dC, M, N, K)
+        assert e.value.status == "GIGA_ERR_NOT_INITIALIZED"
+    finally:
+        giga.finalize()
+
+
 def test_bench_two_ranks_on_one_device(torch_cuda):
     """bench.py's N > 1 path end to end under torchrun (2 ranks sharing cuda:0, gloo plumbing,
     p2p transport): rank init, IPC registration, max-over-ranks timing, one JSON line."""

@@ -257,3 +257,49 @@ def test_rank_api_in_a_cuda_graph(torch_cuda, M, N, K):
             assert not torch.isnan(dC).any().item()
     finally:
         g.finalize()
+
+
+def test_graph_survives_workspace_growth(torch_cuda):
+    """A graph captured at one shape keeps raw pointers to the per-stream workspaces (TF32 +
+    BF16 prepared operands); a later eager call with a larger shape on the same stream grows
+    them. The superseded buffers must stay allocated until giga_finalize, so
+    replaying the older graph is still correct (the freed memory is scribbled over first)."""
+    torch = torch_cuda
+    from paper_2504_01266_b200 import giga as g
+    g.finalize()
+    g.rank_init(0, 1, 0, None)
+    try:
+        M, N, K = 8192, 8192, 2048
+        B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+        dB = torch.from_numpy(B).cuda()
+        A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
+        dA = torch.from_numpy(A).cuda()
+        dC = torch.full((M, N), float("nan"), device="cuda")
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        g.matmul_rank(dA, dB, dC, M, N, K, stream=s)
+        s.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            g.matmul_rank(dA, dB, dC, M, N, K, stream=s)
+        # a larger product on the same stream grows the prepared-operand scratch
+        M2, K2 = 12288, 4096
+        dA2 = torch.ones((M2, K2), device="cuda")
+        dB2 = torch.ones((K2, N), device="cuda")
+        dC2 = torch.empty((M2, N), device="cuda")
+        g.matmul_rank(dA2, dB2, dC2, M2, N, K2, stream=s)
+        s.synchronize()
+        assert float(dC2[0, 0]) == K2
+        junk = torch.full((3 << 30,), 7.0, device="cuda")  # reuse any freed memory
+        torch.cuda.synchronize()
+        dC.fill_(float("nan"))
+        torch.cuda.synchronize()
+        graph.replay()
+        torch.cuda.synchronize()
+        del junk
+        rows = np.array(sorted({0, M - 1} | set(range(1, M, 97))))
+        ok, st = check_exact(dC.cpu().numpy()[rows], oracle.gemm(A[rows], B)[0])
+        assert ok, st
+    finally:
+        g.finalize()
