@@ -6,8 +6,9 @@
     python bench.py --workload dot [--n 67108864]             (the N3 dot product, GB/s)
 
 One step = the whole hot path over one synthetic problem: broadcast B from
-rank 0 (N > 1), the 3xTF32 tcgen05 shard GEMM (the TF32 hi/lo split happens on chip, inside
-the GEMM), gather the C row blocks on every rank. Default workload: M = N = K = 32768 (BASELINE.json configs[4], the
+rank 0 (N > 1), the fp32-accurate tcgen05 shard GEMM (3xTF32 with the hi/lo split on chip,
+or for large launches TF32 + BF16 with its operands prepared in HBM: giga_product_scheme),
+gather the C row blocks on every rank. Default workload: M = N = K = 32768 (BASELINE.json configs[4], the
 problem the north_star's targets are quoted on), strong scaling (the same problem split over
 N GPUs); --config picks the others. Inputs are seeded synthetic fp32 (synth "d2", U[-1,1)),
 resident in HBM before the timed region; each step is bracketed by CUDA events and the L2 is
@@ -140,6 +141,71 @@ def oracle_sample(M, N, K, dist, budget_s, threads):
     return {"rows": rows, "seconds": t, "tflops": 2.0 * rows * N * K / t / 1e12}
 
 
+def rank_launches(giga, M, N, K, world, rank):
+    """(rows, K depth, terms) of every GEMM launch rank `rank` issues in one step, as the
+    library plans them: world 1 one launch; the NCCL pipeline one launch per K-chunk of
+    giga_pipeline_plan over the rank's rows, the last K-chunk in row chunks (scheme chosen on
+    the rank's rows, the row chunks share B's preparation); the p2p transport one launch per
+    K-chunk over the rank's rows."""
+    r0, rows = giga.partition(M, world, rank)
+    if world == 1:
+        return [(M, K, giga.product_scheme(M, N, K))]
+    kb, rc = giga.pipeline_plan(M, N, K, world)
+    out = []
+    p2p = os.environ.get("GIGA_TRANSPORT") == "p2p"
+    for c in range(len(kb) - 1):
+        kc = kb[c + 1] - kb[c]
+        if rows == 0:
+            continue
+        terms = giga.product_scheme(rows, N, kc)
+        if c < len(kb) - 2 or p2p:
+            out.append((rows, kc, terms))
+            continue
+        for q in range(rc):
+            _, brows = giga.plan_block(M, world, rc, rank, q)
+            if brows > 0:
+                out.append((brows, kc, terms))
+    return out
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(M, N, K, args, world):
+    """The oracle, as it stands, on the host cores (SURVEY 8(d) "oracle timing beside it"):
+    a bounded row sample of this workload with every usable core, its extrapolation to the
+    whole product (labelled as such), and the 1-thread time of c1 512^3 (the config note's
+    "about a second")."""
+    import numpy as np
+    import oracle
+    import synth
+    threads = len(os.sched_getaffinity(0))
+    try:
+        r = oracle_sample(M, N, K, args.dist, args.cpu_budget, threads)
+        a1 = synth.gen_matrix(512, 512, synth.MATRIX_A, args.dist)
+        b1 = synth.gen_matrix(512, 512, synth.MATRIX_B, args.dist)
+        t0 = time.perf_counter()
+        oracle.gemm(a1, b1, nthreads=1)
+        c1_1t = time.perf_counter() - t0
+        del np
+        return {"value": round(r["tflops"], 6), "unit": "TFLOP/s", "cores": threads,
+                "kind": "oracle", "cpu_model": cpu_model(), "n_gpus_of_this_run": world,
+                "sample": f"first {r['rows']} rows of C (of {M}), full N={N}, K={K}: "
+                          f"{r['seconds']:.1f} s fp64 i-k-j C triple loop",
+                "full_product_s_extrapolated": round(r["seconds"] * M / r["rows"], 3),
+                "c1_512cubed_1thread_s": round(c1_1t, 3)}
+    except Exception as ex:  # noqa: BLE001
+        return {"value": None, "error": repr(ex)[:300]}
+
+
 def run_reference(args):
     """--impl reference: the CPU fp64 oracle on the host cores, same config and metric."""
     world, rank, _ = dist_env()
@@ -162,9 +228,12 @@ def run_reference(args):
         "data": "synthetic", "config": {"workload": f"{args.config} M={M} N={N} K={K}",
                                         "dist": args.dist},
         "cpu_baseline": {"value": round(tflops, 6), "unit": "TFLOP/s", "cores": threads,
-                         "kind": "oracle",
+                         "kind": "oracle", "cpu_model": cpu_model(),
                          "sample": f"first {vals[0]['rows']} rows of C per step "
-                                   f"(of {M}), full N and K; fp64 i-k-j C triple loop"},
+                                   f"(of {M}), full N and K; fp64 i-k-j C triple loop",
+                         "full_product_s_extrapolated": round(
+                             statistics.median(v["seconds"] for v in vals) * M
+                             / vals[0]["rows"], 3)},
         "e2e": {"value": round(tflops, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -316,101 +385,105 @@ def main():
     wall_ms = (time.perf_counter() - w0) * 1e3  # host upper bound (includes the L2 flushes)
     barrier()
     clk = clocks.stop()
-    ms_total = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     kt = giga.timing_read()
     giga.timing_enable(False)
-    if pg is not None:
-        t = torch.tensor([ms_total], dtype=torch.float64, device=red_dev)
+    if pg is not None:  # per step, the slowest rank's time
+        t = torch.tensor(step_ms, dtype=torch.float64, device=red_dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        ms_total = float(t.item())
-    ms_step = ms_total / args.steps
+        step_ms = [float(v) for v in t.cpu()]
+    ms_step = statistics.median(step_ms)  # the median over the timed steps
+    ms_mean = sum(step_ms) / len(step_ms)
     flops = 2.0 * M * N * K
     tflops = flops / (ms_step * 1e-3) / 1e12
 
     # ---- roofline of the dominant kernel (the shard GEMM) ----
     peaks, peak_src = load_peaks()
-    # TF32 dense peak = measured bf16 x (nominal tf32 / bf16 = 1.1 / 2.25 ~ 0.5)
+    # TF32 dense peak = measured bf16 x (nominal tf32 / bf16 = 1.1 / 2.25 ~ 0.5). The GEMM is
+    # timed inside a seconds-long run of back-to-back steps under the power cap, so the
+    # sustained figure is the denominator (B200_PROFILING.md); the burst one is reported too.
     tf32_sustained = 0.5 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     tf32_burst = 0.5 * peaks["bf16_tflops"]
-    gemm_ms = kt["gemm_ms"] / max(1, kt["gemm_launches"])
-    # algorithmic tensor work per launch in TF32-instruction-equivalent flops: 3xTF32 issues
-    # 3 TF32 MMAs per logical product (6 rows N K); TF32 + BF16 one TF32 MMA plus one BF16 MMA
-    # of twice the depth at twice the rate (2 + 2 = 4 rows N K)
-    terms = giga.product_scheme(rows, N, K)
-    tensor_flops = (3 if terms == 3 else 2) * 2.0 * rows * N * K
-    achieved = tensor_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
-    traffic = None
+    launches = rank_launches(giga, M, N, K, world, rank)
+    # algorithmic tensor work per step in TF32-instruction-equivalent flops: 3xTF32 issues 3
+    # TF32 MMAs per logical product (6 r N K per launch), TF32 + BF16 one TF32 MMA plus one
+    # BF16 MMA of twice the depth at twice the rate (4 r N K)
+    tensor_flops = sum((3 if t == 3 else 2) * 2.0 * r * N * kc for r, kc, t in launches)
+    terms_set = sorted({t for _, _, t in launches})
+    gemm_ms_step = kt["gemm_ms"] / args.steps  # all of this rank's GEMM launches in a step
+    achieved = tensor_flops / (gemm_ms_step * 1e-3) / 1e12 if gemm_ms_step > 0 else None
+    scheme = "+".join("3xTF32" if t == 3 else "TF32+BF16" for t in terms_set)
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tp):
+    if world == 1 and os.path.exists(tp):
         try:
             with open(tp) as f:
-                tr = json.load(f).get(args.config)
-            traffic = tr
+                traffic = json.load(f).get(args.config)
+            traffic_src = ("profiles/gemm_traffic.json: dram__bytes_read.sum + "
+                           "dram__bytes_write.sum of one launch from an ncu --set full capture "
+                           "of this kernel and config (not measured in this run)")
         except Exception:  # noqa: BLE001
             traffic = None
     roof = {"bound": "tensor", "achieved": round(achieved, 2) if achieved else None,
-            "peak": round(tf32_burst, 1), "unit": "TFLOP/s",
-            "frac": round(achieved / tf32_burst, 4) if achieved else None,
-            "traffic": traffic,
-            "kernel": "gemm_3xtf32_kernel", "kernel_ms": round(gemm_ms, 4),
-            "kernel_share_of_step": round(gemm_ms / ms_step, 4) if ms_step else None,
-            "peak_note": f"TF32 dense = 0.5 x {peak_src} cuBLAS bf16 burst "
-                         f"({peaks['bf16_tflops']}; nominal tf32:bf16 = 1.1:2.25); against the "
-                         f"sustained figure ({peaks.get('bf16_tflops_sustained')}) frac = "
-                         f"{round(achieved / tf32_sustained, 4) if achieved else None}; "
-                         f"achieved = {3 if terms == 3 else 2} x 2 x rows x N x K TF32-equivalent "
-                         f"tensor flops per launch / event time",
-            "scheme": "3xTF32" if terms == 3 else "TF32+BF16",
+            "peak": round(tf32_sustained, 1), "unit": "TFLOP/s",
+            "frac": round(achieved / tf32_sustained, 4) if achieved else None,
+            "frac_vs_burst": round(achieved / tf32_burst, 4) if achieved else None,
+            "traffic": traffic, "traffic_source": traffic_src,
+            "kernel": "gemm_3xtf32_kernel", "launches_per_step": len(launches),
+            "kernel_ms_per_step": round(gemm_ms_step, 4),
+            "kernel_share_of_step": round(gemm_ms_step / ms_mean, 4) if ms_mean else None,
+            "peak_note": f"TF32 dense = 0.5 x {peak_src} cuBLAS bf16 sustained "
+                         f"({peaks.get('bf16_tflops_sustained')}; burst {peaks['bf16_tflops']}; "
+                         f"nominal tf32:bf16 = 1.1:2.25); achieved = the scheme's "
+                         f"TF32-equivalent tensor work (3 or 2 x 2 rows N K per launch) / "
+                         f"event time of the GEMM launches of a step",
+            "scheme": scheme,
             "limit_note": ("tensor pipe (3 TF32 MMAs per k8 step) at the power-capped clock"
-                           if terms == 3 else
-                           "operand feed: 32 KiB of TMA fills per CTA per 2-MMA stage against the "
-                           "measured per-SM TMA fill ceiling (roofline.feed), and the power cap; "
-                           "not the MMAs: DESIGN.md 6.7"),
+                           if terms_set == [3] else
+                           "operand feed: 32 KiB of TMA fills per CTA per 2-MMA stage against "
+                           "the per-SM fill ceiling (roofline.feed; multicast measured not to "
+                           "raise it), and the power cap: DESIGN.md 6.7"),
             "prep_ms_per_step": round(kt["split_ms"] / args.steps, 4),
             "prep_launches_per_step": round(kt["split_launches"] / args.steps, 2)}
-
-    # ---- the north_star's whole-step roofline: T_roof / t with
-    #      T_roof = max(2 r_max N K / (P_tf32 / 3), 4 (K N [g > 1] + (M - r_min) N) / BW_nvlink)
-    rows_all = [giga.partition(M, world, g)[1] for g in range(world)]
-    bw_nv = 770e9  # measured NVLink peer-copy GB/s per direction (B200_PROFILING.md)
-    t_comp = 2.0 * max(rows_all) * N * K / (tf32_burst * 1e12 / 3)
-    t_comm = 4.0 * ((K * N if world > 1 else 0) + (M - min(rows_all)) * N) / bw_nv
-    t_roof = max(t_comp, t_comm)
-    step_roof = {"definition": "T_roof / t, T_roof = max(2 r_max N K / (P_tf32/3), "
-                               "4 (KN[g>1] + (M - r_min) N) / 770 GB/s)",
-                 "t_comp_ms": round(t_comp * 1e3, 4), "t_comm_ms": round(t_comm * 1e3, 4),
-                 "bound": "tensor" if t_comp >= t_comm else "nvlink",
-                 "frac": round(t_roof / (ms_step * 1e-3), 4)}
-    if terms == 2:
-        # the prepared TF32 + BF16 kernel is bound by its TMA operand feed: 64 KiB of fills
-        # per 256 x 256 pair tile and 16-deep k-block = rows N K / 16 bytes per launch, against
-        # the measured L2 -> SM TMA fill ceiling (scripts/tma_box_bench.cu: 10.7 TB/s on a
-        # 148-SM B200 for every box shape; profiles/r01_tma_box_bench.jsonl)
-        feed_bytes = rows * N * K / 16.0
-        feed_ach = feed_bytes / (gemm_ms * 1e-3) / 1e9 if gemm_ms > 0 else None
-        roof["feed"] = {"bound": "l2_to_smem_tma", "achieved": round(feed_ach, 1) if feed_ach else None,
-                        "peak": 10714.0, "unit": "GB/s",
-                        "frac": round(feed_ach / 10714.0, 4) if feed_ach else None,
-                        "bytes_per_launch": feed_bytes,
-                        "peak_source": "measured TMA fill ceiling, scripts/tma_box_bench.cu"}
-    if terms == 2:
-        # the prepared TF32 + BF16 kernel is bound by its TMA operand feed: 64 KiB of fills
-        # per 256 x 256 pair tile and 16-deep k-block = rows N K / 16 bytes per launch, against
-        # the measured L2 -> SM TMA fill ceiling (scripts/tma_box_bench.cu: 10.7 TB/s on a
-        # 148-SM B200 for every box shape; profiles/r01_tma_box_bench.jsonl)
-        feed_bytes = rows * N * K / 16.0
-        feed_ach = feed_bytes / (gemm_ms * 1e-3) / 1e9 if gemm_ms > 0 else None
+    if 2 in terms_set:
+        # the prepared TF32 + BF16 kernel's operand feed: 64 KiB of fills per 256 x 256 pair
+        # tile and 16-deep k-block = r N K / 16 bytes per launch, against the measured L2 -> SM
+        # TMA fill ceiling (scripts/tma_box_bench.cu: 10.7 TB/s on a 148-SM B200 for every box
+        # shape; scripts/tma_mcast_bench.cu: multicast does not raise per-SM ingress)
+        feed_bytes = sum(r * N * kc / 16.0 for r, kc, t in launches if t == 2)
+        t2_flops = sum(4.0 * r * N * kc for r, kc, t in launches if t == 2)
+        feed_ms = gemm_ms_step * t2_flops / tensor_flops
+        feed_ach = feed_bytes / (feed_ms * 1e-3) / 1e9 if feed_ms > 0 else None
         roof["feed"] = {"bound": "l2_to_smem_tma",
                         "achieved": round(feed_ach, 1) if feed_ach else None,
                         "peak": 10714.0, "unit": "GB/s",
                         "frac": round(feed_ach / 10714.0, 4) if feed_ach else None,
-                        "bytes_per_launch": feed_bytes,
+                        "bytes_per_step": feed_bytes,
                         "peak_source": "measured TMA fill ceiling, scripts/tma_box_bench.cu"}
-    if terms == 2:  # the scheme's own ceiling: 2 TF32-instruction-equivalents per product
-        t_comp2 = 2.0 * max(rows_all) * N * K / (tf32_burst * 1e12 / 2)
-        step_roof["scheme_note"] = ("the north_star's T_comp assumes 3xTF32 (P_tf32/3); the "
-                                    "TF32 + BF16 scheme's ceiling is P_tf32/2")
-        step_roof["frac_scheme"] = round(max(t_comp2, t_comm) / (ms_step * 1e-3), 4)
+
+    # ---- whole-step roofline: T_roof / t with T_roof = max(T_comp, T_comm),
+    #      T_comp = the scheme's tensor work of the largest shard at the TF32 peak,
+    #      T_comm = 4 (K N [g > 1] + (M - r_min) N) / BW_nvlink (north_star)
+    rows_all = [giga.partition(M, world, g)[1] for g in range(world)]
+    bw_nv = 770e9  # measured NVLink peer-copy GB/s per direction (B200_PROFILING.md)
+    t_comm = 4.0 * ((K * N if world > 1 else 0) + (M - min(rows_all)) * N) / bw_nv
+    w_max = max(range(world), key=lambda g: rows_all[g])
+    tf_max = sum((3 if t == 3 else 2) * 2.0 * r * N * kc
+                 for r, kc, t in rank_launches(giga, M, N, K, world, w_max))
+    t_comp = tf_max / (tf32_sustained * 1e12)
+    t_comp3 = 2.0 * max(rows_all) * N * K / (tf32_sustained * 1e12 / 3)
+    t_roof = max(t_comp, t_comm)
+    step_roof = {"definition": "T_roof / t (median step), T_roof = max(T_comp, T_comm); T_comp "
+                               "= the scheme's TF32-equivalent tensor work of the largest shard "
+                               "at the sustained TF32 peak, T_comm = 4 (K N [g>1] + (M - r_min) "
+                               "N) / 770 GB/s",
+                 "t_comp_ms": round(t_comp * 1e3, 4), "t_comm_ms": round(t_comm * 1e3, 4),
+                 "bound": "tensor" if t_comp >= t_comm else "nvlink",
+                 "frac": round(t_roof / (ms_step * 1e-3), 4),
+                 "frac_vs_3xtf32_ceiling": round(max(t_comp3, t_comm) / (ms_step * 1e-3), 4),
+                 "note": "frac_vs_3xtf32_ceiling is the north_star's reading (P_tf32 / 3 per "
+                         "logical product); above 1 when a launch runs the 2-MMA TF32 + BF16 "
+                         "scheme"}
 
     # ---- end to end: host buffers through the C ABI ----
     e2e = None
@@ -418,7 +491,7 @@ def main():
         if world == 1:  # a failure here must not cost the device-resident line
             try:
                 e2e = measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev,
-                                  pg, red_dev, (A, B, C))
+                                  pg, red_dev, (A, B, C), device_ms=ms_step)
             except Exception as ex:  # noqa: BLE001
                 e2e = {"value": None, "error": repr(ex)[:300]}
         else:  # collectives inside: every rank must run it (no per-rank recovery)
@@ -426,16 +499,8 @@ def main():
                               red_dev, (A, B, C))
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = len(os.sched_getaffinity(0))
-        try:
-            r = oracle_sample(M, N, K, args.dist, args.cpu_budget, threads)
-            cpu = {"value": round(r["tflops"], 6), "unit": "TFLOP/s", "cores": threads,
-                   "kind": "oracle",
-                   "sample": f"first {r['rows']} rows of C (of {M}), full N={N}, K={K}: "
-                             f"{r['seconds']:.1f} s fp64 i-k-j C triple loop"}
-        except Exception as ex:  # noqa: BLE001
-            cpu = {"value": None, "error": repr(ex)[:300]}
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(M, N, K, args, world)
 
     # the paper's only number for this metric is 32768^3 on its 2 GPUs
     # (159 s -> 0.443 TFLOP/s derived, 2x Quadro RTX 6000); context, not the target
@@ -445,10 +510,12 @@ def main():
         line = {
             "metric": METRIC, "value": round(tflops, 3), "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "ms_per_step_mean": round(ms_mean, 4), "timing": "median of per-step CUDA events "
+            "(max over ranks per step)",
             "higher_is_better": True, "scaling": "strong", "vs_baseline": vs_base,
             "wall_ms_per_step": round(wall_ms / args.steps, 4),
             "dtype": "f32",
-            "arithmetic": ("3xTF32 tcgen05 MMAs" if terms == 3 else
+            "arithmetic": ("3xTF32 tcgen05 MMAs" if terms_set == [3] else
                            "TF32 + BF16 tcgen05 MMAs (a_hi b_hi in TF32, a_lo b + a_hi b_lo in one "
                            "K=16 BF16 MMA; operands prepared in HBM per call)")
                           + " + fp32 RN promotion (fp32-accurate: <= 1e-5 sum|A||B|)",
@@ -460,6 +527,8 @@ def main():
                              "per-step events)"},
             "roofline": roof, "roofline_step": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(kt["gemm_launches"] + kt["split_launches"]),
+            "gpu_launches_per_step": round((kt["gemm_launches"] + kt["split_launches"])
+                                           / args.steps, 2),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
@@ -561,8 +630,43 @@ def run_dot(args):
     return 0
 
 
+def pcie_roofline(torch, dev, h2d, d2h, device_ms, e2e_ms):
+    """the host-buffer call moves h2d bytes in and d2h bytes out over this
+    GPU's PCIe link beside the device-resident step, on three engines that overlap, so its
+    time is at least T_roof = max(h2d / R_h2d, d2h / R_d2h, device step). R = pinned 1 GiB
+    copy rates measured here, each direction alone (CUDA events, best of 3)."""
+    n = 1 << 28
+    hb = torch.empty(n, dtype=torch.float32).pin_memory()
+    db = torch.empty(n, dtype=torch.float32, device=dev)
+
+    def rate(fn):
+        best = 1e9
+        for _ in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 4.0 * n / (best * 1e-3) / 1e9
+
+    r_h2d = rate(lambda: db.copy_(hb, non_blocking=True))
+    r_d2h = rate(lambda: hb.copy_(db, non_blocking=True))
+    t_h2d, t_d2h = h2d / r_h2d / 1e6, d2h / r_d2h / 1e6  # ms
+    terms = {"h2d": t_h2d, "d2h": t_d2h, "device_step": device_ms}
+    bound = max(terms, key=terms.get)
+    t_roof = terms[bound]
+    return {"bound": bound, "t_roof_ms": round(t_roof, 3), "frac": round(t_roof / e2e_ms, 4),
+            "h2d_ms_at_link_rate": round(t_h2d, 3), "d2h_ms_at_link_rate": round(t_d2h, 3),
+            "device_step_ms": round(device_ms, 3), "h2d_GBps_measured": round(r_h2d, 2),
+            "d2h_GBps_measured": round(r_d2h, 2),
+            "definition": "max(H2D bytes / R_h2d, D2H bytes / R_d2h, device-resident median "
+                          "step) / e2e step; R = pinned 1 GiB copies each direction alone"}
+
+
 def measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev, pg, red_dev,
-                dev_bufs):
+                dev_bufs, device_ms=None):
     """Same metric with the inputs in pinned HOST memory: every step copies this rank's A
     rows (and B on rank 0) host->device, runs the hot path and copies this rank's C rows
     back (N = 1: the single giga_matmul host-pointer call of the C ABI)."""
@@ -582,10 +686,12 @@ def measure_e2e(giga, torch, synth, args, M, N, K, world, rank, local, dev, pg, 
         t = statistics.median(ts)
         h2d = 4 * (M * K + K * N)
         d2h = 4 * M * N
-        return {"value": round(2.0 * M * N * K / t / 1e12, 3), "unit": "TFLOP/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": round(t * 1e3, 3),
-                "api": "giga_matmul(host pinned A, B, C) blocking, wall clock"}
+        out = {"value": round(2.0 * M * N * K / t / 1e12, 3), "unit": "TFLOP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": round(t * 1e3, 3),
+               "api": "giga_matmul(host pinned A, B, C) blocking, wall clock"}
+        out["roofline"] = pcie_roofline(torch, dev, h2d, d2h, device_ms, t * 1e3)
+        return out
     # N > 1: each rank stages its own rows; rank 0 stages B
     Ah = torch.empty((rows, K), dtype=torch.float32).pin_memory()
     Ah.copy_(synth.gen_rows_torch(r0, rows, K, synth.MATRIX_A, args.dist, device=dev).cpu())

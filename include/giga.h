@@ -253,9 +253,11 @@ int giga_gemm_3xtf32(const float *A, const float *A_lo, const float *B, const fl
 
 /* As giga_gemm_3xtf32 with the numerics and tiling knobs exposed (tests and probes):
  * terms = 3 (3xTF32), 2 (TF32 + BF16: a_hi*b_hi as one TF32 MMA, a_lo*b + a_hi*b_lo as one
- * K=16 BF16 MMA per k8 step, split error <= 2^-18 |a||b| per product with the default RN hi,
- * $GIGA_HI_RN=0 truncates (2^-17); A_lo and B_lo must be NULL) or 1 (plain TF32: a_hi*b_hi
- * only; A_lo/B_lo ignored). The product path uses 3 unless $GIGA_SCHEME=tf32bf16;
+ * K=16 BF16 MMA per k8 step, split error <= 3 * 2^-19 |a||b| (5.7e-6) per product with the
+ * default RN hi (5.3e-6 reached by constructed inputs, tests/adversarial.py); $GIGA_HI_RN=0
+ * truncates hi, a measurement mode whose split error reaches ~3 * 2^-18 = 1.1e-5 and can
+ * exceed the bound; A_lo and B_lo must be NULL) or 1 (plain TF32: a_hi*b_hi only; A_lo/B_lo
+ * ignored). The product path picks 3 or 2 per launch (giga_product_scheme);
  * promote_kblocks = number of 16-wide k-blocks accumulated in TMEM before the partial sum
  * is added into the fp32 register sum; 0 = never promote (one TMEM accumulation over K);
  * -1 = the library default;
@@ -295,7 +297,7 @@ int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *ou
  * DESIGN.md 6.7): *terms = 3 (3xTF32: three kind::tf32 MMAs per k8 step) or 2 (TF32 + BF16:
  * a_hi*b_hi as one kind::tf32 MMA plus a_lo*b + a_hi*b_lo as one K=16 kind::f16 MMA, with
  * hi = RN tf32(x); A_hi, A', B_hi, B' prepared once per launch in library-owned HBM scratch
- * by two elementwise kernels; per-product split error <= 2^-18 |a||b|). 2 when M >= 4096,
+ * by two elementwise kernels; per-product split error <= 3 * 2^-19 |a||b|). 2 when M >= 4096,
  * N >= 8192 and either K >= 2048 with M N K >= 2^37 or K >= 512 with M N K >= 2^38 (the
  * preparation is then amortised: measured crossover), else 3;
  * $GIGA_SCHEME = 3xtf32 | tf32bf16 forces one. Errors: INVALID_ARG. */

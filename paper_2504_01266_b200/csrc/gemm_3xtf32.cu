@@ -210,10 +210,13 @@ __host__ __device__ __forceinline__ void unit_coords(int u, const GemmParams &p,
 // are ONE kind::f16 MMA with K = 16 over bf16 operands concatenated along K:
 //   A' row  = [bf16(a_lo[k0..k7]) | bf16(a_hi[k0..k7])]           (K-major, SW64, 64 B rows)
 //   B' rows = [bf16(b[k0..k7][n]) ; bf16(b_lo[k0..k7][n])]         (MN-major, SW128)
-// bf16 keeps 8 significant bits, so each correction carries <= 2 * 2^-9 of itself:
-// |error| <= 2^-18 |a||b| per product with RN hi (|lo| <= 2^-11 |x|), 2^-17 with truncation,
-// against the 1e-5 = 2^-16.6 bound. A bf16 K16 MMA takes the time of a tf32 K8 MMA, so a
-// k8 step costs 2 MMA times instead of 3xTF32's 3.
+// bf16 keeps 8 significant bits (unit roundoff 2^-8). With RN hi, |lo| <= 2^-11 |x|, and per
+// product the four roundings cost at most 2^-8 |a_lo||b| <= 2^-19 |a||b| (b), 2^-20 |a||b|
+// (a_lo: its exponent is <= that of a minus 12), 2^-19 (a_hi) and 2^-20 (b_lo): |error| <=
+// 3 * 2^-19 |a||b| = 5.7e-6 plus O(2^-27); constructed inputs reach 5.3e-6
+// (tests/adversarial.py). Truncated hi (|lo| < 2^-10 |x|) doubles the lo terms: ~3 * 2^-18,
+// above the 1e-5 bound, so the product path rounds hi to nearest. A bf16 K16 MMA takes the
+// time of a tf32 K8 MMA, so a k8 step costs 2 MMA times instead of 3xTF32's 3.
 // Layouts written here (stage = [A raw | A' | B raw | B']):
 //   A raw: TMA SW64, 128 rows x 64 B, 16-B chunk c of row r at r*64 + ((c ^ (r>>1 & 3)) << 4).
 //     A' has the same geometry: chunk 2h (2h+1) of row r = bf16 lo (hi) of k8 step h.

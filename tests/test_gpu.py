@@ -387,8 +387,18 @@ def test_promotion_is_what_keeps_long_sums_accurate(giga, torch_cuda):
 
 # ---- full-size configurations, row-sampled ---------------------------------------------
 
-def _sampled_rows(M, rng, extra=64):
-    rows = {0, M - 1, M // 2, M // 2 - 1}
+def _sampled_rows(M, rng, extra=256):
+    """`extra` seeded rows plus the first and last row of every shard of the
+    1/2/4/8-GPU partitions (giga_partition's rule), where a tile or shard boundary bug would
+    show first."""
+    rows = {M // 2, M // 2 - 1}
+    for world in (1, 2, 4, 8):
+        base = M // world
+        for g in range(world):
+            r0 = g * base
+            n = base if g < world - 1 else M - (world - 1) * base
+            if n > 0:
+                rows.update((r0, r0 + n - 1))
     rows.update(int(r) for r in rng.integers(0, M, extra))
     return np.array(sorted(rows))
 
@@ -405,7 +415,7 @@ def test_full_size_sampled_rows(giga, torch_cuda, M, N, K, dist):
     dB = synth.gen_rows_torch(0, K, N, synth.MATRIX_B, dist, device="cuda")
     dC = torch.full((M, N), float("nan"), device="cuda")
     giga.matmul_sharded([dA], [dB], [dC], M, N, K)
-    rows = _sampled_rows(M, np.random.default_rng(M + N + K), extra=32 if K <= 16384 else 12)
+    rows = _sampled_rows(M, np.random.default_rng(M + N + K))
     Cs = dC[torch.from_numpy(rows).cuda()].cpu().numpy()
     assert not torch.isnan(dC).any().item()
     del dA, dB, dC
@@ -510,7 +520,7 @@ def test_bench_launch_configuration_full_size(torch_cuda, config):
         for _ in range(2):
             g.matmul_rank(A, B, C, M, N, K, stream=s)
         s.synchronize()
-        rows = _sampled_rows(M, np.random.default_rng(7), extra=6)
+        rows = _sampled_rows(M, np.random.default_rng(7))
         Cs = C[torch.from_numpy(rows).cuda()].cpu().numpy()
         del A, B, C
         torch.cuda.empty_cache()

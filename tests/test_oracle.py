@@ -214,3 +214,38 @@ def test_checker_negative_controls():
     flip = Ci.astype(np.float32)
     flip[4, 3] += 1.0
     assert not check_exact(flip, Ci)[0]
+
+
+# ---- the want_s=False path (worker_noS: the gloo schedule tests' reference and the
+#      cpu_baseline timing leg) --------------------------------------------------------------
+
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_without_s_equals_with_s_bitwise(threads):
+    """C from the path that skips S is the same bits as C from the pinned path (same loop,
+    same ascending k), for full products and for row-index selections."""
+    A = _rand_f32((37, 53))
+    B = _rand_f32((53, 29))
+    C1, S1 = oracle.gemm(A, B, nthreads=threads)
+    C0, S0 = oracle.gemm(A, B, nthreads=threads, want_s=False)
+    assert S0 is None and S1 is not None
+    assert C0.dtype == np.float64 and np.array_equal(C0.view(np.uint64), C1.view(np.uint64))
+    rows = np.array([36, 0, 5, 5, 17])
+    R1, _ = oracle.gemm_row_index(A, B, rows, nthreads=threads)
+    R0, S = oracle.gemm_row_index(A, B, rows, nthreads=threads, want_s=False)
+    assert S is None and np.array_equal(R0.view(np.uint64), R1.view(np.uint64))
+    assert np.array_equal(R0, C1[rows])
+
+
+def test_without_s_closed_forms():
+    """want_s=False pinned on its own against closed forms: all-ones gives K, identity gives
+    A, integer inputs give numpy's exact int64 product."""
+    C, _ = oracle.gemm(np.ones((5, 300), np.float32), np.ones((300, 7), np.float32),
+                       want_s=False)
+    assert np.all(C == 300.0)
+    A = _rand_f32((9, 9))
+    C, _ = oracle.gemm(A, np.eye(9, dtype=np.float32), want_s=False)
+    assert np.array_equal(C, A.astype(np.float64))
+    Ai = RNG.integers(-50, 51, (23, 41))
+    Bi = RNG.integers(-50, 51, (41, 19))
+    C, _ = oracle.gemm(Ai.astype(np.float32), Bi.astype(np.float32), nthreads=4, want_s=False)
+    assert np.array_equal(C, (Ai @ Bi).astype(np.float64))
