@@ -30,6 +30,21 @@ __global__ void __cluster_dims__(2, 1, 1) tmem_pair_alloc_kernel(int *out) {
   }
 }
 
+// Occupier: each CTA (one per SM: its shared memory leaves no room for a GEMM CTA beside it)
+// records its SM and spins for `ns` nanoseconds of %globaltimer. Takes SMs away from a
+// concurrently launched GEMM, the way NCCL's kernels do in the multi-GPU pipeline.
+__global__ void occupy_kernel(int64_t ns, int *smids) {
+  extern __shared__ uint8_t pad[];
+  if (threadIdx.x == 0) {
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    pad[0] = 1;
+    smids[blockIdx.x] = int(sm);
+    const uint64_t t0 = ptx::globaltimer_ns();
+    while (int64_t(ptx::globaltimer_ns() - t0) < ns) __nanosleep(1000);
+  }
+}
+
 // TMA one box into smem, dump the raw smem bytes (box_bytes) to out.
 __global__ void tma_dump_kernel(const __grid_constant__ CUtensorMap tm, int c0, int c1,
                                 uint32_t box_bytes, float *out) {
@@ -160,4 +175,26 @@ extern "C" int giga_dbg_tmem_pair_alloc(int nclusters, int *out) {
   dbg::tmem_pair_alloc_kernel<<<2 * nclusters, 64>>>(out);
   if (cudaGetLastError() != cudaSuccess) return -3;
   return cudaDeviceSynchronize() == cudaSuccess ? 0 : -4;
+}
+
+// k occupier CTAs (occupy_kernel) on `stream`, `smem` bytes of shared memory each.
+extern "C" int giga_dbg_occupy(int nctas, int smem, int64_t ns, int *smids, void *stream) {
+  if (cudaFuncSetAttribute(dbg::occupy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smem) != cudaSuccess)
+    return -2;
+  dbg::occupy_kernel<<<nctas, 32, smem, static_cast<cudaStream_t>(stream)>>>(ns, smids);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
+// One GEMM launch of the product scheme's kernel with its persistent grid capped at max_ctas
+// SMs (the NCCL pipeline's configuration: GemmExtra::max_ctas), on `stream`.
+extern "C" int giga_dbg_gemm_max_ctas(const float *A, const float *B, float *C, int64_t M,
+                                      int64_t N, int64_t K, int terms, int max_ctas,
+                                      void *stream) {
+  giga::GemmExtra ex;
+  ex.max_ctas = max_ctas;
+  return giga::launch_gemm_3xtf32(A, nullptr, B, nullptr, C, M, N, K, N, terms, -1,
+                                  static_cast<cudaStream_t>(stream), 0, &ex) == cudaSuccess
+             ? 0
+             : -3;
 }

@@ -80,6 +80,7 @@ constexpr size_t SMEM_RING = 192 * 1024;         // operand ring per CTA
 constexpr uint32_t EPI_STAGE_BYTES = 32 * 32 * 4;  // per epilogue warp: 32 rows x 32 fp32
 constexpr uint32_t EPI_BYTES = NUM_EPI_WARPS * EPI_STAGE_BYTES;  // 32 KiB C staging
 constexpr size_t EPI_SLOT_BYTES = 32 * 128 * 4;  // K-split partial of one epilogue warp
+constexpr int SCHED_SLOTS = 8;                   // ring of claimed work units (power of 2)
 }  // namespace cfg
 
 template <int CG>
@@ -113,7 +114,13 @@ struct GemmParams {
   float *sk_ws;     // (num_tiles - first_split) * split_s * CG * 8 slots of 32 x 128 fp32
   unsigned *sk_cnt; // (num_tiles - first_split) * CG * 8 arrival counters, 0 between launches
   int group_m;    // L2 raster: consecutive tiles walk group_m M-tiles before the next N-tile
-  unsigned *wave_sync;  // non-null: zeroed counter for the producers' per-wave barrier
+  // Dynamic schedule (per-stream counters, zero between launches; the last CTA to finish
+  // resets them): sched[0] = next unit to claim, sched[1] = units whose loads a CTA has
+  // issued (the producers' wave barrier), sched[2] = CTAs finished. nullptr: static
+  // round-robin units, no wave barrier (no counters could be had, e.g. inside a capture).
+  unsigned *sched;
+  int wave_sync;  // 1: a producer starts unit u's loads once every unit of the previous waves
+                  // (u / clusters) has been issued by all its CTAs
   int n_cdst;     // C destinations in CMaps (1 + peers when the gather is fused)
   int lo_smem;    // 1: lo tiles computed in smem from the raw tiles; 0: TMA-loaded (A_lo, B_lo)
   int hi_rn;      // terms == 2: hi = RN tf32(x) written over the raw tile (else hi = trunc)
@@ -316,6 +323,30 @@ __device__ __forceinline__ void xform_tf32_bf16(uint32_t sA, int xt, int rn) {
   }
 }
 
+// Consumer side of the claimed-unit ring: wait for the unit of ring position `it`, read it,
+// release the slot on the leader's sched_empty (one arrive per consuming warp: lane 0, after
+// the whole warp has read the slot; or a lone thread). Returns the unit, -1 = no more work.
+template <int CG>
+__device__ __forceinline__ int sched_take(int it, uint64_t *sched_full, uint64_t *sched_empty,
+                                          uint32_t sempty_leader, volatile int *ring,
+                                          bool whole_warp) {
+  const int slot = it & (cfg::SCHED_SLOTS - 1);
+  const uint32_t ph = uint32_t(it / cfg::SCHED_SLOTS) & 1;
+  if (CG == 2)
+    ptx::mbar_wait_cluster(&sched_full[slot], ph);  // the leader published it remotely
+  else
+    ptx::mbar_wait(&sched_full[slot], ph);
+  const int u = ring[slot];
+  if (whole_warp) __syncwarp();
+  if (!whole_warp || (threadIdx.x & 31) == 0) {
+    if (CG == 2)
+      ptx::mbar_arrive_cluster(sempty_leader + 8u * uint32_t(slot));
+    else
+      ptx::mbar_arrive(&sched_empty[slot]);
+  }
+  return u;
+}
+
 template <int CG>
 __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -338,6 +369,11 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(lofull + STAGES);
   uint8_t *sig = reinterpret_cast<uint8_t *>(lofull + STAGES) + 16;  // 16 B aligned, 32 B
   uint64_t *cbar = reinterpret_cast<uint64_t *>(sig + 32);  // per epilogue warp: C block loads
+  // claimed-unit ring: the leader's producer claims a unit and publishes it to every consumer
+  // warp of both CTAs (sched_full); they release the slot on the leader's sched_empty
+  uint64_t *sched_full = cbar + NUM_EPI_WARPS;
+  uint64_t *sched_empty = sched_full + SCHED_SLOTS;
+  volatile int *sched_ring = reinterpret_cast<volatile int *>(sched_empty + SCHED_SLOTS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -362,6 +398,14 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       ptx::mbar_init(&lofull[s], NUM_XFORM_WARPS);
     }
     for (int w = 0; w < NUM_EPI_WARPS; ++w) ptx::mbar_init(&cbar[w], 1);
+    // consumers of a claimed unit: every epilogue (and, unless direct, transform) warp of both
+    // CTAs, the MMA issuer and the peer's producer
+    const uint32_t n_cons =
+        uint32_t(CG * (NUM_EPI_WARPS + (direct ? 0 : NUM_XFORM_WARPS)) + 1 + (CG == 2 ? 1 : 0));
+    for (int q = 0; q < SCHED_SLOTS; ++q) {
+      ptx::mbar_init(&sched_full[q], 1);
+      ptx::mbar_init(&sched_empty[q], n_cons);
+    }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], NUM_EPI_WARPS * CG);
@@ -398,22 +442,44 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
                                         : (A_BYTES + T::B_BYTES);
       int stage = 0;
       uint32_t phase = 0;
-      int wave = 0;
-      uint32_t wave_target = 0;
-      for (int u = cluster_id; u < p.num_units; u += num_clusters, ++wave) {
-        if (p.wave_sync && wave > 0) {
-          // Wave barrier among the producers: start loading wave w only when every CTA that
-          // has a tile in wave w has issued all loads of wave w-1, so the clusters sharing
-          // A / B panels stay within one tile of each other and hit in L2 (unsynchronised,
-          // persistent clusters drift apart over the waves and re-fetch panels from HBM:
-          // 147 -> 35 GB of DRAM reads at 16384^3). A locality hint only, never needed for
-          // correctness: the wait gives up after 2 ms, so CTAs kept off the GPU by another
-          // kernel cannot deadlock it.
-          const int active = min(num_clusters, p.num_units - wave * num_clusters);
-          wave_target += uint32_t(active * CG);
-          atomicAdd(p.wave_sync, 1u);
+      const uint32_t ring_peer = CG == 2 ? ptx::map_cluster((const void *)sched_ring, 1) : 0;
+      const uint32_t sfull_peer = CG == 2 ? ptx::map_cluster(&sched_full[0], 1) : 0;
+      const uint32_t sempty_leader = ptx::smem_u32(&sched_empty[0]) & ptx::kPeerBitMask;
+      for (int it = 0;; ++it) {
+        // Work units are claimed dynamically (an atomic counter, in unit order) by the running
+        // clusters, so a cluster that another kernel keeps off the GPU (NCCL's CTAs, a
+        // co-running GEMM) takes no units at all instead of owning every num_clusters-th one
+        // the others would wait for. The leader's producer claims and publishes the unit to
+        // every consumer warp of both CTAs through the ring.
+        int u;
+        const int slot = it & (SCHED_SLOTS - 1);
+        const uint32_t sph = uint32_t(it / SCHED_SLOTS) & 1;
+        if (leader) {
+          if (it >= SCHED_SLOTS) ptx::mbar_wait_cluster(&sched_empty[slot], sph ^ 1);
+          u = p.sched ? int(atomicAdd(&p.sched[0], 1u)) : cluster_id + it * num_clusters;
+          if (u >= p.num_units) u = -1;
+          sched_ring[slot] = u;
+          if (CG == 2) {
+            ptx::st_cluster_u32(ring_peer + 4u * uint32_t(slot), uint32_t(u));
+            ptx::mbar_arrive_cluster(sfull_peer + 8u * uint32_t(slot));
+          }
+          ptx::mbar_arrive(&sched_full[slot]);
+        } else {
+          u = sched_take<CG>(it, sched_full, sched_empty, sempty_leader, sched_ring, false);
+        }
+        if (u < 0) break;
+        const int wave = u / num_clusters;
+        if (p.sched && p.wave_sync && wave > 0) {
+          // Wave barrier among the producers: start loading unit u only when every unit of
+          // the earlier waves has been issued by all its CTAs, so the clusters sharing A / B
+          // panels stay within about one tile of each other and hit in L2 (unsynchronised,
+          // persistent clusters drift apart and re-fetch panels from HBM: 147 -> 35 GB of
+          // DRAM reads at 16384^3). Deadlock-free: units are claimed in increasing order, only
+          // by running clusters, and the loads of a claimed unit wait for nothing but earlier
+          // units. The 2 ms cap only bounds a locality hint (never needed for correctness).
+          const uint32_t target = uint32_t(CG) * uint32_t(wave) * uint32_t(num_clusters);
           const uint64_t t_start = ptx::globaltimer_ns();
-          while (ptx::ld_acquire_gpu(p.wave_sync) < wave_target &&
+          while (ptx::ld_acquire_gpu(&p.sched[1]) < target &&
                  ptx::globaltimer_ns() - t_start < 2000000ull)
             __nanosleep(64);
         }
@@ -483,6 +549,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
             phase ^= 1;
           }
         }
+        if (p.sched) atomicAdd(&p.sched[1], 1u);  // this CTA has issued every load of unit u
       }
     }
   } else if (warp == 1) {
@@ -493,7 +560,10 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
-      for (int u = cluster_id; u < p.num_units; u += num_clusters) {
+      for (int it = 0;; ++it) {
+        const int u = sched_take<CG>(it, sched_full, sched_empty,
+                                     ptx::smem_u32(&sched_empty[0]), sched_ring, false);
+        if (u < 0) break;
         int t, kb, kb1, part;
         unit_coords(u, p, t, kb, kb1, part);
         const int n_int = (kb1 - kb + p.p_kb - 1) / p.p_kb;
@@ -579,9 +649,12 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     const uint32_t lofull_leader = ptx::smem_u32(&lofull[0]) & ptx::kPeerBitMask;
     const uint32_t sig_leader = ptx::smem_u32(sig) & ptx::kPeerBitMask;
     const int xw = warp - XFORM_WARP0;
+    const uint32_t sempty_leader = ptx::smem_u32(&sched_empty[0]) & ptx::kPeerBitMask;
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = direct ? p.num_units : cluster_id; u < p.num_units; u += num_clusters) {
+    for (int it = 0; !direct; ++it) {  // direct: no transform work, not a ring consumer
+      const int u = sched_take<CG>(it, sched_full, sched_empty, sempty_leader, sched_ring, true);
+      if (u < 0) break;
       int t, kb0, kb1, part;
       unit_coords(u, p, t, kb0, kb1, part);
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -638,9 +711,12 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     const int half = e >> 2;    // column half of the 256-wide tile
     const uint32_t tempty_leader0 = ptx::smem_u32(&tempty[0]) & ptx::kPeerBitMask;
     const uint32_t tempty_leader1 = ptx::smem_u32(&tempty[1]) & ptx::kPeerBitMask;
+    const uint32_t sempty_leader = ptx::smem_u32(&sched_empty[0]) & ptx::kPeerBitMask;
     uint32_t acc_iter = 0;
     uint32_t cphase = 0;  // parity of this warp's C-load barrier
-    for (int u = cluster_id; u < p.num_units; u += num_clusters) {
+    for (int it = 0;; ++it) {
+      const int u = sched_take<CG>(it, sched_full, sched_empty, sempty_leader, sched_ring, true);
+      if (u < 0) break;
       int t, kb0, kb1, mb, nb, part;
       unit_coords(u, p, t, kb0, kb1, part);
       tile_coords(t, p, mb, nb);
@@ -778,6 +854,17 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       ptx::tmem_dealloc_cg2(tmem_base, TMEM_COLS);
     else
       ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+  if (threadIdx.x == 0 && p.sched) {
+    // thread 0 made every claim and issued-count of this CTA; the last CTA of the grid to
+    // finish returns the counters to zero for the next launch on this stream
+    __threadfence();
+    if (atomicAdd(&p.sched[2], 1u) == gridDim.x - 1) {
+      p.sched[0] = 0;
+      p.sched[1] = 0;
+      p.sched[2] = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -1127,6 +1214,38 @@ bool ksplit_workspace(cudaStream_t st, size_t ws_bytes, size_t cnt_n, float **ws
   return true;
 }
 
+// Dynamic-schedule counters of the GEMM (GemmParams::sched): 3 words per (device, stream),
+// zeroed once at creation (stream-ordered), returned to zero by the last CTA of every launch.
+struct SchedCnt {
+  cudaStream_t st;
+  int dev;
+  unsigned *p;
+};
+static std::vector<SchedCnt> g_sched;
+
+unsigned *sched_counters(cudaStream_t st) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_ksplit_mu);
+  for (auto &c : g_sched)
+    if (c.st == st && c.dev == dev) return c.p;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return nullptr;
+  void *q = nullptr;
+  if (cudaMalloc(&q, 64) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (cudaMemsetAsync(q, 0, 64, st) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(q);
+    return nullptr;
+  }
+  g_sched.push_back({st, dev, static_cast<unsigned *>(q)});
+  return g_sched.back().p;
+}
+
 // Per-(device, stream) scratch of the TF32 + BF16 scheme's B_hi / B' (grow-only, like the
 // K-split workspace; growth waits for the stream's earlier launches).
 // The B part comes first in the buffer and remembers what it holds (key: B, ldb, K, N of the
@@ -1181,6 +1300,12 @@ void release_gemm_caches() {
     cudaFree(e.second.cnt);
   }
   g_ksplit.clear();
+  for (auto &c : g_sched) {
+    cudaSetDevice(c.dev);
+    cudaDeviceSynchronize();
+    cudaFree(c.p);
+  }
+  g_sched.clear();
   std::lock_guard<std::mutex> lr(g_retire_mu);
   for (auto &r : g_retired) {
     cudaSetDevice(r.first);
@@ -1437,7 +1562,8 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
     return (e && atoi(e) > 0) ? atoi(e) : 0;
   }();
   p.group_m = group_env ? group_env : GROUP_M;
-  p.wave_sync = nullptr;
+  p.sched = nullptr;
+  p.wave_sync = 0;
   p.n_cdst = 1 + ex->n_peer_c;
   const int nclu = sch.nclu;
   // K-split (gemm_schedule): kSplitReduce halves reduce-add into C zeroed here; kSplitWorkspace
@@ -1479,21 +1605,14 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
     const char *e = getenv("GIGA_WAVE_SYNC");
     return !(e && *e == '0');
   }();
-  if (wave_env && p.num_units > nclu) {
-    // one counter per device, zeroed on the launch stream before each launch
-    static std::mutex wmu;
-    static unsigned *wbuf[64] = {nullptr};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(wmu);
-    if (!wbuf[dev & 63]) {
-      cudaError_t e = cudaMalloc(&wbuf[dev & 63], sizeof(unsigned));
-      if (e != cudaSuccess) return e;
-    }
-    cudaError_t e = cudaMemsetAsync(wbuf[dev & 63], 0, sizeof(unsigned), st);
-    if (e != cudaSuccess) return e;
-    p.wave_sync = wbuf[dev & 63];
-  }
+  static const bool dyn_env = [] {  // $GIGA_DYNAMIC_SCHED=0: static round-robin units
+    const char *e = getenv("GIGA_DYNAMIC_SCHED");
+    return !(e && *e == '0');
+  }();
+  // the launch's dynamic-schedule counters (per device and stream: concurrent launches on
+  // other streams have their own); none inside a capture that has not seen this stream yet
+  if (dyn_env) p.sched = sched_counters(st);
+  p.wave_sync = (wave_env && p.num_units > nclu) ? 1 : 0;
 
   if (cg == 1) {
     cudaError_t e = ensure_smem_attr<1>();

@@ -115,6 +115,10 @@ GemmSchedule gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int cta
 // cannot be had (stream capture, out of memory): the launch then runs whole tiles.
 bool ksplit_workspace(cudaStream_t st, size_t ws_bytes, size_t cnt_n, float **ws,
                       unsigned **cnt);
+// The GEMM's dynamic-schedule counters for launches on `st` (current device): created zeroed
+// on first use (outside a capture; nullptr otherwise: the launch then runs static
+// round-robin units without the wave barrier).
+unsigned *sched_counters(cudaStream_t st);
 // Frees the K-split workspaces of every device (giga_finalize).
 void release_gemm_caches();
 // A library buffer superseded by a larger one (workspace growth): freed at once, unless a
