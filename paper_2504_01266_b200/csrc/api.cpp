@@ -680,8 +680,8 @@ int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const
                         int promote_kblocks, int cta_group, void *stream) {
   if (cta_group < 0 || cta_group > 2)
     return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_3xtf32_ex: cta_group must be 0, 1 or 2");
-  if (!A || !B || !C || (!A_lo) != (!B_lo) || (terms != 1 && terms != 2 && terms != 3) ||
-      (terms == 2 && A_lo))
+  if (!A || !B || !C || (!A_lo) != (!B_lo) || terms < 1 || terms > 4 ||
+      ((terms == 2 || terms == 4) && A_lo))
     return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_3xtf32: bad pointers/terms");
   TRY(check_dims(M, N, K));
   if ((K & 3) || (N & 3) || (ldc & 3) || ldc < N || !aligned16(A) || !aligned16(B) ||
@@ -740,7 +740,7 @@ int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *ou
   const int terms =
       product_terms(lo_presplit() ? reinterpret_cast<const float *>(1) : nullptr, M, N, K);
   const GemmSchedule s = gemm_schedule(M, N, K, num_sms > 0 ? num_sms : 148, 0, true,
-                                       default_promote_kblocks(terms));
+                                       default_promote_kblocks(terms), terms == 4 ? 32 : 16);
   const int64_t v[8] = {s.cg,          s.num_tiles, s.nclu,      s.n_kb,
                         s.first_split, s.s,         s.num_units, s.mode};
   for (int i = 0; i < 8; ++i) out[i] = v[i];

@@ -47,6 +47,7 @@
 //     CTA publishes its lo tiles to the leader's MMA with an async-proxy bulk signal
 //     (ptx::bulk_signal_leader): a release.cluster arrive per k-block cost 40%.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
@@ -128,6 +129,9 @@ struct GemmParams {
                   // through tmB / tmBlo); the transform warps handle A only
   int a_pre;      // terms == 2 (with b_pre): A_hi and A' precomputed too (tmA / tmAlo); no
                   // transform work in the kernel
+  // terms == 4 (3xFP16): the accumulator holds sum_k a'_ik b'_kj of the scaled operands
+  // a' = a 2^-ea[i], b' = b 2^-eb[j]; the epilogue stores ldexp(sum, ea[i] + eb[j])
+  const int *ea, *eb;
 };
 
 // C tensor maps: [0] this GPU's C, [1..] the same rows of the peers' C_full buffers.
@@ -168,6 +172,13 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
 // MN-major (the correction tiles of the TF32 + BF16 scheme, below).
 __host__ __device__ constexpr uint32_t make_idesc_bf16(int m, int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
+         (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+
+// Instruction descriptor, kind::f16 with FP16 A and B (format 0), F32 D; A K-major, B MN-major
+// (the three products of the 3xFP16 scheme).
+__host__ __device__ constexpr uint32_t make_idesc_f16(int m, int n) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | (0u << 15) | (1u << 16) |
          (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
@@ -382,12 +393,13 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
   const int cluster_id = blockIdx.x / CG;
   const int num_clusters = gridDim.x / CG;
   // TF32 + BF16 with both operands prepared in HBM: no transform, the MMA waits on `full`
-  const bool direct = p.terms == 2 && p.a_pre && p.b_pre;
+  // (and the 3xFP16 scheme, whose fp16 hi / lo operands always come prepared)
+  const bool direct = (p.terms == 2 && p.a_pre && p.b_pre) || p.terms == 4;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
-    if (p.terms == 3 && !p.lo_smem) {
+    if ((p.terms == 3 && !p.lo_smem) || p.terms == 4) {
       ptx::prefetch_tmap(&tmAlo);
       ptx::prefetch_tmap(&tmBlo);
     }
@@ -436,7 +448,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     if (lane == 0) {
       const bool load_lo = p.terms == 3 && !p.lo_smem;
       const bool load_bx = p.terms == 2 && p.b_pre;
-      const bool load_ax = load_bx && p.a_pre;
+      const bool load_ax = (load_bx && p.a_pre) || p.terms == 4;
       const uint32_t tx_cta = (load_lo || load_ax) ? T::STAGE_BYTES
                               : load_bx ? (A_BYTES + 2 * T::B_BYTES)
                                         : (A_BYTES + T::B_BYTES);
@@ -495,6 +507,37 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
           uint8_t *sB = sA + 2 * A_BYTES;
           uint8_t *sBlo = sB + T::B_BYTES;
           const int k0 = kb * BK;
+          if (p.terms == 4) {
+            // 3xFP16: k-blocks of 32; A_hi / A_lo fp16 K-major boxes {32, 128} (64 B rows,
+            // SW64), B_hi / B_lo fp16 N-major boxes {64, 32} (128 B rows, SW128): the same
+            // geometry as A' / B' of the TF32 + BF16 scheme
+            const int k32 = kb * 32;
+            if (CG == 1) {
+              ptx::mbar_expect_tx(&full[stage], tx_cta);
+              ptx::tma_load_2d(sA, &tmA, &full[stage], k32, m0);
+              ptx::tma_load_2d(sAlo, &tmAlo, &full[stage], k32, m0);
+#pragma unroll
+              for (int c = 0; c < T::B_COLS / 64; ++c) {
+                ptx::tma_load_2d(sB + c * 4096, &tmB, &full[stage], n0 + 64 * c, k32);
+                ptx::tma_load_2d(sBlo + c * 4096, &tmBlo, &full[stage], n0 + 64 * c, k32);
+              }
+            } else {
+              const uint32_t fb = ptx::smem_u32(&full[stage]) & ptx::kPeerBitMask;
+              if (leader) ptx::mbar_expect_tx(&full[stage], 2 * tx_cta);
+              ptx::tma_load_2d_cg2(sA, &tmA, fb, k32, m0);
+              ptx::tma_load_2d_cg2(sAlo, &tmAlo, fb, k32, m0);
+#pragma unroll
+              for (int c = 0; c < T::B_COLS / 64; ++c) {
+                ptx::tma_load_2d_cg2(sB + c * 4096, &tmB, fb, n0 + 64 * c, k32);
+                ptx::tma_load_2d_cg2(sBlo + c * 4096, &tmBlo, fb, n0 + 64 * c, k32);
+              }
+            }
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           if (direct) {
             // no transform: every tile lands on the leader's `full` barrier, which the MMA
             // issuer waits on (cta_group::2 loads complete on the peer's barrier)
@@ -557,6 +600,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     if (lane == 0 && leader) {
       constexpr uint32_t idesc = make_idesc(BM * CG, BN);
       constexpr uint32_t idesc2 = make_idesc_bf16(BM * CG, BN);
+      constexpr uint32_t idesc4 = make_idesc_f16(BM * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
@@ -581,6 +625,27 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
             const uint32_t sAlo = sA + A_BYTES;
             const uint32_t sB = sA + 2 * A_BYTES;
             const uint32_t sBlo = sB + T::B_BYTES;
+            if (p.terms == 4) {
+              // 3xFP16, two k16 steps per 32-wide k-block, small terms first:
+              // a_lo b_hi, a_hi b_lo, a_hi b_hi (a_lo b_lo, <= 2^-22 relative, is dropped)
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const uint64_t dAh = make_sdesc(sA + 32 * j, 16, 512, 4);
+                const uint64_t dAl = make_sdesc(sAlo + 32 * j, 16, 512, 4);
+                const uint64_t dBh = make_sdesc(sB + 2048 * j, 4096, 1024, 2);
+                const uint64_t dBl = make_sdesc(sBlo + 2048 * j, 4096, 1024, 2);
+                if (CG == 1) {
+                  ptx::mma_bf16(d_tmem, dAl, dBh, idesc4, acc);
+                  ptx::mma_bf16(d_tmem, dAh, dBl, idesc4, 1u);
+                  ptx::mma_bf16(d_tmem, dAh, dBh, idesc4, 1u);
+                } else {
+                  ptx::mma_bf16_cg2(d_tmem, dAl, dBh, idesc4, acc);
+                  ptx::mma_bf16_cg2(d_tmem, dAh, dBl, idesc4, 1u);
+                  ptx::mma_bf16_cg2(d_tmem, dAh, dBh, idesc4, 1u);
+                }
+                acc = 1;
+              }
+            } else {
 #pragma unroll
             for (int k8 = 0; k8 < BK / 8; ++k8) {
               const uint64_t dA = make_sdesc(sA + 32 * k8, 16, 512, 4);
@@ -617,6 +682,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
                 ptx::mma_tf32_cg2(d_tmem, dA, dB, idesc, acc);
               }
               acc = 1;
+            }
             }
             if (CG == 1)
               ptx::mma_commit(&empty[stage]);
@@ -792,6 +858,19 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       const uint32_t stg = ptx::smem_u32(epi_stage + e * EPI_STAGE_BYTES);
       const int crow0 = mb * T::TILE_M + int(rank) * BM + quad * 32;
       const int ccol0 = nb * BN + half * 128;
+      if (p.ea) {
+        // 3xFP16: undo the power-of-two operand scales (exact; ldexpf rounds only a result
+        // that leaves the normal range). ea / eb are padded to whole tiles.
+        const int ei = p.ea[crow0 + lane];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int4 f = *reinterpret_cast<const int4 *>(p.eb + ccol0 + 4 * q);
+          sum[4 * q] = ldexpf(sum[4 * q], ei + f.x);
+          sum[4 * q + 1] = ldexpf(sum[4 * q + 1], ei + f.y);
+          sum[4 * q + 2] = ldexpf(sum[4 * q + 2], ei + f.z);
+          sum[4 * q + 3] = ldexpf(sum[4 * q + 3], ei + f.w);
+        }
+      }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (lane == 0) ptx::bulk_wait_read<0>();  // previous store has left the staging tile
@@ -973,6 +1052,178 @@ __global__ void __launch_bounds__(256) prep_a_kernel(const float *__restrict__ A
   }
 }
 
+// ---- 3xFP16 scheme (terms == 4): operand preparation -----------------------------------------
+// TF32 is fp16's 11-bit significand with fp32's exponent range. The scheme keeps the
+// significand split of 3xTF32 (x = hi + lo, three products, small terms first) on the fp16
+// tensor-core path (K = 16 per instruction: twice kind::tf32's K per MMA time) and moves the
+// exponent range into exact power-of-two scales: row i of A is scaled by 2^-ea[i], column j
+// of B by 2^-eb[j], so that the row / column maximum lies in [2^14, 2^15) (fp16 max 65504);
+// the epilogue multiplies C_ij by 2^(ea[i] + eb[j]). hi = fp16 RN(x'), lo = fp16 RN(x' - hi)
+// (x' - hi is exact in fp32). For |x'| >= 2^-3 both are normal fp16 numbers and
+// |x' - hi - lo| <= 2^-22 |x'|; elements far below their row's (column's) maximum lose
+// relative precision to fp16's subnormal floor (2^-25 absolute in the scaled units).
+// An exponent of a row / column with no finite non-zero maximum is 0 (zeros stay exact,
+// Inf / NaN propagate as the contract states).
+__device__ __forceinline__ int scale_exp(uint32_t maxbits) {
+  if (maxbits == 0u || maxbits >= 0x7f800000u) return 0;
+  return ilogbf(__uint_as_float(maxbits)) - 14;
+}
+__device__ __forceinline__ void split_f16(float x, int e, uint16_t &h, uint16_t &l) {
+  const float xs = ldexpf(x, -e);
+  const __half hh = __float2half_rn(xs);
+  const __half ll = __float2half_rn(__fsub_rn(xs, __half2float(hh)));
+  h = __half_as_ushort(hh);
+  l = __half_as_ushort(ll);
+}
+
+// A: one block per row (rows >= M only write their exponent 0: ea is padded to whole tiles).
+// Pass 1: max |a| of the row (bit patterns: NaN > Inf > finite); pass 2 re-reads the row
+// (L2-resident) and writes A_hi / A_lo (fp16, row stride ldh). 4 B read (+ the L2 re-read),
+// 4 B written per element.
+__global__ void __launch_bounds__(512) prep16_a_kernel(const float *__restrict__ A, int64_t lda,
+                                                       int M, int K, uint16_t *__restrict__ Ah,
+                                                       uint16_t *__restrict__ Al, int64_t ldh,
+                                                       int *__restrict__ ea) {
+  __shared__ uint32_t red[16];
+  const int m = blockIdx.x;
+  if (m >= M) {
+    if (threadIdx.x == 0) ea[m] = 0;
+    return;
+  }
+  const float *row = A + int64_t(m) * lda;
+  const int k4 = K >> 2;
+  uint32_t mx = 0;
+  for (int i = threadIdx.x; i < k4; i += blockDim.x) {
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(row) + i);
+    mx = max(mx, max(max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu),
+                     max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu)));
+  }
+  for (int k = (k4 << 2) + int(threadIdx.x); k < K; k += blockDim.x)
+    mx = max(mx, __float_as_uint(row[k]) & 0x7fffffffu);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u;
+    v = __reduce_max_sync(0xffffffffu, v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const int e = scale_exp(red[0]);
+  if (threadIdx.x == 0) ea[m] = e;
+  uint16_t *hd = Ah + int64_t(m) * ldh, *ld = Al + int64_t(m) * ldh;
+  for (int i = threadIdx.x; i < k4; i += blockDim.x) {
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(row) + i);
+    uint16_t h[4], l[4];
+    split_f16(v.x, e, h[0], l[0]);
+    split_f16(v.y, e, h[1], l[1]);
+    split_f16(v.z, e, h[2], l[2]);
+    split_f16(v.w, e, h[3], l[3]);
+    __stcs(reinterpret_cast<uint2 *>(hd) + i,
+           make_uint2(h[0] | uint32_t(h[1]) << 16, h[2] | uint32_t(h[3]) << 16));
+    __stcs(reinterpret_cast<uint2 *>(ld) + i,
+           make_uint2(l[0] | uint32_t(l[1]) << 16, l[2] | uint32_t(l[3]) << 16));
+  }
+  for (int k = (k4 << 2) + int(threadIdx.x); k < K; k += blockDim.x) {
+    uint16_t h, l;
+    split_f16(row[k], e, h, l);
+    hd[k] = h;
+    ld[k] = l;
+  }
+}
+
+// B pass 1: per-column max |b| bits into bmax (zeroed before): a block covers 256 columns
+// (64 threads x 4) and 512 rows (4 row lanes), reduces in shared memory, one atomicMax per
+// column per block.
+constexpr int kPrepBRows = 512;
+__global__ void __launch_bounds__(256) prep16_bmax_kernel(const float *__restrict__ B, int64_t ldb,
+                                                          int K, int N, unsigned *__restrict__ bmax) {
+  __shared__ uint4 red[4][64];
+  const int cg = threadIdx.x & 63, rl = threadIdx.x >> 6;
+  const int n = (blockIdx.x * 64 + cg) * 4;
+  const int r0 = blockIdx.y * kPrepBRows;
+  const int r1 = min(K, r0 + kPrepBRows);
+  uint4 mx = make_uint4(0, 0, 0, 0);
+  if (n < N) {
+    for (int r = r0 + rl; r < r1; r += 4) {
+      const float *src = B + int64_t(r) * ldb + n;
+      float4 v;
+      if (n + 3 < N) {
+        v = __ldg(reinterpret_cast<const float4 *>(src));
+      } else {
+        v.x = src[0];
+        v.y = n + 1 < N ? src[1] : 0.f;
+        v.z = n + 2 < N ? src[2] : 0.f;
+        v.w = 0.f;
+      }
+      mx.x = max(mx.x, __float_as_uint(v.x) & 0x7fffffffu);
+      mx.y = max(mx.y, __float_as_uint(v.y) & 0x7fffffffu);
+      mx.z = max(mx.z, __float_as_uint(v.z) & 0x7fffffffu);
+      mx.w = max(mx.w, __float_as_uint(v.w) & 0x7fffffffu);
+    }
+  }
+  red[rl][cg] = mx;
+  __syncthreads();
+  if (rl == 0 && n < N) {
+#pragma unroll
+    for (int q = 1; q < 4; ++q) {
+      const uint4 o = red[q][cg];
+      mx.x = max(mx.x, o.x);
+      mx.y = max(mx.y, o.y);
+      mx.z = max(mx.z, o.z);
+      mx.w = max(mx.w, o.w);
+    }
+    atomicMax(bmax + n, mx.x);
+    if (n + 1 < N) atomicMax(bmax + n + 1, mx.y);
+    if (n + 2 < N) atomicMax(bmax + n + 2, mx.z);
+    if (n + 3 < N) atomicMax(bmax + n + 3, mx.w);
+  }
+}
+
+// B pass 2: eb[j] for every padded column (bmax of padding columns is 0 -> exponent 0).
+__global__ void prep16_bexp_kernel(const unsigned *__restrict__ bmax, int n_pad,
+                                   int *__restrict__ eb) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n_pad) eb[j] = scale_exp(bmax[j]);
+}
+
+// B pass 3: B_hi / B_lo (fp16, K x N row-major, row stride ldh). Thread = 4 columns x 8 rows.
+__global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__ B, int64_t ldb,
+                                                       int K, int N, const int *__restrict__ eb,
+                                                       uint16_t *__restrict__ Bh,
+                                                       uint16_t *__restrict__ Bl, int64_t ldh) {
+  const int n4 = (N + 3) >> 2, kb8 = (K + 7) >> 3;
+  const int64_t total = int64_t(kb8) * n4;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int kb = int(i / n4), n = int(i - int64_t(kb) * n4) * 4;
+    const int4 e = *reinterpret_cast<const int4 *>(eb + n);  // eb is padded to 256 columns
+    for (int k = kb * 8; k < min(K, kb * 8 + 8); ++k) {
+      const float *src = B + int64_t(k) * ldb + n;
+      uint16_t h[4], l[4];
+      if (n + 3 < N) {
+        const float4 v = __ldcs(reinterpret_cast<const float4 *>(src));
+        split_f16(v.x, e.x, h[0], l[0]);
+        split_f16(v.y, e.y, h[1], l[1]);
+        split_f16(v.z, e.z, h[2], l[2]);
+        split_f16(v.w, e.w, h[3], l[3]);
+        uint16_t *hd = Bh + int64_t(k) * ldh + n, *ld = Bl + int64_t(k) * ldh + n;
+        __stcs(reinterpret_cast<uint2 *>(hd),
+               make_uint2(h[0] | uint32_t(h[1]) << 16, h[2] | uint32_t(h[3]) << 16));
+        __stcs(reinterpret_cast<uint2 *>(ld),
+               make_uint2(l[0] | uint32_t(l[1]) << 16, l[2] | uint32_t(l[3]) << 16));
+      } else {
+        const int ev[4] = {e.x, e.y, e.z, e.w};
+        for (int q = 0; q < 4 && n + q < N; ++q) {
+          split_f16(src[q], ev[q], h[q], l[q]);
+          Bh[int64_t(k) * ldh + n + q] = h[q];
+          Bl[int64_t(k) * ldh + n + q] = l[q];
+        }
+      }
+    }
+  }
+}
+
 // ---- host side ----------------------------------------------------------------------------
 // Promotion interval: kDefaultPromoteKBlocks, overridable once per process with the
 // GIGA_PROMOTE_KBLOCKS environment variable (0 = never promote; tests / sweeps only).
@@ -986,7 +1237,9 @@ int default_promote_kblocks(int terms) {
     return -1;
   }();
   if (v >= 0) return v;
-  return terms == 2 ? kDefaultPromoteKBlocksT2 : kDefaultPromoteKBlocks;
+  return terms == 2 ? kDefaultPromoteKBlocksT2
+         : terms == 4 ? kDefaultPromoteKBlocksT4
+                      : kDefaultPromoteKBlocks;
 }
 
 static int forced_scheme() {
@@ -994,6 +1247,7 @@ static int forced_scheme() {
     const char *e = getenv("GIGA_SCHEME");
     if (e && strcmp(e, "3xtf32") == 0) return 3;
     if (e && strcmp(e, "tf32bf16") == 0) return 2;
+    if (e && strcmp(e, "3xfp16") == 0) return 4;
     return 0;
   }();
   return forced;
@@ -1065,15 +1319,16 @@ static bool make_map(CUtensorMap *m, const float *ptr, uint64_t cols, uint64_t r
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// 2-D bf16 map (B' of the TF32 + BF16 scheme), 128B swizzle.
+// 2-D 16-bit map (bf16: A' / B' of the TF32 + BF16 scheme; fp16: the 3xFP16 operands).
 static bool make_map_bf16(CUtensorMap *m, const uint16_t *ptr, uint64_t cols, uint64_t rows,
                           uint64_t ld, uint32_t box_cols, uint32_t box_rows,
-                          CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+                          CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B,
+                          CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   const cuuint64_t dims[2] = {cols, rows};
   const cuuint64_t strides[1] = {ld * sizeof(uint16_t)};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t *>(ptr), dims,
+  return g_encode(m, dt, 2, const_cast<uint16_t *>(ptr), dims,
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
@@ -1257,6 +1512,7 @@ struct ScratchBuf {
   size_t bytes;
   const float *key_b;
   int64_t key_ldb, key_k, key_n;
+  int key_scheme;
 };
 static std::list<ScratchBuf> g_bpre;
 
@@ -1281,7 +1537,7 @@ static ScratchBuf *bpre_scratch(cudaStream_t st, size_t bytes) {
     cudaGetLastError();
     return nullptr;
   }
-  g_bpre.push_back({st, dev, p, bytes, nullptr, 0, 0, 0});
+  g_bpre.push_back({st, dev, p, bytes, nullptr, 0, 0, 0, 0});
   return &g_bpre.back();
 }
 
@@ -1317,7 +1573,7 @@ void release_gemm_caches() {
 }
 
 GemmSchedule gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int cta_group,
-                           bool plain, int p_kb) {
+                           bool plain, int p_kb, int bk) {
   GemmSchedule s;
   s.cg = (cta_group == 1 || cta_group == 2) ? cta_group : choose_cta_group(M, N, num_sms);
   const int tile_m = cfg::BM * s.cg;
@@ -1325,7 +1581,7 @@ GemmSchedule gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int cta
   s.n_tiles = int((N + cfg::BN - 1) / cfg::BN);
   s.num_tiles = s.m_tiles * s.n_tiles;
   s.nclu = s.cg == 2 ? num_sms / 2 : num_sms;
-  s.n_kb = int((K + cfg::BK - 1) / cfg::BK);
+  s.n_kb = int((K + bk - 1) / bk);
   if (p_kb <= 0 || p_kb > s.n_kb) p_kb = s.n_kb;
   // $GIGA_TAIL_SPLIT=0 disables the k-split
   static const bool split_env = [] {
@@ -1396,9 +1652,38 @@ static cudaError_t ensure_smem_attr() {
 }
 
 // ---- TF32 + BF16 operand preparation (terms = 2) ---------------------------------------------
-cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, TermsPrep *tp) {
+cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, TermsPrep *tp,
+                             int terms) {
   *tp = TermsPrep();
   if (ensure_tma_encoder() != 0) return cudaErrorNotSupported;
+  auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+  if (terms == 4) {
+    // 3xFP16: [B_hi | B_lo | eb | bmax | A_hi | A_lo | ea]; exponent arrays padded to whole
+    // 256-row / 256-column tiles (the epilogue reads them unguarded)
+    const int64_t ldah = (K + 7) / 8 * 8, ldbh = (N + 7) / 8 * 8;
+    const int64_t n_pad = (N + 255) / 256 * 256, m_pad = (M + 255) / 256 * 256;
+    const size_t bh = up(size_t(K) * ldbh * 2), ebb = up(size_t(n_pad) * 4);
+    const size_t ah = up(size_t(M) * ldah * 2), eab = up(size_t(m_pad) * 4);
+    ScratchBuf *sb = bpre_scratch(st, 2 * bh + 2 * ebb + 2 * ah + eab);
+    if (!sb) return cudaSuccess;
+    uint8_t *scr = static_cast<uint8_t *>(sb->p);
+    tp->scheme = 4;
+    tp->owner = sb;
+    tp->ldah = ldah;
+    tp->ldbh = ldbh;
+    tp->Bh = reinterpret_cast<uint16_t *>(scr);
+    tp->Bl = reinterpret_cast<uint16_t *>(scr + bh);
+    tp->eb = reinterpret_cast<int *>(scr + 2 * bh);
+    tp->bmax = reinterpret_cast<unsigned *>(scr + 2 * bh + ebb);
+    tp->Ah = reinterpret_cast<uint16_t *>(scr + 2 * bh + 2 * ebb);
+    tp->Al = reinterpret_cast<uint16_t *>(scr + 2 * bh + 2 * ebb + ah);
+    tp->ea = reinterpret_cast<int *>(scr + 2 * bh + 2 * ebb + 2 * ah);
+    tp->key_b = sb->key_scheme == 4 ? sb->key_b : nullptr;
+    tp->key_ldb = sb->key_ldb;
+    tp->key_k = sb->key_k;
+    tp->key_n = sb->key_n;
+    return cudaSuccess;
+  }
   // $GIGA_B_PRE=0: the transform warps build B' per tile (and A' too); $GIGA_A_PRE=0: A' only
   static const bool b_pre_env = [] {
     const char *e = getenv("GIGA_B_PRE");
@@ -1410,7 +1695,6 @@ cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, T
   }();
   if (!b_pre_env) return cudaSuccess;
   const int64_t k8 = (K + 7) / 8 * 8, ldx = (N + 7) / 8 * 8;
-  auto up = [](size_t b) { return (b + 255) / 256 * 256; };
   const size_t hi_b = up(size_t(K) * size_t(N) * 4), bx_b = up(size_t(2 * k8) * ldx * 2);
   const size_t hi_a = up(size_t(M) * size_t(K) * 4), ax_b = up(size_t(M) * size_t(2 * k8) * 2);
   ScratchBuf *sb = bpre_scratch(st, hi_b + bx_b + (a_pre_env ? hi_a + ax_b : 0));
@@ -1425,7 +1709,7 @@ cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, T
     tp->Ahi = reinterpret_cast<float *>(scr + hi_b + bx_b);
     tp->Ax = reinterpret_cast<uint16_t *>(scr + hi_b + bx_b + hi_a);
   }
-  tp->key_b = sb->key_b;
+  tp->key_b = sb->key_scheme == 2 ? sb->key_b : nullptr;
   tp->key_ldb = sb->key_ldb;
   tp->key_k = sb->key_k;
   tp->key_n = sb->key_n;
@@ -1433,7 +1717,43 @@ cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, T
 }
 
 bool TermsPrep::b_matches(const float *B, int64_t ldb, int64_t N, int64_t K) const {
-  return Bhi && key_b == B && key_ldb == ldb && key_k == K && key_n == N;
+  return (Bhi || Bh) && key_b == B && key_ldb == ldb && key_k == K && key_n == N;
+}
+
+cudaError_t launch_prep16_b(const float *B, int64_t ldb, int64_t N, int64_t K, TermsPrep *tp,
+                            cudaStream_t st) {
+  ScratchBuf *sb = static_cast<ScratchBuf *>(tp->owner);
+  const int64_t n_pad = (N + 255) / 256 * 256;
+  sb->key_b = nullptr;
+  cudaError_t e = cudaMemsetAsync(tp->bmax, 0, size_t(n_pad) * 4, st);
+  if (e != cudaSuccess) return e;
+  const dim3 g1(unsigned((N + 255) / 256), unsigned((K + kPrepBRows - 1) / kPrepBRows));
+  prep16_bmax_kernel<<<g1, 256, 0, st>>>(B, ldb, int(K), int(N), tp->bmax);
+  prep16_bexp_kernel<<<unsigned((n_pad + 255) / 256), 256, 0, st>>>(
+      tp->bmax, int(n_pad), const_cast<int *>(tp->eb));
+  const int64_t units = ((K + 7) / 8) * ((N + 3) / 4);
+  const int64_t blocks = std::min<int64_t>((units + 255) / 256, int64_t(num_sms_current()) * 8);
+  prep16_b_kernel<<<unsigned(std::max<int64_t>(blocks, 1)), 256, 0, st>>>(
+      B, ldb, int(K), int(N), tp->eb, const_cast<uint16_t *>(tp->Bh),
+      const_cast<uint16_t *>(tp->Bl), tp->ldbh);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  sb->key_b = tp->key_b = B;
+  sb->key_ldb = tp->key_ldb = ldb;
+  sb->key_k = tp->key_k = K;
+  sb->key_n = tp->key_n = N;
+  sb->key_scheme = 4;
+  return cudaSuccess;
+}
+
+cudaError_t launch_prep16_a(const float *A, int64_t lda, int64_t M, int64_t K, TermsPrep *tp,
+                            cudaStream_t st) {
+  const int64_t m_pad = (M + 255) / 256 * 256;
+  prep16_a_kernel<<<unsigned(m_pad), 512, 0, st>>>(A, lda, int(M), int(K),
+                                                   const_cast<uint16_t *>(tp->Ah),
+                                                   const_cast<uint16_t *>(tp->Al), tp->ldah,
+                                                   const_cast<int *>(tp->ea));
+  return cudaGetLastError();
 }
 
 cudaError_t launch_prep_b(const float *B, int64_t ldb, int64_t N, int64_t K, TermsPrep *tp,
@@ -1451,6 +1771,7 @@ cudaError_t launch_prep_b(const float *B, int64_t ldb, int64_t N, int64_t K, Ter
   sb->key_ldb = tp->key_ldb = ldb;
   sb->key_k = tp->key_k = K;
   sb->key_n = tp->key_n = N;
+  sb->key_scheme = 2;
   return cudaSuccess;
 }
 
@@ -1477,9 +1798,9 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
     return cudaErrorInvalidValue;
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || ldc > INT32_MAX)
     return cudaErrorInvalidValue;
-  if (terms != 1 && terms != 2 && terms != 3) return cudaErrorInvalidValue;
+  if (terms < 1 || terms > 4) return cudaErrorInvalidValue;
   if (terms == 3 && (!A_lo) != (!B_lo)) return cudaErrorInvalidValue;  // both or neither
-  if (terms == 2 && (A_lo || B_lo)) return cudaErrorInvalidValue;     // on chip only
+  if ((terms == 2 || terms == 4) && (A_lo || B_lo)) return cudaErrorInvalidValue;
   const bool lo_smem = terms == 3 && !A_lo;
   if (ensure_tma_encoder() != 0) return cudaErrorNotSupported;
 
@@ -1523,6 +1844,35 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.hi_rn = hi_rn_env;
   p.b_pre = 0;
   p.a_pre = 0;
+  p.ea = nullptr;
+  p.eb = nullptr;
+  // k-block width in elements of K: 16 (tf32 schemes), 32 (3xFP16)
+  const int bk = terms == 4 ? 32 : BK;
+  if (terms == 4) {
+    // scaled fp16 hi / lo operands (the caller's TermsPrep, else prepared here)
+    TermsPrep local;
+    const TermsPrep *tp = ex->prep;
+    if (!tp || tp->scheme != 4) {
+      cudaError_t e = terms_prep_alloc(M, N, K, st, &local, 4);
+      if (e == cudaSuccess && !local.Bh) e = cudaErrorMemoryAllocation;
+      if (e == cudaSuccess && !(ex->b_prep_reuse && local.b_matches(B, ldb, N, K)))
+        e = launch_prep16_b(B, ldb, N, K, &local, st);
+      if (e == cudaSuccess) e = launch_prep16_a(A, lda, M, K, &local, st);
+      if (e != cudaSuccess) return e;
+      tp = &local;
+    }
+    if (!make_map_bf16(&tA, tp->Ah, K, M, tp->ldah, 32, BM, CU_TENSOR_MAP_SWIZZLE_64B,
+                       CU_TENSOR_MAP_DATA_TYPE_FLOAT16) ||
+        !make_map_bf16(&tAlo, tp->Al, K, M, tp->ldah, 32, BM, CU_TENSOR_MAP_SWIZZLE_64B,
+                       CU_TENSOR_MAP_DATA_TYPE_FLOAT16) ||
+        !make_map_bf16(&tB, tp->Bh, N, K, tp->ldbh, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_DATA_TYPE_FLOAT16) ||
+        !make_map_bf16(&tBlo, tp->Bl, N, K, tp->ldbh, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
+      return cudaErrorInvalidValue;
+    p.ea = tp->ea;
+    p.eb = tp->eb;
+  }
   if (terms == 2) {
     // operands prepared in HBM (the caller's TermsPrep, else here, untimed)
     TermsPrep local;
@@ -1549,11 +1899,11 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
       p.b_pre = 1;
     }
   }
-  p.n_kb = int((K + BK - 1) / BK);
+  p.n_kb = int((K + bk - 1) / bk);
   int pk = promote_kblocks < 0 ? default_promote_kblocks(terms) : promote_kblocks;
   p.p_kb = (pk == 0 || pk > p.n_kb) ? p.n_kb : pk;
   const bool plain = !p.accumulate && !p.load_c && ex->n_peer_c == 0;
-  const GemmSchedule sch = gemm_schedule(M, N, K, num_sms, cg, plain, p.p_kb);
+  const GemmSchedule sch = gemm_schedule(M, N, K, num_sms, cg, plain, p.p_kb, bk);
   p.m_tiles = sch.m_tiles;
   p.n_tiles = sch.n_tiles;
   p.num_tiles = sch.num_tiles;

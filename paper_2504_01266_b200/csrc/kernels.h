@@ -12,6 +12,8 @@ namespace giga {
 // bound, so it keeps 8 too.
 constexpr int kDefaultPromoteKBlocks = 8;
 constexpr int kDefaultPromoteKBlocksT2 = 8;
+// The 3xFP16 scheme (terms = 4) runs 32-wide k-blocks: 4 of them = K 128 per TMEM partial.
+constexpr int kDefaultPromoteKBlocksT4 = 4;
 
 // The promotion interval in effect for `terms` (the defaults above or $GIGA_PROMOTE_KBLOCKS).
 int default_promote_kblocks(int terms = 3);
@@ -55,6 +57,14 @@ struct TermsPrep {
   const float *Ahi = nullptr, *Bhi = nullptr;
   const uint16_t *Ax = nullptr, *Bx = nullptr;
   int64_t k8 = 0, ldbx = 0;
+  // 3xFP16 scheme (terms = 4): fp16 hi / lo of the power-of-two scaled operands, row-major
+  // (A: M x K, row stride ldah; B: K x N, row stride ldbh), and the scale exponents: row i
+  // of A was scaled by 2^-ea[i], column j of B by 2^-eb[j]
+  const uint16_t *Ah = nullptr, *Al = nullptr, *Bh = nullptr, *Bl = nullptr;
+  const int *ea = nullptr, *eb = nullptr;
+  unsigned *bmax = nullptr;  // per-column max |b| bits (preparation scratch)
+  int64_t ldah = 0, ldbh = 0;
+  int scheme = 2;
   void *owner = nullptr;
   const float *key_b = nullptr;
   int64_t key_ldb = 0, key_k = 0, key_n = 0;
@@ -62,11 +72,18 @@ struct TermsPrep {
 };
 // Reserve the scratch for an M x N x K product on `st` (pointers stay null when it cannot be
 // had: stream capture, OOM, $GIGA_B_PRE=0), then prepare B and A into it (stream-ordered).
-cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, TermsPrep *tp);
+cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, TermsPrep *tp,
+                             int terms = 2);
 cudaError_t launch_prep_b(const float *B, int64_t ldb, int64_t N, int64_t K, TermsPrep *tp,
                           cudaStream_t st);
 cudaError_t launch_prep_a(const float *A, int64_t lda, int64_t M, int64_t K, TermsPrep *tp,
                           cudaStream_t st);
+// Operand preparation of the 3xFP16 scheme (terms = 4): per-row exponents of A / per-column
+// exponents of B and the fp16 hi / lo arrays of the scaled operands (stream-ordered).
+cudaError_t launch_prep16_b(const float *B, int64_t ldb, int64_t N, int64_t K, TermsPrep *tp,
+                            cudaStream_t st);
+cudaError_t launch_prep16_a(const float *A, int64_t lda, int64_t M, int64_t K, TermsPrep *tp,
+                            cudaStream_t st);
 struct GemmExtra {
   int64_t lda = 0, ldb = 0;
   int accumulate = 0;
@@ -110,7 +127,7 @@ struct GemmSchedule {
   int cg, m_tiles, n_tiles, num_tiles, nclu, n_kb, first_split, s, mode, num_units;
 };
 GemmSchedule gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int cta_group,
-                           bool plain, int p_kb);
+                           bool plain, int p_kb, int bk = 16);
 // Workspace of the K-split partials for launches on `st` (current device); false when it
 // cannot be had (stream capture, out of memory): the launch then runs whole tiles.
 bool ksplit_workspace(cudaStream_t st, size_t ws_bytes, size_t cnt_n, float **ws,

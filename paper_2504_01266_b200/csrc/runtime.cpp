@@ -173,6 +173,20 @@ int run_gemm(const float *A, const float *Alo, const float *B, const float *Blo,
   int terms = product_terms(Alo, std::max(M, ex.rows_hint), N, K);
   GemmExtra e = ex;
   TermsPrep tp;
+  if (terms == 4) {
+    // 3xFP16: scaled fp16 hi / lo operands prepared in HBM
+    const int64_t lda = e.lda ? e.lda : K, ldb = e.ldb ? e.ldb : N;
+    CK(terms_prep_alloc(M, N, K, st, &tp, 4));
+    if (!tp.Bh) {
+      if (scheme_forced()) return fail(GIGA_ERR_OOM, "3xFP16 operand scratch unavailable");
+      terms = 3;
+    } else {
+      if (!(e.b_prep_reuse && tp.b_matches(B, ldb, N, K)))
+        CK(timed(1, st, [&] { return launch_prep16_b(B, ldb, N, K, &tp, st); }));
+      CK(timed(1, st, [&] { return launch_prep16_a(A, lda, M, K, &tp, st); }));
+      e.prep = &tp;
+    }
+  }
   if (terms == 2) {
     const int64_t lda = e.lda ? e.lda : K, ldb = e.ldb ? e.ldb : N;
     CK(terms_prep_alloc(M, N, K, st, &tp));

@@ -106,6 +106,8 @@ def test_concurrent_launches_on_two_streams(env):
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
     ref1 = torch.empty((M, N), device="cuda")
     ref2 = torch.empty((M, N), device="cuda")
+    # the inputs were generated on the default stream; torch's side streams do not wait for it
+    torch.cuda.synchronize()
     _gemm(torch, dbg, A, B, ref1, 3, 0, s1)
     _gemm(torch, dbg, A2, B, ref2, 3, 0, s1)
     torch.cuda.synchronize()
