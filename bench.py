@@ -40,6 +40,19 @@ CONFIGS = {
 # The north_star's targets are quoted on 32768^3 (>= 60% of the 8-GPU roofline, >= 6.5x from 1
 # to 8 GPUs); it fits one GPU, so it is the default workload at every N (strong scaling).
 DEFAULT_CONFIG = "c5_32768"
+# the shard GEMM's fp32-accurate schemes (giga_product_scheme): MMA instruction times per k8
+# step in TF32 units, names, what they compute
+SCHEME_WEIGHT = {1: 1.0, 2: 2.0, 3: 3.0, 4: 1.5}
+SCHEME_NAME = {1: "TF32", 2: "TF32+BF16", 3: "3xTF32", 4: "3xFP16"}
+SCHEME_ARITH = {
+    1: "plain TF32 tcgen05 MMAs (not fp32-accurate)",
+    2: "TF32 + BF16 tcgen05 MMAs (a_hi b_hi in TF32, a_lo b + a_hi b_lo in one K=16 BF16 MMA; "
+       "operands prepared in HBM per call)",
+    3: "3xTF32 tcgen05 MMAs",
+    4: "3xFP16 tcgen05 MMAs (the 3xTF32 split a_lo b_hi + a_hi b_lo + a_hi b_hi on fp16 "
+       "operands of power-of-two scaled rows of A / columns of B, prepared in HBM per call; "
+       "exceptions fixed in fp64)"}
+FILL_PEAK_GBPS = 12829.1  # profiles/r02_tma_fill_sweep.jsonl (max over the sweep)
 METRIC = "GEMM TFLOP/s (fp32-accurate) at 1/2/4/8 B200 and % of TF32 tensor roofline"
 
 
@@ -405,20 +418,21 @@ def main():
     tf32_sustained = 0.5 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     tf32_burst = 0.5 * peaks["bf16_tflops"]
     launches = rank_launches(giga, M, N, K, world, rank)
-    # algorithmic tensor work per step in TF32-instruction-equivalent flops: 3xTF32 issues 3
-    # TF32 MMAs per logical product (6 r N K per launch), TF32 + BF16 one TF32 MMA plus one
-    # BF16 MMA of twice the depth at twice the rate (4 r N K)
-    tensor_flops = sum((3 if t == 3 else 2) * 2.0 * r * N * kc for r, kc, t in launches)
+    # algorithmic tensor work per step in TF32-instruction-equivalent flops (MMA instruction
+    # times x the TF32 rate): 3xTF32 issues 3 TF32 MMAs per logical product (6 r N K per
+    # launch), TF32 + BF16 one TF32 MMA plus one BF16 MMA of twice the depth at twice the rate
+    # (4 r N K), 3xFP16 three FP16 MMAs of twice the depth at twice the rate (3 r N K)
+    tensor_flops = sum(SCHEME_WEIGHT[t] * 2.0 * r * N * kc for r, kc, t in launches)
     terms_set = sorted({t for _, _, t in launches})
     gemm_ms_step = kt["gemm_ms"] / args.steps  # all of this rank's GEMM launches in a step
     achieved = tensor_flops / (gemm_ms_step * 1e-3) / 1e12 if gemm_ms_step > 0 else None
-    scheme = "+".join("3xTF32" if t == 3 else "TF32+BF16" for t in terms_set)
+    scheme = "+".join(SCHEME_NAME[t] for t in terms_set)
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if world == 1 and os.path.exists(tp):
         try:
             with open(tp) as f:
-                traffic = json.load(f).get(args.config)
+                traffic = json.load(f).get(f"{args.config}:{scheme}")
             traffic_src = ("profiles/gemm_traffic.json: dram__bytes_read.sum + "
                            "dram__bytes_write.sum of one launch from an ncu --set full capture "
                            "of this kernel and config (not measured in this run)")
@@ -440,26 +454,47 @@ def main():
             "scheme": scheme,
             "limit_note": ("tensor pipe (3 TF32 MMAs per k8 step) at the power-capped clock"
                            if terms_set == [3] else
+                           "tensor pipe (3 FP16 MMAs per k16 step) at the power-capped clock"
+                           if terms_set == [4] else
                            "operand feed: 32 KiB of TMA fills per CTA per 2-MMA stage against "
                            "the per-SM fill ceiling (roofline.feed; multicast measured not to "
                            "raise it), and the power cap: DESIGN.md 6.7"),
             "prep_ms_per_step": round(kt["split_ms"] / args.steps, 4),
             "prep_launches_per_step": round(kt["split_launches"] / args.steps, 2)}
-    if 2 in terms_set:
+    if terms_set == [4] and achieved:
+        # one scheme, one dtype: state the kernel in its own units -- fp16 tensor flops (three
+        # FP16 products per logical product: 6 r N K per launch) against the dense FP16 / BF16
+        # peak (the same rate), i.e. the same fraction as the TF32-equivalent accounting
+        f16 = 2.0 * achieved
+        roof.update({"achieved": round(f16, 2), "peak": round(2 * tf32_sustained, 1),
+                     "frac": round(f16 / (2 * tf32_sustained), 4),
+                     "frac_vs_burst": round(f16 / (2 * tf32_burst), 4), "dtype": "f16",
+                     "peak_note": f"dense FP16 = BF16 rate: {peak_src} cuBLAS bf16 sustained "
+                                  f"({peaks.get('bf16_tflops_sustained')}; burst "
+                                  f"{peaks['bf16_tflops']}); achieved = 3 FP16 products x 2 rows "
+                                  f"N K per launch / event time of the GEMM launches of a step"})
+    if 2 in terms_set or 4 in terms_set:
         # the prepared TF32 + BF16 kernel's operand feed: 64 KiB of fills per 256 x 256 pair
         # tile and 16-deep k-block = r N K / 16 bytes per launch, against the measured L2 -> SM
         # TMA fill ceiling (scripts/tma_box_bench.cu: 10.7 TB/s on a 148-SM B200 for every box
         # shape; scripts/tma_mcast_bench.cu: multicast does not raise per-SM ingress)
-        feed_bytes = sum(r * N * kc / 16.0 for r, kc, t in launches if t == 2)
-        t2_flops = sum(4.0 * r * N * kc for r, kc, t in launches if t == 2)
-        feed_ms = gemm_ms_step * t2_flops / tensor_flops
+        # (3xFP16: 64 KiB per pair tile and 32-deep k-block = r N K / 32 bytes per launch)
+        feed_bytes = sum(r * N * kc / (16.0 if t == 2 else 32.0)
+                         for r, kc, t in launches if t in (2, 4))
+        fed_flops = sum(SCHEME_WEIGHT[t] * 2.0 * r * N * kc for r, kc, t in launches
+                        if t in (2, 4))
+        feed_ms = gemm_ms_step * fed_flops / tensor_flops
         feed_ach = feed_bytes / (feed_ms * 1e-3) / 1e9 if feed_ms > 0 else None
         roof["feed"] = {"bound": "l2_to_smem_tma",
                         "achieved": round(feed_ach, 1) if feed_ach else None,
-                        "peak": 10714.0, "unit": "GB/s",
-                        "frac": round(feed_ach / 10714.0, 4) if feed_ach else None,
+                        "peak": FILL_PEAK_GBPS, "unit": "GB/s",
+                        "frac": round(feed_ach / FILL_PEAK_GBPS, 4) if feed_ach else None,
                         "bytes_per_step": feed_bytes,
-                        "peak_source": "measured TMA fill ceiling, scripts/tma_box_bench.cu"}
+                        "peak_source": "highest TMA fill rate measured in isolation "
+                                       "(scripts/tma_fill_sweep.cu, "
+                                       "profiles/r02_tma_fill_sweep.jsonl: 12.8 TB/s both with 3 "
+                                       "CTAs per SM x 2 x 32 KiB stages of 8 KiB boxes and with "
+                                       "1 CTA per SM x 3 x 64 KiB stages of 32 KiB boxes)"}
 
     # ---- whole-step roofline: T_roof / t with T_roof = max(T_comp, T_comm),
     #      T_comp = the scheme's tensor work of the largest shard at the TF32 peak,
@@ -468,7 +503,7 @@ def main():
     bw_nv = 770e9  # measured NVLink peer-copy GB/s per direction (B200_PROFILING.md)
     t_comm = 4.0 * ((K * N if world > 1 else 0) + (M - min(rows_all)) * N) / bw_nv
     w_max = max(range(world), key=lambda g: rows_all[g])
-    tf_max = sum((3 if t == 3 else 2) * 2.0 * r * N * kc
+    tf_max = sum(SCHEME_WEIGHT[t] * 2.0 * r * N * kc
                  for r, kc, t in rank_launches(giga, M, N, K, world, w_max))
     t_comp = tf_max / (tf32_sustained * 1e12)
     t_comp3 = 2.0 * max(rows_all) * N * K / (tf32_sustained * 1e12 / 3)
@@ -482,8 +517,8 @@ def main():
                  "frac": round(t_roof / (ms_step * 1e-3), 4),
                  "frac_vs_3xtf32_ceiling": round(max(t_comp3, t_comm) / (ms_step * 1e-3), 4),
                  "note": "frac_vs_3xtf32_ceiling is the north_star's reading (P_tf32 / 3 per "
-                         "logical product); above 1 when a launch runs the 2-MMA TF32 + BF16 "
-                         "scheme"}
+                         "logical product); above 1 when a launch runs a scheme cheaper than "
+                         "3xTF32 (TF32 + BF16: 2 MMA times per k8 step, 3xFP16: 1.5)"}
 
     # ---- end to end: host buffers through the C ABI ----
     e2e = None
@@ -515,9 +550,7 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": vs_base,
             "wall_ms_per_step": round(wall_ms / args.steps, 4),
             "dtype": "f32",
-            "arithmetic": ("3xTF32 tcgen05 MMAs" if terms_set == [3] else
-                           "TF32 + BF16 tcgen05 MMAs (a_hi b_hi in TF32, a_lo b + a_hi b_lo in one "
-                           "K=16 BF16 MMA; operands prepared in HBM per call)")
+            "arithmetic": " / ".join(SCHEME_ARITH[t] for t in terms_set)
                           + " + fp32 RN promotion (fp32-accurate: <= 1e-5 sum|A||B|)",
             "data": "synthetic",
             "config": {"workload": f"{args.config} M={M} N={N} K={K}", "dist": args.dist,

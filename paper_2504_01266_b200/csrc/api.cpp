@@ -784,7 +784,7 @@ int giga_timing_read(double *gemm_ms, int64_t *gemm_launches, double *split_ms,
       cudaGetLastError();
     } else {
       g_tms[r.kind] += ms;
-      g_tcount[r.kind] += 1;
+      g_tcount[r.kind] += r.n;
     }
     g_tpool.push_back({r.dev, r.a});
     g_tpool.push_back({r.dev, r.b});

@@ -1068,84 +1068,123 @@ __device__ __forceinline__ int scale_exp(uint32_t maxbits) {
   if (maxbits == 0u || maxbits >= 0x7f800000u) return 0;
   return ilogbf(__uint_as_float(maxbits)) - 14;
 }
-__device__ __forceinline__ void split_f16(float x, int e, uint16_t &h, uint16_t &l) {
-  const float xs = ldexpf(x, -e);
+// Returns true when x is an *exception*: its representation 2^e (hi + lo) is off by more than
+// 2^-20 |x| (elements more than ~2^20 below their row's / column's maximum, where fp16's
+// subnormal floor cuts lo). Exceptions are recorded in a bitmap and their remainders added to
+// C by fix16_a_kernel / fix16_b_kernel, so every product keeps a split error <= 2 * 2^-20 +
+// 2^-22 relative. In the scaled domain x' - hi and (x' - hi) - lo are exact in fp32; x' itself
+// is exact unless it underflows fp32 (then hi = lo = 0 and x != 0 flags it). NaN / Inf are
+// never exceptions (the GEMM propagates them).
+__device__ __forceinline__ bool split_f16(float x, int e, uint16_t &h, uint16_t &l) {
+  // x 2^-e: one multiplication by the power of two when it is a normal float (ldexpf otherwise)
+  const float xs = (e >= -126 && e <= 126) ? x * __int_as_float((127 - e) << 23) : ldexpf(x, -e);
   const __half hh = __float2half_rn(xs);
-  const __half ll = __float2half_rn(__fsub_rn(xs, __half2float(hh)));
+  const float r = __fsub_rn(xs, __half2float(hh));
+  const __half ll = __float2half_rn(r);
   h = __half_as_ushort(hh);
   l = __half_as_ushort(ll);
+  const float err = fabsf(__fsub_rn(r, __half2float(ll)));
+  return err > 0x1p-20f * fabsf(xs) || (xs == 0.0f && x != 0.0f);
+}
+// Exception bitmaps: bit k of row i of A at word i * wa + k / 32; bit j of row k of B at word
+// (j / 32) * K + k (strip-major: fix16_b reads a strip's words contiguously). flag arrays: 1 for a row of A / column of B holding any exception.
+__device__ __forceinline__ void mark_exception(unsigned *bits, int64_t word, int bit,
+                                               int *flag) {
+  atomicOr(bits + word, 1u << bit);
+  *reinterpret_cast<volatile int *>(flag) = 1;
 }
 
-// A: one block per row (rows >= M only write their exponent 0: ea is padded to whole tiles).
-// Pass 1: max |a| of the row (bit patterns: NaN > Inf > finite); pass 2 re-reads the row
-// (L2-resident) and writes A_hi / A_lo (fp16, row stride ldh). 4 B read (+ the L2 re-read),
-// 4 B written per element.
+// A: TPR threads per row (512: one row per block for long rows, whose second read then hits
+// L2; 32: one warp per row), row groups grid-strided; padding rows (M <= m < m_pad) only write
+// their exponent 0 (ea is padded to whole tiles). Pass 1: max |a| of the row (bit patterns:
+// NaN > Inf > finite); pass 2 re-reads the row and writes A_hi / A_lo (fp16, row stride ldh)
+// and the row's exceptions. 4 B read (+ the re-read), 4 B written per element.
+template <int TPR>
 __global__ void __launch_bounds__(512) prep16_a_kernel(const float *__restrict__ A, int64_t lda,
-                                                       int M, int K, uint16_t *__restrict__ Ah,
+                                                       int M, int m_pad, int K,
+                                                       uint16_t *__restrict__ Ah,
                                                        uint16_t *__restrict__ Al, int64_t ldh,
-                                                       int *__restrict__ ea) {
+                                                       int *__restrict__ ea,
+                                                       unsigned *__restrict__ bits, int wa,
+                                                       int *__restrict__ flag) {
+  constexpr int RPB = 512 / TPR;
   __shared__ uint32_t red[16];
-  const int m = blockIdx.x;
-  if (m >= M) {
-    if (threadIdx.x == 0) ea[m] = 0;
-    return;
-  }
-  const float *row = A + int64_t(m) * lda;
+  const int t = int(threadIdx.x) % TPR, rsub = int(threadIdx.x) / TPR;
   const int k4 = K >> 2;
-  uint32_t mx = 0;
-  for (int i = threadIdx.x; i < k4; i += blockDim.x) {
-    const float4 v = __ldg(reinterpret_cast<const float4 *>(row) + i);
-    mx = max(mx, max(max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu),
-                     max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu)));
-  }
-  for (int k = (k4 << 2) + int(threadIdx.x); k < K; k += blockDim.x)
-    mx = max(mx, __float_as_uint(row[k]) & 0x7fffffffu);
-  mx = __reduce_max_sync(0xffffffffu, mx);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    uint32_t v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u;
-    v = __reduce_max_sync(0xffffffffu, v);
-    if (threadIdx.x == 0) red[0] = v;
-  }
-  __syncthreads();
-  const int e = scale_exp(red[0]);
-  if (threadIdx.x == 0) ea[m] = e;
-  uint16_t *hd = Ah + int64_t(m) * ldh, *ld = Al + int64_t(m) * ldh;
-  for (int i = threadIdx.x; i < k4; i += blockDim.x) {
-    const float4 v = __ldg(reinterpret_cast<const float4 *>(row) + i);
-    uint16_t h[4], l[4];
-    split_f16(v.x, e, h[0], l[0]);
-    split_f16(v.y, e, h[1], l[1]);
-    split_f16(v.z, e, h[2], l[2]);
-    split_f16(v.w, e, h[3], l[3]);
-    __stcs(reinterpret_cast<uint2 *>(hd) + i,
-           make_uint2(h[0] | uint32_t(h[1]) << 16, h[2] | uint32_t(h[3]) << 16));
-    __stcs(reinterpret_cast<uint2 *>(ld) + i,
-           make_uint2(l[0] | uint32_t(l[1]) << 16, l[2] | uint32_t(l[3]) << 16));
-  }
-  for (int k = (k4 << 2) + int(threadIdx.x); k < K; k += blockDim.x) {
-    uint16_t h, l;
-    split_f16(row[k], e, h, l);
-    hd[k] = h;
-    ld[k] = l;
+  for (int g = blockIdx.x; g * RPB < m_pad; g += gridDim.x) {
+    const int m = g * RPB + rsub;
+    const bool live = m < M;
+    const float *row = A + int64_t(live ? m : 0) * lda;
+    uint32_t mx = 0;
+    if (live) {
+      for (int i = t; i < k4; i += TPR) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(row) + i);
+        mx = max(mx, max(max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu),
+                         max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu)));
+      }
+      for (int k = (k4 << 2) + t; k < K; k += TPR) mx = max(mx, __float_as_uint(row[k]) & 0x7fffffffu);
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (TPR > 32) {
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        uint32_t v = threadIdx.x < (TPR >> 5) ? red[threadIdx.x] : 0u;
+        v = __reduce_max_sync(0xffffffffu, v);
+        if (threadIdx.x == 0) red[0] = v;
+      }
+      __syncthreads();
+      mx = red[0];
+      __syncthreads();  // red is reused by the next row group
+    }
+    if (m >= m_pad) continue;
+    const int e = live ? scale_exp(mx) : 0;
+    if (t == 0) ea[m] = e;
+    if (!live) continue;
+    uint16_t *hd = Ah + int64_t(m) * ldh, *ld = Al + int64_t(m) * ldh;
+    for (int i = t; i < k4; i += TPR) {
+      const float4 v = __ldg(reinterpret_cast<const float4 *>(row) + i);
+      uint16_t h[4], l[4];
+      const bool x0 = split_f16(v.x, e, h[0], l[0]);
+      const bool x1 = split_f16(v.y, e, h[1], l[1]);
+      const bool x2 = split_f16(v.z, e, h[2], l[2]);
+      const bool x3 = split_f16(v.w, e, h[3], l[3]);
+      if (x0 | x1 | x2 | x3) {
+        const unsigned nib =
+            unsigned(x0) | unsigned(x1) << 1 | unsigned(x2) << 2 | unsigned(x3) << 3;
+        const int k = 4 * i;
+        atomicOr(bits + int64_t(m) * wa + (k >> 5), nib << (k & 31));
+        *reinterpret_cast<volatile int *>(flag + m) = 1;
+      }
+      __stcs(reinterpret_cast<uint2 *>(hd) + i,
+             make_uint2(h[0] | uint32_t(h[1]) << 16, h[2] | uint32_t(h[3]) << 16));
+      __stcs(reinterpret_cast<uint2 *>(ld) + i,
+             make_uint2(l[0] | uint32_t(l[1]) << 16, l[2] | uint32_t(l[3]) << 16));
+    }
+    for (int k = (k4 << 2) + t; k < K; k += TPR) {
+      uint16_t h, l;
+      if (split_f16(row[k], e, h, l))
+        mark_exception(bits, int64_t(m) * wa + (k >> 5), k & 31, flag + m);
+      hd[k] = h;
+      ld[k] = l;
+    }
   }
 }
 
-// B pass 1: per-column max |b| bits into bmax (zeroed before): a block covers 256 columns
-// (64 threads x 4) and 512 rows (4 row lanes), reduces in shared memory, one atomicMax per
-// column per block.
-constexpr int kPrepBRows = 512;
+// B pass 1: per-column max |b| bits into bmax (zeroed before): a block covers 128 columns
+// (32 threads x 4) and `rows` rows (8 row lanes), reduces in shared memory, one atomicMax
+// per column per block. rows is chosen so the grid is ~8 blocks per SM.
 __global__ void __launch_bounds__(256) prep16_bmax_kernel(const float *__restrict__ B, int64_t ldb,
-                                                          int K, int N, unsigned *__restrict__ bmax) {
-  __shared__ uint4 red[4][64];
-  const int cg = threadIdx.x & 63, rl = threadIdx.x >> 6;
-  const int n = (blockIdx.x * 64 + cg) * 4;
-  const int r0 = blockIdx.y * kPrepBRows;
-  const int r1 = min(K, r0 + kPrepBRows);
+                                                          int K, int N, int rows,
+                                                          unsigned *__restrict__ bmax) {
+  __shared__ uint4 red[8][32];
+  const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int n = (blockIdx.x * 32 + cg) * 4;
+  const int r0 = blockIdx.y * rows;
+  const int r1 = min(K, r0 + rows);
   uint4 mx = make_uint4(0, 0, 0, 0);
   if (n < N) {
-    for (int r = r0 + rl; r < r1; r += 4) {
+    for (int r = r0 + rl; r < r1; r += 8) {
       const float *src = B + int64_t(r) * ldb + n;
       float4 v;
       if (n + 3 < N) {
@@ -1166,7 +1205,7 @@ __global__ void __launch_bounds__(256) prep16_bmax_kernel(const float *__restric
   __syncthreads();
   if (rl == 0 && n < N) {
 #pragma unroll
-    for (int q = 1; q < 4; ++q) {
+    for (int q = 1; q < 8; ++q) {
       const uint4 o = red[q][cg];
       mx.x = max(mx.x, o.x);
       mx.y = max(mx.y, o.y);
@@ -1191,7 +1230,9 @@ __global__ void prep16_bexp_kernel(const unsigned *__restrict__ bmax, int n_pad,
 __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__ B, int64_t ldb,
                                                        int K, int N, const int *__restrict__ eb,
                                                        uint16_t *__restrict__ Bh,
-                                                       uint16_t *__restrict__ Bl, int64_t ldh) {
+                                                       uint16_t *__restrict__ Bl, int64_t ldh,
+                                                       unsigned *__restrict__ bits, int wb,
+                                                       int *__restrict__ flag) {
   const int n4 = (N + 3) >> 2, kb8 = (K + 7) >> 3;
   const int64_t total = int64_t(kb8) * n4;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
@@ -1203,10 +1244,20 @@ __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__
       uint16_t h[4], l[4];
       if (n + 3 < N) {
         const float4 v = __ldcs(reinterpret_cast<const float4 *>(src));
-        split_f16(v.x, e.x, h[0], l[0]);
-        split_f16(v.y, e.y, h[1], l[1]);
-        split_f16(v.z, e.z, h[2], l[2]);
-        split_f16(v.w, e.w, h[3], l[3]);
+        const bool x0 = split_f16(v.x, e.x, h[0], l[0]);
+        const bool x1 = split_f16(v.y, e.y, h[1], l[1]);
+        const bool x2 = split_f16(v.z, e.z, h[2], l[2]);
+        const bool x3 = split_f16(v.w, e.w, h[3], l[3]);
+        if (x0 | x1 | x2 | x3) {
+          const unsigned nib =
+              unsigned(x0) | unsigned(x1) << 1 | unsigned(x2) << 2 | unsigned(x3) << 3;
+          atomicOr(bits + int64_t(n >> 5) * K + k, nib << (n & 31));
+          volatile int *f = flag + n;
+          if (x0) f[0] = 1;
+          if (x1) f[1] = 1;
+          if (x2) f[2] = 1;
+          if (x3) f[3] = 1;
+        }
         uint16_t *hd = Bh + int64_t(k) * ldh + n, *ld = Bl + int64_t(k) * ldh + n;
         __stcs(reinterpret_cast<uint2 *>(hd),
                make_uint2(h[0] | uint32_t(h[1]) << 16, h[2] | uint32_t(h[3]) << 16));
@@ -1215,12 +1266,187 @@ __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__
       } else {
         const int ev[4] = {e.x, e.y, e.z, e.w};
         for (int q = 0; q < 4 && n + q < N; ++q) {
-          split_f16(src[q], ev[q], h[q], l[q]);
+          if (split_f16(src[q], ev[q], h[q], l[q]))
+            mark_exception(bits, int64_t((n + q) >> 5) * K + k, (n + q) & 31, flag + n + q);
           Bh[int64_t(k) * ldh + n + q] = h[q];
           Bl[int64_t(k) * ldh + n + q] = l[q];
         }
       }
     }
+  }
+}
+
+// ---- 3xFP16 exceptions: C += the remainders the split could not carry -----------------------
+// a b = rep(a) rep(b) + (a - rep(a)) b + rep(a) (b - rep(b)) exactly, rep(x) = 2^e (hi + lo).
+// The GEMM computes rep(a) rep(b); fix16_a adds (a - rep(a)) b for the exceptions of A (row by
+// row), fix16_b adds rep(a) (b - rep(b)) for those of B (column strip by column strip). Both
+// sum in fp64 in ascending k and round once into C (deterministic), mirror the new value to
+// the peers' copies when the epilogue also wrote those (fused gather), and do nothing for rows /
+// strips without exceptions -- the common case: uniform data has ~1e-6 of its elements more
+// than 2^20 below their row / column maximum.
+struct PeerC {
+  float *p[kMaxCDst - 1];
+  int n;
+};
+constexpr int kFixCap = 1024;  // exceptions staged in shared memory per pass
+
+__device__ __forceinline__ double rep16(uint16_t h, uint16_t l, int e) {
+  return ldexp(double(__half2float(__ushort_as_half(h))) + double(__half2float(__ushort_as_half(l))), e);
+}
+
+// One block per row of A (blocks of rows without exceptions return at once). Warp 0 stages
+// the row's exceptions in ascending k (up to kFixCap per pass: a 32-word group holds at most
+// 1024), then all threads add sum_k delta_k B[k][j] to C[i][j] for every column j.
+__global__ void __launch_bounds__(256) fix16_a_kernel(
+    const float *__restrict__ A, int64_t lda, const float *__restrict__ B, int64_t ldb, int M,
+    int N, const uint16_t *__restrict__ Ah, const uint16_t *__restrict__ Al, int64_t ldh,
+    const int *__restrict__ ea, const unsigned *__restrict__ bits, int wa,
+    const int *__restrict__ flag, float *C, int64_t ldc, const PeerC peers) {
+  __shared__ int ks[kFixCap];
+  __shared__ double ds[kFixCap];
+  __shared__ int n_sh, w_sh;
+  for (int i = blockIdx.x; i < M; i += gridDim.x) {
+  if (flag[i] == 0) continue;
+  const int e = ea[i];
+  for (int w = 0; w < wa;) {
+    if (threadIdx.x < 32) {
+      int n = 0, ww = w;
+      for (; ww < wa; ww += 32) {
+        const int wi = ww + int(threadIdx.x);
+        const unsigned word = wi < wa ? bits[int64_t(i) * wa + wi] : 0u;
+        const int c = __popc(word);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (threadIdx.x >= unsigned(o)) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        if (n + total > kFixCap) break;  // apply what is staged first
+        int pos = n + incl - c;
+        for (unsigned b = word; b; b &= b - 1) {
+          const int k = wi * 32 + __ffs(b) - 1;
+          const int64_t o = int64_t(i) * ldh + k;
+          ks[pos] = k;
+          ds[pos++] = double(A[int64_t(i) * lda + k]) - rep16(Ah[o], Al[o], e);
+        }
+        n += total;
+      }
+      if (threadIdx.x == 0) {
+        n_sh = n;
+        w_sh = ww;
+      }
+    }
+    __syncthreads();
+    const int n = n_sh;
+    w = w_sh;
+    for (int j = threadIdx.x; j < N && n > 0; j += blockDim.x) {
+      double t = 0.0;
+      for (int q = 0; q < n; ++q) t = fma(ds[q], double(B[int64_t(ks[q]) * ldb + j]), t);
+      const float v = float(double(C[int64_t(i) * ldc + j]) + t);
+      C[int64_t(i) * ldc + j] = v;
+      for (int pi = 0; pi < peers.n; ++pi) peers.p[pi][int64_t(i) * ldc + j] = v;
+    }
+    __syncthreads();  // the next pass overwrites the staged exceptions
+  }
+  }
+}
+
+// One block per strip of 32 columns of B (strips without exceptions return at once). Warp 0
+// stages the strip's exceptions in ascending k (then j), counting-sorts them by column, then
+// every thread takes rows i and adds sum_k rep(a_ik) delta_kj to C[i][j] per column.
+__global__ void __launch_bounds__(256) fix16_b_kernel(
+    const float *__restrict__ B, int64_t ldb, int M, int N, int K,
+    const uint16_t *__restrict__ Ah, const uint16_t *__restrict__ Al, int64_t ldah,
+    const int *__restrict__ ea, const uint16_t *__restrict__ Bh, const uint16_t *__restrict__ Bl,
+    int64_t ldbh, const int *__restrict__ eb, const unsigned *__restrict__ bits, int wb,
+    const int *__restrict__ flag, float *C, int64_t ldc, const PeerC peers) {
+  __shared__ int ks[kFixCap];
+  __shared__ unsigned char js[kFixCap];
+  __shared__ double ds[kFixCap];
+  __shared__ int sk[kFixCap];
+  __shared__ double sd[kFixCap];
+  __shared__ int seg[33];
+  __shared__ int n_sh, k_sh, any_sh;
+  for (int s = blockIdx.x; s * 32 < N; s += gridDim.x) {
+  const int j0 = s * 32;
+  if (threadIdx.x < 32) {
+    const int j = j0 + int(threadIdx.x);
+    const unsigned any = __ballot_sync(0xffffffffu, j < N && flag[j] != 0);
+    if (threadIdx.x == 0) any_sh = any != 0u;
+  }
+  __syncthreads();
+  const bool any = any_sh;
+  __syncthreads();  // any_sh is rewritten for the next strip
+  if (!any) continue;
+  for (int k0 = 0; k0 < K;) {
+    if (threadIdx.x < 32) {
+      int n = 0, kk = k0;
+      for (; kk < K; kk += 32) {
+        const int k = kk + int(threadIdx.x);
+        const unsigned word = k < K ? bits[int64_t(s) * K + k] : 0u;
+        const int c = __popc(word);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (threadIdx.x >= unsigned(o)) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        if (n + total > kFixCap) break;
+        int pos = n + incl - c;
+        for (unsigned b = word; b; b &= b - 1) {
+          const int jb = __ffs(b) - 1, j = j0 + jb;
+          const int64_t o = int64_t(k) * ldbh + j;
+          ks[pos] = k;
+          js[pos] = (unsigned char)jb;
+          ds[pos++] = double(B[int64_t(k) * ldb + j]) - rep16(Bh[o], Bl[o], eb[j]);
+        }
+        n += total;
+      }
+      // counting sort by column (stable: ascending k within a column)
+      int cnt = 0;
+      for (int q = 0; q < n; ++q) cnt += js[q] == threadIdx.x;
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (threadIdx.x >= unsigned(o)) incl += y;
+      }
+      int pos = incl - cnt;
+      seg[threadIdx.x] = pos;
+      if (threadIdx.x == 31) seg[32] = incl;
+      for (int q = 0; q < n; ++q)
+        if (js[q] == threadIdx.x) {
+          sk[pos] = ks[q];
+          sd[pos++] = ds[q];
+        }
+      if (threadIdx.x == 0) {
+        n_sh = n;
+        k_sh = kk;
+      }
+    }
+    __syncthreads();
+    const int n = n_sh;
+    k0 = k_sh;
+    for (int i = threadIdx.x; i < M && n > 0; i += blockDim.x) {
+      const int e = ea[i];
+      for (int jb = 0; jb < 32; ++jb) {
+        const int q0 = seg[jb], q1 = seg[jb + 1];
+        if (q0 == q1) continue;
+        double t = 0.0;
+        for (int q = q0; q < q1; ++q) {
+          const int64_t o = int64_t(i) * ldah + sk[q];
+          t = fma(rep16(Ah[o], Al[o], e), sd[q], t);
+        }
+        const int64_t c = int64_t(i) * ldc + j0 + jb;
+        const float v = float(double(C[c]) + t);
+        C[c] = v;
+        for (int pi = 0; pi < peers.n; ++pi) peers.p[pi][c] = v;
+      }
+    }
+    __syncthreads();
+  }
   }
 }
 
@@ -1662,11 +1888,22 @@ cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, T
     // 256-row / 256-column tiles (the epilogue reads them unguarded)
     const int64_t ldah = (K + 7) / 8 * 8, ldbh = (N + 7) / 8 * 8;
     const int64_t n_pad = (N + 255) / 256 * 256, m_pad = (M + 255) / 256 * 256;
+    const int64_t wa = (K + 31) / 32, wb = (N + 31) / 32;
     const size_t bh = up(size_t(K) * ldbh * 2), ebb = up(size_t(n_pad) * 4);
     const size_t ah = up(size_t(M) * ldah * 2), eab = up(size_t(m_pad) * 4);
-    ScratchBuf *sb = bpre_scratch(st, 2 * bh + 2 * ebb + 2 * ah + eab);
+    // exception bitmaps + flags: [xb | fb] belongs to B (kept with B for b_prep_reuse)
+    const size_t xbb = up(size_t(K) * wb * 4 + size_t(n_pad) * 4);
+    const size_t xab = up(size_t(M) * wa * 4 + size_t(m_pad) * 4);
+    const size_t b_part = 2 * bh + 2 * ebb + xbb;
+    ScratchBuf *sb = bpre_scratch(st, b_part + 2 * ah + eab + xab);
     if (!sb) return cudaSuccess;
     uint8_t *scr = static_cast<uint8_t *>(sb->p);
+    tp->wa = int(wa);
+    tp->wb = int(wb);
+    tp->xb = reinterpret_cast<unsigned *>(scr + 2 * bh + 2 * ebb);
+    tp->fb = reinterpret_cast<int *>(scr + 2 * bh + 2 * ebb + size_t(K) * wb * 4);
+    tp->xa = reinterpret_cast<unsigned *>(scr + b_part + 2 * ah + eab);
+    tp->fa = reinterpret_cast<int *>(scr + b_part + 2 * ah + eab + size_t(M) * wa * 4);
     tp->scheme = 4;
     tp->owner = sb;
     tp->ldah = ldah;
@@ -1675,9 +1912,9 @@ cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, T
     tp->Bl = reinterpret_cast<uint16_t *>(scr + bh);
     tp->eb = reinterpret_cast<int *>(scr + 2 * bh);
     tp->bmax = reinterpret_cast<unsigned *>(scr + 2 * bh + ebb);
-    tp->Ah = reinterpret_cast<uint16_t *>(scr + 2 * bh + 2 * ebb);
-    tp->Al = reinterpret_cast<uint16_t *>(scr + 2 * bh + 2 * ebb + ah);
-    tp->ea = reinterpret_cast<int *>(scr + 2 * bh + 2 * ebb + 2 * ah);
+    tp->Ah = reinterpret_cast<uint16_t *>(scr + b_part);
+    tp->Al = reinterpret_cast<uint16_t *>(scr + b_part + ah);
+    tp->ea = reinterpret_cast<int *>(scr + b_part + 2 * ah);
     tp->key_b = sb->key_scheme == 4 ? sb->key_b : nullptr;
     tp->key_ldb = sb->key_ldb;
     tp->key_k = sb->key_k;
@@ -1726,16 +1963,22 @@ cudaError_t launch_prep16_b(const float *B, int64_t ldb, int64_t N, int64_t K, T
   const int64_t n_pad = (N + 255) / 256 * 256;
   sb->key_b = nullptr;
   cudaError_t e = cudaMemsetAsync(tp->bmax, 0, size_t(n_pad) * 4, st);
+  if (e == cudaSuccess)  // exception bitmap + column flags (contiguous)
+    e = cudaMemsetAsync(tp->xb, 0, size_t(K) * tp->wb * 4 + size_t(n_pad) * 4, st);
   if (e != cudaSuccess) return e;
-  const dim3 g1(unsigned((N + 255) / 256), unsigned((K + kPrepBRows - 1) / kPrepBRows));
-  prep16_bmax_kernel<<<g1, 256, 0, st>>>(B, ldb, int(K), int(N), tp->bmax);
+  const int64_t bx = (N + 127) / 128;
+  const int64_t by = std::max<int64_t>(1, std::min<int64_t>((K + 7) / 8,
+                                                            int64_t(num_sms_current()) * 8 / bx));
+  const int64_t rows = ((K + by - 1) / by + 7) / 8 * 8;
+  const dim3 g1(unsigned(bx), unsigned((K + rows - 1) / rows));
+  prep16_bmax_kernel<<<g1, 256, 0, st>>>(B, ldb, int(K), int(N), int(rows), tp->bmax);
   prep16_bexp_kernel<<<unsigned((n_pad + 255) / 256), 256, 0, st>>>(
       tp->bmax, int(n_pad), const_cast<int *>(tp->eb));
   const int64_t units = ((K + 7) / 8) * ((N + 3) / 4);
   const int64_t blocks = std::min<int64_t>((units + 255) / 256, int64_t(num_sms_current()) * 8);
   prep16_b_kernel<<<unsigned(std::max<int64_t>(blocks, 1)), 256, 0, st>>>(
       B, ldb, int(K), int(N), tp->eb, const_cast<uint16_t *>(tp->Bh),
-      const_cast<uint16_t *>(tp->Bl), tp->ldbh);
+      const_cast<uint16_t *>(tp->Bl), tp->ldbh, tp->xb, tp->wb, tp->fb);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   sb->key_b = tp->key_b = B;
@@ -1749,10 +1992,38 @@ cudaError_t launch_prep16_b(const float *B, int64_t ldb, int64_t N, int64_t K, T
 cudaError_t launch_prep16_a(const float *A, int64_t lda, int64_t M, int64_t K, TermsPrep *tp,
                             cudaStream_t st) {
   const int64_t m_pad = (M + 255) / 256 * 256;
-  prep16_a_kernel<<<unsigned(m_pad), 512, 0, st>>>(A, lda, int(M), int(K),
-                                                   const_cast<uint16_t *>(tp->Ah),
-                                                   const_cast<uint16_t *>(tp->Al), tp->ldah,
-                                                   const_cast<int *>(tp->ea));
+  cudaError_t e = cudaMemsetAsync(tp->xa, 0, size_t(M) * tp->wa * 4 + size_t(m_pad) * 4, st);
+  if (e != cudaSuccess) return e;
+  const int64_t cap = int64_t(num_sms_current()) * 4;
+  if (K >= 8192) {
+    prep16_a_kernel<512><<<unsigned(std::min(m_pad, cap)), 512, 0, st>>>(
+        A, lda, int(M), int(m_pad), int(K), const_cast<uint16_t *>(tp->Ah),
+        const_cast<uint16_t *>(tp->Al), tp->ldah, const_cast<int *>(tp->ea), tp->xa, tp->wa,
+        tp->fa);
+  } else {
+    prep16_a_kernel<32><<<unsigned(std::min((m_pad + 15) / 16, cap)), 512, 0, st>>>(
+        A, lda, int(M), int(m_pad), int(K), const_cast<uint16_t *>(tp->Ah),
+        const_cast<uint16_t *>(tp->Al), tp->ldah, const_cast<int *>(tp->ea), tp->xa, tp->wa,
+        tp->fa);
+  }
+  return cudaGetLastError();
+}
+
+// The exception fixes of one 3xFP16 launch (after its GEMM, same stream).
+cudaError_t launch_fix16(const float *A, int64_t lda, const float *B, int64_t ldb,
+                                int64_t M, int64_t N, int64_t K, const TermsPrep *tp, float *C,
+                                int64_t ldc, const GemmExtra *ex, cudaStream_t st) {
+  PeerC peers;
+  peers.n = ex->n_peer_c;
+  for (int i = 0; i < peers.n; ++i) peers.p[i] = ex->peer_c[i];
+  // grid-strided rows / strips: blocks of rows or strips without exceptions only read a flag
+  const int64_t cap = int64_t(num_sms_current()) * 4;
+  fix16_a_kernel<<<unsigned(std::min<int64_t>(M, cap)), 256, 0, st>>>(A, lda, B, ldb, int(M), int(N), tp->Ah, tp->Al,
+                                              tp->ldah, tp->ea, tp->xa, tp->wa, tp->fa, C, ldc,
+                                              peers);
+  fix16_b_kernel<<<unsigned(std::min<int64_t>((N + 31) / 32, cap)), 256, 0, st>>>(
+      B, ldb, int(M), int(N), int(K), tp->Ah, tp->Al, tp->ldah, tp->ea, tp->Bh, tp->Bl,
+      tp->ldbh, tp->eb, tp->xb, tp->wb, tp->fb, C, ldc, peers);
   return cudaGetLastError();
 }
 
@@ -1848,9 +2119,11 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.eb = nullptr;
   // k-block width in elements of K: 16 (tf32 schemes), 32 (3xFP16)
   const int bk = terms == 4 ? 32 : BK;
+  TermsPrep local4;
+  const TermsPrep *tp4 = nullptr;
   if (terms == 4) {
     // scaled fp16 hi / lo operands (the caller's TermsPrep, else prepared here)
-    TermsPrep local;
+    TermsPrep &local = local4;
     const TermsPrep *tp = ex->prep;
     if (!tp || tp->scheme != 4) {
       cudaError_t e = terms_prep_alloc(M, N, K, st, &local, 4);
@@ -1872,6 +2145,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
       return cudaErrorInvalidValue;
     p.ea = tp->ea;
     p.eb = tp->eb;
+    tp4 = tp;
   }
   if (terms == 2) {
     // operands prepared in HBM (the caller's TermsPrep, else here, untimed)
@@ -1963,16 +2237,20 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   // other streams have their own); none inside a capture that has not seen this stream yet
   if (dyn_env) p.sched = sched_counters(st);
   p.wave_sync = (wave_env && p.num_units > nclu) ? 1 : 0;
+  cudaError_t e = cudaSuccess;
 
   if (cg == 1) {
-    cudaError_t e = ensure_smem_attr<1>();
+    e = ensure_smem_attr<1>();
     if (e != cudaSuccess) return e;
     const int grid = p.num_units < num_sms ? p.num_units : num_sms;
     gemm_3xtf32_kernel<1><<<grid, NUM_THREADS, Tile<1>::SMEM_BYTES, st>>>(tA, tAlo, tB, tBlo,
                                                                           tC, p);
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    if (e == cudaSuccess && tp4 && !ex->defer_fix)
+      e = launch_fix16(A, lda, B, ldb, M, N, K, tp4, C, ldc, ex, st);
+    return e;
   }
-  cudaError_t e = ensure_smem_attr<2>();
+  e = ensure_smem_attr<2>();
   if (e != cudaSuccess) return e;
   const int pairs = num_sms / 2;
   const int clusters = p.num_units < pairs ? p.num_units : pairs;
@@ -1988,7 +2266,10 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  return cudaLaunchKernelEx(&lc, gemm_3xtf32_kernel<2>, tA, tAlo, tB, tBlo, tC, p);
+  e = cudaLaunchKernelEx(&lc, gemm_3xtf32_kernel<2>, tA, tAlo, tB, tBlo, tC, p);
+  if (e == cudaSuccess && tp4 && !ex->defer_fix)
+    e = launch_fix16(A, lda, B, ldb, M, N, K, tp4, C, ldc, ex, st);
+  return e;
 }
 
 }  // namespace giga

@@ -64,6 +64,11 @@ struct TermsPrep {
   const int *ea = nullptr, *eb = nullptr;
   unsigned *bmax = nullptr;  // per-column max |b| bits (preparation scratch)
   int64_t ldah = 0, ldbh = 0;
+  // exceptions (elements the fp16 split cannot carry to 2^-20): bitmaps (A: M rows of wa
+  // words, B: K rows of wb words) and per-row / per-column flags
+  unsigned *xa = nullptr, *xb = nullptr;
+  int *fa = nullptr, *fb = nullptr;
+  int wa = 0, wb = 0;
   int scheme = 2;
   void *owner = nullptr;
   const float *key_b = nullptr;
@@ -98,7 +103,16 @@ struct GemmExtra {
   // amortises B's preparation over them (0 = this launch's M)
   int64_t rows_hint = 0;
   const TermsPrep *prep = nullptr;  // terms = 2: operands already prepared by the caller
+  // terms = 4: 1 = the caller launches the exception fixes itself (launch_fix16, after the GEMM
+  // on the same stream; run_gemm does, to time them apart from the GEMM)
+  int defer_fix = 0;
 };
+// The 3xFP16 exception fixes of a launch whose GEMM ran with defer_fix (same arguments).
+cudaError_t launch_fix16(const float *A, int64_t lda, const float *B, int64_t ldb, int64_t M,
+                         int64_t N, int64_t K, const TermsPrep *tp, float *C, int64_t ldc,
+                         const GemmExtra *ex, cudaStream_t st);
+// Kernels launch_prep16_b / launch_prep16_a / launch_fix16 issue (bench.py's launch count).
+constexpr int kPrep16BLaunches = 3, kPrep16ALaunches = 1, kFix16Launches = 2;
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
                                const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,
                                int64_t ldc, int terms, int promote_kblocks, cudaStream_t st,

@@ -182,9 +182,12 @@ int run_gemm(const float *A, const float *Alo, const float *B, const float *Blo,
       terms = 3;
     } else {
       if (!(e.b_prep_reuse && tp.b_matches(B, ldb, N, K)))
-        CK(timed(1, st, [&] { return launch_prep16_b(B, ldb, N, K, &tp, st); }));
-      CK(timed(1, st, [&] { return launch_prep16_a(A, lda, M, K, &tp, st); }));
+        CK(timed(1, st, [&] { return launch_prep16_b(B, ldb, N, K, &tp, st); },
+                 kPrep16BLaunches));
+      CK(timed(1, st, [&] { return launch_prep16_a(A, lda, M, K, &tp, st); },
+               kPrep16ALaunches));
       e.prep = &tp;
+      e.defer_fix = 1;
     }
   }
   if (terms == 2) {
@@ -204,6 +207,11 @@ int run_gemm(const float *A, const float *Alo, const float *B, const float *Blo,
   CK(timed(0, st, [&] {
     return launch_gemm_3xtf32(A, Alo, B, Blo, C, M, N, K, ldc, terms, -1, st, 0, &e);
   }));
+  if (terms == 4) {
+    const int64_t lda = e.lda ? e.lda : K, ldb = e.ldb ? e.ldb : N;
+    CK(timed(1, st, [&] { return launch_fix16(A, lda, B, ldb, M, N, K, &tp, C, ldc, &e, st); },
+             kFix16Launches));
+  }
   return GIGA_OK;
 }
 

@@ -99,8 +99,9 @@ extern State g;
 
 struct TimeRec {
   int dev;
-  int kind;  // 0 gemm, 1 split
+  int kind;  // 0 gemm, 1 split / operand preparation / exception fixes
   cudaEvent_t a, b;
+  int n;     // kernels the bracketed call launched
 };
 extern std::mutex g_tmu;
 extern bool g_timing;
@@ -112,9 +113,10 @@ extern int64_t g_tcount[2];
 
 cudaEvent_t pool_event(int dev);  // a timing event for `dev` (caller holds g_tmu)
 
-// Launch `fn` on `st`, bracketed by timing events when timing is enabled.
+// Launch `fn` on `st`, bracketed by timing events when timing is enabled; `n` = the number of
+// kernels fn launches (the launch count bench.py reports).
 template <class F>
-cudaError_t timed(int kind, cudaStream_t st, F fn) {
+cudaError_t timed(int kind, cudaStream_t st, F fn, int n = 1) {
   bool on;
   {
     std::lock_guard<std::mutex> lk(g_tmu);
@@ -134,7 +136,7 @@ cudaError_t timed(int kind, cudaStream_t st, F fn) {
   if (b) cudaEventRecord(b, st);
   std::lock_guard<std::mutex> lk(g_tmu);
   if (a && b)
-    g_tpending.push_back({dev, kind, a, b});
+    g_tpending.push_back({dev, kind, a, b, n});
   else {
     if (a) g_tpool.push_back({dev, a});
     if (b) g_tpool.push_back({dev, b});

@@ -5,9 +5,13 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2504_01266_b200 import giga
 giga.init(1)
-shapes = [(4096, 4096, 4096), (8192, 8192, 8192), (8192, 8192, 2048), (12288, 12288, 12288),
-          (8192, 16384, 8192), (16384, 8192, 8192), (4096, 32768, 32768), (16384, 16384, 4096),
+shapes = [(512, 512, 512), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 4096),
+          (2048, 4096, 4096), (32768, 1024, 1024), (262144, 1024, 1024), (8192, 8192, 2048),
+          (8192, 8192, 8192), (2048, 16384, 16384), (4096, 16384, 16384), (8192, 16384, 16384),
+          (16384, 16384, 4096), (16384, 32768, 1024), (16384, 32768, 576), (4096, 32768, 32768),
           (16384, 16384, 16384)]
+if os.environ.get("XO_SHAPES"):
+    shapes = [tuple(int(v) for v in x.split("x")) for x in os.environ["XO_SHAPES"].split(",")]
 for (M, N, K) in shapes:
     A = torch.randn(M, K, device="cuda"); B = torch.randn(K, N, device="cuda")
     C = torch.empty(M, N, device="cuda")

@@ -98,8 +98,9 @@ def test_gemm_building_block_guard_columns(lib, torch_cuda, terms, M, N, K):
     A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3")
     B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
     c_out, dC = _guarded(torch, M, N, ldc)
-    giga.gemm_3xtf32(torch.from_numpy(A).cuda(), None, torch.from_numpy(B).cuda(), None, dC,
-                     M, N, K, ldc=ldc, terms=terms)
+    # dC is a strided view (ldc > N): pass its address (the binding takes contiguous tensors)
+    giga.gemm_3xtf32(torch.from_numpy(A).cuda(), None, torch.from_numpy(B).cuda(), None,
+                     dC.data_ptr(), M, N, K, ldc=ldc, terms=terms)
     torch.cuda.synchronize()
     _check_canary(c_out, M, N, ldc, f"C (terms {terms})")
     Cref, _ = oracle.gemm(A, B)
