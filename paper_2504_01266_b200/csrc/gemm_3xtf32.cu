@@ -1057,16 +1057,20 @@ __global__ void __launch_bounds__(256) prep_a_kernel(const float *__restrict__ A
 // significand split of 3xTF32 (x = hi + lo, three products, small terms first) on the fp16
 // tensor-core path (K = 16 per instruction: twice kind::tf32's K per MMA time) and moves the
 // exponent range into exact power-of-two scales: row i of A is scaled by 2^-ea[i], column j
-// of B by 2^-eb[j], so that the row / column maximum lies in [2^14, 2^15) (fp16 max 65504);
+// of B by 2^-eb[j], so that the row / column maximum lies in [2^15, 65504) (fp16's top binade
+// below its largest finite value: the higher the scale, the fewer elements sink to fp16's
+// subnormal floor);
 // the epilogue multiplies C_ij by 2^(ea[i] + eb[j]). hi = fp16 RN(x'), lo = fp16 RN(x' - hi)
-// (x' - hi is exact in fp32). For |x'| >= 2^-3 both are normal fp16 numbers and
-// |x' - hi - lo| <= 2^-22 |x'|; elements far below their row's (column's) maximum lose
-// relative precision to fp16's subnormal floor (2^-25 absolute in the scaled units).
+// (x' - hi is exact in fp32). For |x'| >= 2^-3, |x' - hi - lo| <= 2^-22 |x'| (both RN to
+// 11 bits, or lo at fp16's subnormal floor: 2^-25 absolute in the scaled units); elements far
+// below their row's (column's) maximum lose relative precision to that floor.
 // An exponent of a row / column with no finite non-zero maximum is 0 (zeros stay exact,
 // Inf / NaN propagate as the contract states).
 __device__ __forceinline__ int scale_exp(uint32_t maxbits) {
   if (maxbits == 0u || maxbits >= 0x7f800000u) return 0;
-  return ilogbf(__uint_as_float(maxbits)) - 14;
+  const float m = __uint_as_float(maxbits);
+  const int e = ilogbf(m) - 15;  // max' in [2^15, 2^16) ...
+  return ldexpf(m, -e) >= 65504.0f ? e + 1 : e;  // ... below fp16's largest finite value
 }
 // Returns true when x is an *exception*: its representation 2^e (hi + lo) is off by more than
 // 2^-20 |x| (elements more than ~2^20 below their row's / column's maximum, where fp16's
@@ -1087,10 +1091,14 @@ __device__ __forceinline__ bool split_f16(float x, int e, uint16_t &h, uint16_t 
   return err > 0x1p-20f * fabsf(xs) || (xs == 0.0f && x != 0.0f);
 }
 // Exception bitmaps: bit k of row i of A at word i * wa + k / 32; bit j of row k of B at word
-// (j / 32) * K + k (strip-major: fix16_b reads a strip's words contiguously). flag arrays: 1 for a row of A / column of B holding any exception.
-__device__ __forceinline__ void mark_exception(unsigned *bits, int64_t word, int bit,
+// (j / 32) * K + k (strip-major: fix16_b reads a strip's words contiguously). Their summaries
+// (one bit per bitmap word) let the fix kernels skip empty stretches; flag arrays: 1 for a row
+// of A / column of B holding any exception.
+__device__ __forceinline__ void mark_exception(unsigned *bits, int64_t word, unsigned mask,
+                                               unsigned *summ, int64_t sword, int sbit,
                                                int *flag) {
-  atomicOr(bits + word, 1u << bit);
+  atomicOr(bits + word, mask);
+  atomicOr(summ + sword, 1u << sbit);
   *reinterpret_cast<volatile int *>(flag) = 1;
 }
 
@@ -1106,6 +1114,7 @@ __global__ void __launch_bounds__(512) prep16_a_kernel(const float *__restrict__
                                                        uint16_t *__restrict__ Al, int64_t ldh,
                                                        int *__restrict__ ea,
                                                        unsigned *__restrict__ bits, int wa,
+                                                       unsigned *__restrict__ summ, int w2,
                                                        int *__restrict__ flag) {
   constexpr int RPB = 512 / TPR;
   __shared__ uint32_t red[16];
@@ -1152,9 +1161,9 @@ __global__ void __launch_bounds__(512) prep16_a_kernel(const float *__restrict__
       if (x0 | x1 | x2 | x3) {
         const unsigned nib =
             unsigned(x0) | unsigned(x1) << 1 | unsigned(x2) << 2 | unsigned(x3) << 3;
-        const int k = 4 * i;
-        atomicOr(bits + int64_t(m) * wa + (k >> 5), nib << (k & 31));
-        *reinterpret_cast<volatile int *>(flag + m) = 1;
+        const int k = 4 * i, w = k >> 5;
+        mark_exception(bits, int64_t(m) * wa + w, nib << (k & 31), summ, int64_t(m) * w2 + (w >> 5),
+                       w & 31, flag + m);
       }
       __stcs(reinterpret_cast<uint2 *>(hd) + i,
              make_uint2(h[0] | uint32_t(h[1]) << 16, h[2] | uint32_t(h[3]) << 16));
@@ -1164,7 +1173,8 @@ __global__ void __launch_bounds__(512) prep16_a_kernel(const float *__restrict__
     for (int k = (k4 << 2) + t; k < K; k += TPR) {
       uint16_t h, l;
       if (split_f16(row[k], e, h, l))
-        mark_exception(bits, int64_t(m) * wa + (k >> 5), k & 31, flag + m);
+        mark_exception(bits, int64_t(m) * wa + (k >> 5), 1u << (k & 31), summ,
+                       int64_t(m) * w2 + (k >> 10), (k >> 5) & 31, flag + m);
       hd[k] = h;
       ld[k] = l;
     }
@@ -1231,7 +1241,8 @@ __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__
                                                        int K, int N, const int *__restrict__ eb,
                                                        uint16_t *__restrict__ Bh,
                                                        uint16_t *__restrict__ Bl, int64_t ldh,
-                                                       unsigned *__restrict__ bits, int wb,
+                                                       unsigned *__restrict__ bits,
+                                                       unsigned *__restrict__ summ, int w2,
                                                        int *__restrict__ flag) {
   const int n4 = (N + 3) >> 2, kb8 = (K + 7) >> 3;
   const int64_t total = int64_t(kb8) * n4;
@@ -1252,6 +1263,7 @@ __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__
           const unsigned nib =
               unsigned(x0) | unsigned(x1) << 1 | unsigned(x2) << 2 | unsigned(x3) << 3;
           atomicOr(bits + int64_t(n >> 5) * K + k, nib << (n & 31));
+          atomicOr(summ + int64_t(n >> 5) * w2 + (k >> 5), 1u << (k & 31));
           volatile int *f = flag + n;
           if (x0) f[0] = 1;
           if (x1) f[1] = 1;
@@ -1267,7 +1279,8 @@ __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__
         const int ev[4] = {e.x, e.y, e.z, e.w};
         for (int q = 0; q < 4 && n + q < N; ++q) {
           if (split_f16(src[q], ev[q], h[q], l[q]))
-            mark_exception(bits, int64_t((n + q) >> 5) * K + k, (n + q) & 31, flag + n + q);
+            mark_exception(bits, int64_t((n + q) >> 5) * K + k, 1u << ((n + q) & 31), summ,
+                           int64_t((n + q) >> 5) * w2 + (k >> 5), k & 31, flag + n + q);
           Bh[int64_t(k) * ldh + n + q] = h[q];
           Bl[int64_t(k) * ldh + n + q] = l[q];
         }
@@ -1277,9 +1290,10 @@ __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__
 }
 
 // ---- 3xFP16 exceptions: C += the remainders the split could not carry -----------------------
-// a b = rep(a) rep(b) + (a - rep(a)) b + rep(a) (b - rep(b)) exactly, rep(x) = 2^e (hi + lo).
-// The GEMM computes rep(a) rep(b); fix16_a adds (a - rep(a)) b for the exceptions of A (row by
-// row), fix16_b adds rep(a) (b - rep(b)) for those of B (column strip by column strip). Both
+// a b = rep(a) rep(b) + (a - rep(a)) rep(b) + a (b - rep(b)) exactly, rep(x) = 2^e (hi + lo).
+// The GEMM computes rep(a) rep(b); fix16_a adds (a - rep(a)) rep(b) for the exceptions of A
+// (row by row: rep(b) rows are contiguous), fix16_b adds a (b - rep(b)) for those of B (column
+// strip by column strip, reading A's fp32 column: one sector per row and exception). Both
 // sum in fp64 in ascending k and round once into C (deterministic), mirror the new value to
 // the peers' copies when the epilogue also wrote those (fused gather), and do nothing for rows /
 // strips without exceptions -- the common case: uniform data has ~1e-6 of its elements more
@@ -1294,159 +1308,221 @@ __device__ __forceinline__ double rep16(uint16_t h, uint16_t l, int e) {
   return ldexp(double(__half2float(__ushort_as_half(h))) + double(__half2float(__ushort_as_half(l))), e);
 }
 
-// One block per row of A (blocks of rows without exceptions return at once). Warp 0 stages
-// the row's exceptions in ascending k (up to kFixCap per pass: a 32-word group holds at most
-// 1024), then all threads add sum_k delta_k B[k][j] to C[i][j] for every column j.
+// Warp 0's staging of exceptions in ascending order. L: level-1 bitmap words, S: their
+// summary (bit w % 32 of S[w / 32] set iff L[w] != 0). Starting at summary word s0 it walks the
+// non-zero summary words (granules: 32 level-1 words, at most 1024 exceptions = kFixCap) in
+// order and emits every set bit (emit(pos, word, bit), pos = its slot in the staging buffer)
+// while the buffer has room for the whole granule. Returns (staged count, next summary word;
+// n2 when done) to every lane.
+template <class Emit>
+__device__ __forceinline__ int2 stage_exceptions(const unsigned *__restrict__ S, int n2,
+                                                 const unsigned *__restrict__ L, int n1, int s0,
+                                                 Emit emit) {
+  const int lane = threadIdx.x & 31;
+  int n = 0;
+  for (int c0 = s0; c0 < n2; c0 += 32) {
+    const unsigned sw = c0 + lane < n2 ? S[c0 + lane] : 0u;
+    unsigned nz = __ballot_sync(0xffffffffu, sw != 0u);
+    while (nz) {
+      const int src = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const int g = c0 + src;
+      const unsigned swv = __shfl_sync(0xffffffffu, sw, src);
+      const int wi = g * 32 + lane;
+      const unsigned word = ((swv >> lane) & 1u) && wi < n1 ? L[wi] : 0u;
+      const int c = __popc(word);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (n + total > kFixCap) return make_int2(n, g);  // apply what is staged first
+      int pos = n + incl - c;
+      for (unsigned b = word; b; b &= b - 1) emit(pos++, wi, __ffs(b) - 1);
+      n += total;
+    }
+  }
+  return make_int2(n, n2);
+}
+
+// Blocks take 32-row windows of A (grid-strided), find the rows flagged with exceptions in
+// one parallel read of their flags and process those rows one by one: warp 0 stages the row's
+// exceptions in ascending k through the summary words, then all threads add
+// sum_k delta_k rep(B[k][j]) to C[i][j] for every column j.
 __global__ void __launch_bounds__(256) fix16_a_kernel(
-    const float *__restrict__ A, int64_t lda, const float *__restrict__ B, int64_t ldb, int M,
-    int N, const uint16_t *__restrict__ Ah, const uint16_t *__restrict__ Al, int64_t ldh,
-    const int *__restrict__ ea, const unsigned *__restrict__ bits, int wa,
-    const int *__restrict__ flag, float *C, int64_t ldc, const PeerC peers) {
+    const float *__restrict__ A, int64_t lda, int M, int N, const uint16_t *__restrict__ Ah,
+    const uint16_t *__restrict__ Al, int64_t ldh, const int *__restrict__ ea,
+    const uint16_t *__restrict__ Bh, const uint16_t *__restrict__ Bl, int64_t ldbh,
+    const int *__restrict__ eb, const unsigned *__restrict__ bits, int wa,
+    const unsigned *__restrict__ summ, int w2, const int *__restrict__ flag,
+    float *__restrict__ C, int64_t ldc, const PeerC peers) {
   __shared__ int ks[kFixCap];
   __shared__ double ds[kFixCap];
-  __shared__ int n_sh, w_sh;
-  for (int i = blockIdx.x; i < M; i += gridDim.x) {
-  if (flag[i] == 0) continue;
-  const int e = ea[i];
-  for (int w = 0; w < wa;) {
+  __shared__ int n_sh, s_sh, nrows;
+  __shared__ int rows[256];
+  for (int base = blockIdx.x * 32; base < M; base += gridDim.x * 32) {
+    // the flags of 256 rows at once; the rows holding exceptions (any order: rows are
+    // independent)
+    __syncthreads();
+    if (threadIdx.x == 0) nrows = 0;
+    __syncthreads();
     if (threadIdx.x < 32) {
-      int n = 0, ww = w;
-      for (; ww < wa; ww += 32) {
-        const int wi = ww + int(threadIdx.x);
-        const unsigned word = wi < wa ? bits[int64_t(i) * wa + wi] : 0u;
-        const int c = __popc(word);
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (threadIdx.x >= unsigned(o)) incl += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        if (n + total > kFixCap) break;  // apply what is staged first
-        int pos = n + incl - c;
-        for (unsigned b = word; b; b &= b - 1) {
-          const int k = wi * 32 + __ffs(b) - 1;
-          const int64_t o = int64_t(i) * ldh + k;
-          ks[pos] = k;
-          ds[pos++] = double(A[int64_t(i) * lda + k]) - rep16(Ah[o], Al[o], e);
-        }
-        n += total;
-      }
-      if (threadIdx.x == 0) {
-        n_sh = n;
-        w_sh = ww;
-      }
+      const int r = base + int(threadIdx.x);
+      const bool f = r < M && flag[r] != 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      int wofs = 0;
+      if ((threadIdx.x & 31) == 0 && bal) wofs = atomicAdd(&nrows, __popc(bal));
+      wofs = __shfl_sync(0xffffffffu, wofs, 0);
+      if (f) rows[wofs + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = r;
     }
     __syncthreads();
-    const int n = n_sh;
-    w = w_sh;
-    for (int j = threadIdx.x; j < N && n > 0; j += blockDim.x) {
-      double t = 0.0;
-      for (int q = 0; q < n; ++q) t = fma(ds[q], double(B[int64_t(ks[q]) * ldb + j]), t);
-      const float v = float(double(C[int64_t(i) * ldc + j]) + t);
-      C[int64_t(i) * ldc + j] = v;
-      for (int pi = 0; pi < peers.n; ++pi) peers.p[pi][int64_t(i) * ldc + j] = v;
+    const int nr = nrows;
+    for (int ri = 0; ri < nr; ++ri) {
+      const int i = rows[ri];
+      const int e = ea[i];
+      for (int s = 0; s < w2;) {
+        if (threadIdx.x < 32) {
+          const int2 r = stage_exceptions(
+              summ + int64_t(i) * w2, w2, bits + int64_t(i) * wa, wa, s,
+              [&](int pos, int wi, int bit) {
+                const int k = wi * 32 + bit;
+                const int64_t o = int64_t(i) * ldh + k;
+                ks[pos] = k;
+                ds[pos] = double(A[int64_t(i) * lda + k]) - rep16(Ah[o], Al[o], e);
+              });
+          if (threadIdx.x == 0) {
+            n_sh = r.x;
+            s_sh = r.y;
+          }
+        }
+        __syncthreads();
+        const int n = n_sh;
+        s = s_sh;
+        // 4 columns per thread and step (N, ldc, ldbh are multiples of 4: float4 / 8-byte
+        // loads), all loads of a step issued before the stores
+        float *__restrict__ crow = C + int64_t(i) * ldc;
+        for (int j = 4 * int(threadIdx.x); j < N && n > 0; j += 4 * int(blockDim.x)) {
+          const int4 ev = *reinterpret_cast<const int4 *>(eb + j);
+          double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+          for (int q = 0; q < n; ++q) {
+            const int64_t o = int64_t(ks[q]) * ldbh + j;
+            const uint2 h = *reinterpret_cast<const uint2 *>(Bh + o);
+            const uint2 l = *reinterpret_cast<const uint2 *>(Bl + o);
+            const double d = ds[q];
+            t0 = fma(d, rep16(uint16_t(h.x), uint16_t(l.x), ev.x), t0);
+            t1 = fma(d, rep16(uint16_t(h.x >> 16), uint16_t(l.x >> 16), ev.y), t1);
+            t2 = fma(d, rep16(uint16_t(h.y), uint16_t(l.y), ev.z), t2);
+            t3 = fma(d, rep16(uint16_t(h.y >> 16), uint16_t(l.y >> 16), ev.w), t3);
+          }
+          const float4 c = *reinterpret_cast<const float4 *>(crow + j);
+          const float4 v = make_float4(float(double(c.x) + t0), float(double(c.y) + t1),
+                                       float(double(c.z) + t2), float(double(c.w) + t3));
+          *reinterpret_cast<float4 *>(crow + j) = v;
+          for (int pi = 0; pi < peers.n; ++pi)
+            *reinterpret_cast<float4 *>(peers.p[pi] + int64_t(i) * ldc + j) = v;
+        }
+        __syncthreads();  // the next pass overwrites the staged exceptions
+      }
     }
-    __syncthreads();  // the next pass overwrites the staged exceptions
-  }
   }
 }
 
-// One block per strip of 32 columns of B (strips without exceptions return at once). Warp 0
-// stages the strip's exceptions in ascending k (then j), counting-sorts them by column, then
-// every thread takes rows i and adds sum_k rep(a_ik) delta_kj to C[i][j] per column.
+// Blocks take strips of 32 columns of B (grid-strided; strips without exceptions cost one flag
+// read) times a chunk of the rows of C (blockIdx.y). Warp 0 stages the strip's exceptions in
+// ascending k (then j) through the strip's summary words, counting-sorts them by column, then
+// every thread takes rows i and adds sum_k a_ik delta_kj to C[i][j] per column.
 __global__ void __launch_bounds__(256) fix16_b_kernel(
-    const float *__restrict__ B, int64_t ldb, int M, int N, int K,
-    const uint16_t *__restrict__ Ah, const uint16_t *__restrict__ Al, int64_t ldah,
-    const int *__restrict__ ea, const uint16_t *__restrict__ Bh, const uint16_t *__restrict__ Bl,
-    int64_t ldbh, const int *__restrict__ eb, const unsigned *__restrict__ bits, int wb,
-    const int *__restrict__ flag, float *C, int64_t ldc, const PeerC peers) {
+    const float *__restrict__ A, int64_t lda, const float *__restrict__ B, int64_t ldb, int M,
+    int N, int K, const uint16_t *__restrict__ Bh, const uint16_t *__restrict__ Bl, int64_t ldbh,
+    const int *__restrict__ eb, const unsigned *__restrict__ bits,
+    const unsigned *__restrict__ summ, int w2, const int *__restrict__ flag,
+    float *__restrict__ C, int64_t ldc, const PeerC peers) {
   __shared__ int ks[kFixCap];
   __shared__ unsigned char js[kFixCap];
   __shared__ double ds[kFixCap];
   __shared__ int sk[kFixCap];
   __shared__ double sd[kFixCap];
   __shared__ int seg[33];
-  __shared__ int n_sh, k_sh, any_sh;
-  for (int s = blockIdx.x; s * 32 < N; s += gridDim.x) {
-  const int j0 = s * 32;
-  if (threadIdx.x < 32) {
-    const int j = j0 + int(threadIdx.x);
-    const unsigned any = __ballot_sync(0xffffffffu, j < N && flag[j] != 0);
-    if (threadIdx.x == 0) any_sh = any != 0u;
-  }
-  __syncthreads();
-  const bool any = any_sh;
-  __syncthreads();  // any_sh is rewritten for the next strip
-  if (!any) continue;
-  for (int k0 = 0; k0 < K;) {
+  __shared__ int n_sh, s_sh, any_sh;
+  const int rows_per = (M + int(gridDim.y) - 1) / int(gridDim.y);
+  const int i0 = int(blockIdx.y) * rows_per, i1 = min(M, i0 + rows_per);
+  for (int st = blockIdx.x; st * 32 < N; st += gridDim.x) {
+    const int j0 = st * 32;
     if (threadIdx.x < 32) {
-      int n = 0, kk = k0;
-      for (; kk < K; kk += 32) {
-        const int k = kk + int(threadIdx.x);
-        const unsigned word = k < K ? bits[int64_t(s) * K + k] : 0u;
-        const int c = __popc(word);
-        int incl = c;
+      const int j = j0 + int(threadIdx.x);
+      const unsigned any = __ballot_sync(0xffffffffu, j < N && flag[j] != 0);
+      if (threadIdx.x == 0) any_sh = any != 0u;
+    }
+    __syncthreads();
+    const bool any = any_sh;
+    __syncthreads();  // any_sh is rewritten for the next strip
+    if (!any) continue;
+    for (int s = 0; s < w2;) {
+      if (threadIdx.x < 32) {
+        const int2 r = stage_exceptions(
+            summ + int64_t(st) * w2, w2, bits + int64_t(st) * K, K, s,
+            [&](int pos, int k, int jb) {
+              const int j = j0 + jb;
+              const int64_t o = int64_t(k) * ldbh + j;
+              ks[pos] = k;
+              js[pos] = (unsigned char)jb;
+              ds[pos] = double(B[int64_t(k) * ldb + j]) - rep16(Bh[o], Bl[o], eb[j]);
+            });
+        const int n = r.x;
+        // counting sort by column (stable: ascending k within a column)
+        int cnt = 0;
+        for (int q = 0; q < n; ++q) cnt += js[q] == threadIdx.x;
+        int incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int y = __shfl_up_sync(0xffffffffu, incl, o);
           if (threadIdx.x >= unsigned(o)) incl += y;
         }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        if (n + total > kFixCap) break;
-        int pos = n + incl - c;
-        for (unsigned b = word; b; b &= b - 1) {
-          const int jb = __ffs(b) - 1, j = j0 + jb;
-          const int64_t o = int64_t(k) * ldbh + j;
-          ks[pos] = k;
-          js[pos] = (unsigned char)jb;
-          ds[pos++] = double(B[int64_t(k) * ldb + j]) - rep16(Bh[o], Bl[o], eb[j]);
+        int pos = incl - cnt;
+        seg[threadIdx.x] = pos;
+        if (threadIdx.x == 31) seg[32] = incl;
+        for (int q = 0; q < n; ++q)
+          if (js[q] == threadIdx.x) {
+            sk[pos] = ks[q];
+            sd[pos++] = ds[q];
+          }
+        if (threadIdx.x == 0) {
+          n_sh = n;
+          s_sh = r.y;
         }
-        n += total;
       }
-      // counting sort by column (stable: ascending k within a column)
-      int cnt = 0;
-      for (int q = 0; q < n; ++q) cnt += js[q] == threadIdx.x;
-      int incl = cnt;
+      __syncthreads();
+      const int n = n_sh;
+      s = s_sh;
+      // 4 rows per thread and step (their loads independent of each other and of the stores)
+      const int step = 4 * int(blockDim.x);
+      for (int ib = i0 + int(threadIdx.x); ib < i1 && n > 0; ib += step) {
+        for (int jb = 0; jb < 32; ++jb) {
+          const int q0 = seg[jb], q1 = seg[jb + 1];
+          if (q0 == q1) continue;
+          double t[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int q = q0; q < q1; ++q) {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (threadIdx.x >= unsigned(o)) incl += y;
-      }
-      int pos = incl - cnt;
-      seg[threadIdx.x] = pos;
-      if (threadIdx.x == 31) seg[32] = incl;
-      for (int q = 0; q < n; ++q)
-        if (js[q] == threadIdx.x) {
-          sk[pos] = ks[q];
-          sd[pos++] = ds[q];
+            for (int u = 0; u < 4; ++u) {
+              const int i = ib + u * int(blockDim.x);
+              if (i < i1) t[u] = fma(double(A[int64_t(i) * lda + sk[q]]), sd[q], t[u]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = ib + u * int(blockDim.x);
+            if (i >= i1) continue;
+            const int64_t c = int64_t(i) * ldc + j0 + jb;
+            const float v = float(double(C[c]) + t[u]);
+            C[c] = v;
+            for (int pi = 0; pi < peers.n; ++pi) peers.p[pi][c] = v;
+          }
         }
-      if (threadIdx.x == 0) {
-        n_sh = n;
-        k_sh = kk;
       }
+      __syncthreads();
     }
-    __syncthreads();
-    const int n = n_sh;
-    k0 = k_sh;
-    for (int i = threadIdx.x; i < M && n > 0; i += blockDim.x) {
-      const int e = ea[i];
-      for (int jb = 0; jb < 32; ++jb) {
-        const int q0 = seg[jb], q1 = seg[jb + 1];
-        if (q0 == q1) continue;
-        double t = 0.0;
-        for (int q = q0; q < q1; ++q) {
-          const int64_t o = int64_t(i) * ldah + sk[q];
-          t = fma(rep16(Ah[o], Al[o], e), sd[q], t);
-        }
-        const int64_t c = int64_t(i) * ldc + j0 + jb;
-        const float v = float(double(C[c]) + t);
-        C[c] = v;
-        for (int pi = 0; pi < peers.n; ++pi) peers.p[pi][c] = v;
-      }
-    }
-    __syncthreads();
-  }
   }
 }
 
@@ -1486,15 +1562,17 @@ int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K) {
   if (A_lo) return 3;
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return 3;  // the launch rejects these
   if (forced) return forced;
-  // measured crossover (profiles/r01_scheme_crossover.jsonl, r01_kchunk_crossover.jsonl;
-  // preparation included): TF32 + BF16 wins 2-11% from 8192 x 8192 x 2048 and 4096 x 32768^2
-  // up and 3-10% on 16384 x 32768 x (576..1792) (the host schedule's K-chunks); it ties at
-  // 8192 x 16384 x 1024 and loses 2-5% at 4096^3 and 4096 x 32768 x 768
   const double mnk = double(M) * double(N) * double(K);
-  return (M >= 4096 && N >= 8192 &&
-          ((K >= 2048 && mnk >= 0x1p37) || (K >= 512 && mnk >= 0x1p38)))
-             ? 2
-             : 3;
+  // measured crossover, operand preparation and exception fixes included
+  // (profiles/r02_scheme_crossover*.jsonl, scripts/scheme_crossover.py): 3xFP16 wins from
+  // 8192 x 8192 x 2048 (+10%) and 2048 x 16384^2 (+5%) up to +52-58% at 16384^3 and
+  // 32768^3, and on 16384 x 32768 x 1024 (+8%); it loses where the preparation (~12 B per
+  // element of A and B) is not amortised: 4096^3 (-9%), 2048 x 4096^2, 32768 x 1024^2, and
+  // K = 576 (-19%)
+  if (M >= 2048 && N >= 1024 && K >= 1024 && mnk >= 0x1p37) return 4;
+  // below that, TF32 + BF16 only ties 3xTF32 (16384 x 32768 x 576: 219 vs 217; r01: it won
+  // 3-10% on 16384 x 32768 x (576..1792), the host schedule's K-chunks, before 3xFP16)
+  return (M >= 4096 && N >= 8192 && K >= 512 && mnk >= 0x1p38) ? 2 : 3;
 }
 
 // CTA-group size: 2 (CTA pairs) unless the problem has fewer 256-row tiles than SM pairs,
@@ -1891,19 +1969,25 @@ cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, T
     const int64_t wa = (K + 31) / 32, wb = (N + 31) / 32;
     const size_t bh = up(size_t(K) * ldbh * 2), ebb = up(size_t(n_pad) * 4);
     const size_t ah = up(size_t(M) * ldah * 2), eab = up(size_t(m_pad) * 4);
-    // exception bitmaps + flags: [xb | fb] belongs to B (kept with B for b_prep_reuse)
-    const size_t xbb = up(size_t(K) * wb * 4 + size_t(n_pad) * 4);
-    const size_t xab = up(size_t(M) * wa * 4 + size_t(m_pad) * 4);
+    // exception bitmaps + summaries + flags: [xb | sb2 | fb] belongs to B (kept with B for
+    // b_prep_reuse), [xa | sa2 | fa] to A
+    const int64_t w2a = (wa + 31) / 32, w2b = (K + 31) / 32;
+    const size_t xbb = up(size_t(K) * wb * 4 + size_t(wb) * w2b * 4 + size_t(n_pad) * 4);
+    const size_t xab = up(size_t(M) * wa * 4 + size_t(M) * w2a * 4 + size_t(m_pad) * 4);
     const size_t b_part = 2 * bh + 2 * ebb + xbb;
     ScratchBuf *sb = bpre_scratch(st, b_part + 2 * ah + eab + xab);
     if (!sb) return cudaSuccess;
     uint8_t *scr = static_cast<uint8_t *>(sb->p);
     tp->wa = int(wa);
     tp->wb = int(wb);
+    tp->w2a = int(w2a);
+    tp->w2b = int(w2b);
     tp->xb = reinterpret_cast<unsigned *>(scr + 2 * bh + 2 * ebb);
-    tp->fb = reinterpret_cast<int *>(scr + 2 * bh + 2 * ebb + size_t(K) * wb * 4);
+    tp->sb2 = tp->xb + size_t(K) * wb;
+    tp->fb = reinterpret_cast<int *>(tp->sb2 + size_t(wb) * w2b);
     tp->xa = reinterpret_cast<unsigned *>(scr + b_part + 2 * ah + eab);
-    tp->fa = reinterpret_cast<int *>(scr + b_part + 2 * ah + eab + size_t(M) * wa * 4);
+    tp->sa2 = tp->xa + size_t(M) * wa;
+    tp->fa = reinterpret_cast<int *>(tp->sa2 + size_t(M) * w2a);
     tp->scheme = 4;
     tp->owner = sb;
     tp->ldah = ldah;
@@ -1964,7 +2048,9 @@ cudaError_t launch_prep16_b(const float *B, int64_t ldb, int64_t N, int64_t K, T
   sb->key_b = nullptr;
   cudaError_t e = cudaMemsetAsync(tp->bmax, 0, size_t(n_pad) * 4, st);
   if (e == cudaSuccess)  // exception bitmap + column flags (contiguous)
-    e = cudaMemsetAsync(tp->xb, 0, size_t(K) * tp->wb * 4 + size_t(n_pad) * 4, st);
+    e = cudaMemsetAsync(tp->xb, 0,
+                        size_t(K) * tp->wb * 4 + size_t(tp->wb) * tp->w2b * 4 + size_t(n_pad) * 4,
+                        st);
   if (e != cudaSuccess) return e;
   const int64_t bx = (N + 127) / 128;
   const int64_t by = std::max<int64_t>(1, std::min<int64_t>((K + 7) / 8,
@@ -1978,7 +2064,7 @@ cudaError_t launch_prep16_b(const float *B, int64_t ldb, int64_t N, int64_t K, T
   const int64_t blocks = std::min<int64_t>((units + 255) / 256, int64_t(num_sms_current()) * 8);
   prep16_b_kernel<<<unsigned(std::max<int64_t>(blocks, 1)), 256, 0, st>>>(
       B, ldb, int(K), int(N), tp->eb, const_cast<uint16_t *>(tp->Bh),
-      const_cast<uint16_t *>(tp->Bl), tp->ldbh, tp->xb, tp->wb, tp->fb);
+      const_cast<uint16_t *>(tp->Bl), tp->ldbh, tp->xb, tp->sb2, tp->w2b, tp->fb);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   sb->key_b = tp->key_b = B;
@@ -1992,19 +2078,20 @@ cudaError_t launch_prep16_b(const float *B, int64_t ldb, int64_t N, int64_t K, T
 cudaError_t launch_prep16_a(const float *A, int64_t lda, int64_t M, int64_t K, TermsPrep *tp,
                             cudaStream_t st) {
   const int64_t m_pad = (M + 255) / 256 * 256;
-  cudaError_t e = cudaMemsetAsync(tp->xa, 0, size_t(M) * tp->wa * 4 + size_t(m_pad) * 4, st);
+  cudaError_t e = cudaMemsetAsync(
+      tp->xa, 0, size_t(M) * tp->wa * 4 + size_t(M) * tp->w2a * 4 + size_t(m_pad) * 4, st);
   if (e != cudaSuccess) return e;
   const int64_t cap = int64_t(num_sms_current()) * 4;
   if (K >= 8192) {
     prep16_a_kernel<512><<<unsigned(std::min(m_pad, cap)), 512, 0, st>>>(
         A, lda, int(M), int(m_pad), int(K), const_cast<uint16_t *>(tp->Ah),
         const_cast<uint16_t *>(tp->Al), tp->ldah, const_cast<int *>(tp->ea), tp->xa, tp->wa,
-        tp->fa);
+        tp->sa2, tp->w2a, tp->fa);
   } else {
     prep16_a_kernel<32><<<unsigned(std::min((m_pad + 15) / 16, cap)), 512, 0, st>>>(
         A, lda, int(M), int(m_pad), int(K), const_cast<uint16_t *>(tp->Ah),
         const_cast<uint16_t *>(tp->Al), tp->ldah, const_cast<int *>(tp->ea), tp->xa, tp->wa,
-        tp->fa);
+        tp->sa2, tp->w2a, tp->fa);
   }
   return cudaGetLastError();
 }
@@ -2018,12 +2105,15 @@ cudaError_t launch_fix16(const float *A, int64_t lda, const float *B, int64_t ld
   for (int i = 0; i < peers.n; ++i) peers.p[i] = ex->peer_c[i];
   // grid-strided rows / strips: blocks of rows or strips without exceptions only read a flag
   const int64_t cap = int64_t(num_sms_current()) * 4;
-  fix16_a_kernel<<<unsigned(std::min<int64_t>(M, cap)), 256, 0, st>>>(A, lda, B, ldb, int(M), int(N), tp->Ah, tp->Al,
-                                              tp->ldah, tp->ea, tp->xa, tp->wa, tp->fa, C, ldc,
-                                              peers);
-  fix16_b_kernel<<<unsigned(std::min<int64_t>((N + 31) / 32, cap)), 256, 0, st>>>(
-      B, ldb, int(M), int(N), int(K), tp->Ah, tp->Al, tp->ldah, tp->ea, tp->Bh, tp->Bl,
-      tp->ldbh, tp->eb, tp->xb, tp->wb, tp->fb, C, ldc, peers);
+  fix16_a_kernel<<<unsigned(std::min<int64_t>((M + 31) / 32, cap)), 256, 0, st>>>(
+      A, lda, int(M), int(N), tp->Ah, tp->Al, tp->ldah, tp->ea, tp->Bh, tp->Bl, tp->ldbh, tp->eb,
+      tp->xa, tp->wa, tp->sa2, tp->w2a, tp->fa, C, ldc, peers);
+  // strips x row chunks (a strip's exceptions are applied by all its row-chunk blocks)
+  const dim3 gb(unsigned(std::min<int64_t>((N + 31) / 32, cap)),
+                unsigned(std::max<int64_t>(1, std::min<int64_t>(64, M / 2048))));
+  fix16_b_kernel<<<gb, 256, 0, st>>>(
+      A, lda, B, ldb, int(M), int(N), int(K), tp->Bh, tp->Bl, tp->ldbh, tp->eb, tp->xb, tp->sb2,
+      tp->w2b, tp->fb, C, ldc, peers);
   return cudaGetLastError();
 }
 

@@ -12,18 +12,22 @@ namespace giga {
 // bound, so it keeps 8 too.
 constexpr int kDefaultPromoteKBlocks = 8;
 constexpr int kDefaultPromoteKBlocksT2 = 8;
-// The 3xFP16 scheme (terms = 4) runs 32-wide k-blocks: 4 of them = K 128 per TMEM partial.
-constexpr int kDefaultPromoteKBlocksT4 = 4;
+// The 3xFP16 scheme (terms = 4) runs 32-wide k-blocks: 8 of them = K 256 per TMEM partial
+// (24 truncating adds per K 128 instead of 3xTF32's 48: the same count per partial as 3xTF32 at
+// K 128; measured +8% at 32768^3, worst long-K all-positive error 2.2e-6 vs 1.5e-6 at 4).
+constexpr int kDefaultPromoteKBlocksT4 = 8;
 
 // The promotion interval in effect for `terms` (the defaults above or $GIGA_PROMOTE_KBLOCKS).
 int default_promote_kblocks(int terms = 3);
 
-// The product path's fp32-accurate scheme for an M x N x K launch: 3 = 3xTF32
-// (three kind::tf32 MMAs per k8 step), 2 = TF32 + BF16 (hi*hi as kind::tf32, both corrections
-// as one K=16 kind::f16 MMA, operands prepared once per launch in HBM). 2 where the operand
-// preparation (~12 B per element of A and B) is amortised: M >= 4096, N >= 8192 and either
-// K >= 2048 with M N K >= 2^37 or K >= 512 with M N K >= 2^38 (measured crossover); else 3. $GIGA_SCHEME = "3xtf32" / "tf32bf16" forces one. With pre-split
-// lo operands (A_lo != nullptr) the scheme is always 3.
+// The product path's fp32-accurate scheme for an M x N x K launch:
+// 4 = 3xFP16 (the 3xTF32 split on fp16 operands of power-of-two scaled rows / columns, three
+// K=16 kind::f16 MMAs per k16 step, operands prepared once per launch in HBM, exceptions fixed)
+// where the preparation is amortised: M >= 2048, N >= 1024, K >= 1024, M N K >= 2^37;
+// else 2 = TF32 + BF16 (hi*hi as kind::tf32, both corrections as one K=16 kind::f16 MMA) for
+// M >= 4096, N >= 8192, K >= 512, M N K >= 2^38; else 3 = 3xTF32 (three kind::tf32 MMAs per
+// k8 step, no preparation). Measured crossovers. $GIGA_SCHEME = "3xtf32" / "tf32bf16" /
+// "3xfp16" forces one. With pre-split lo operands (A_lo != nullptr) the scheme is always 3.
 int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K);
 // true when $GIGA_SCHEME forces the scheme (measurements keep it even without scratch)
 bool scheme_forced();
@@ -69,6 +73,10 @@ struct TermsPrep {
   unsigned *xa = nullptr, *xb = nullptr;
   int *fa = nullptr, *fb = nullptr;
   int wa = 0, wb = 0;
+  // summaries of the bitmaps (bit w % 32 of word w / 32 set iff bitmap word w is non-zero):
+  // A per row (w2a words), B per 32-column strip (w2b words over its K words)
+  unsigned *sa2 = nullptr, *sb2 = nullptr;
+  int w2a = 0, w2b = 0;
   int scheme = 2;
   void *owner = nullptr;
   const float *key_b = nullptr;

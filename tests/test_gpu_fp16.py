@@ -145,14 +145,14 @@ def test_sparse_exceptions_mixed_with_normal_data(giga, torch_cuda):
 
 
 def test_split_worst_case_at_the_exception_threshold(giga, torch_cuda):
-    """The products a split error can reach without being an exception: row maximum 2^14
-    (scaled units) meeting a zero of B, the rest 2^-6..2^-4 of it (lo subnormal in fp16,
+    """The products a split error can reach without being an exception: row maximum (scaled
+    to [2^15, 65504)) meeting a zero of B, the rest 2^-21..2^-18 of it (lo subnormal in fp16,
     rounded to 2^-24 steps: up to 2^-20 relative before an element becomes an exception),
     all positive so the errors add coherently. Must stay inside the bound with margin."""
     M, N, K = 256, 256, 8192
     rng = np.random.default_rng(17)
-    A = (rng.uniform(2.0 ** -20, 2.0 ** -18, (M, K))).astype(np.float32)
-    B = (rng.uniform(2.0 ** -20, 2.0 ** -18, (K, N))).astype(np.float32)
+    A = (rng.uniform(2.0 ** -21, 2.0 ** -18, (M, K))).astype(np.float32)
+    B = (rng.uniform(2.0 ** -21, 2.0 ** -18, (K, N))).astype(np.float32)
     A[:, 0] = 1.0
     B[0, :] = 0.0
     B[1, :] = 1.0
