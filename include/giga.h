@@ -19,13 +19,16 @@
  * alpha/beta.
  *
  * Precision: fp32 in, fp32 out, fp32-accurate: internally each product is formed from
- * TF32 hi / lo parts on the tcgen05 tensor cores -- 3xTF32 (a_lo*b_hi + a_hi*b_lo +
- * a_hi*b_hi) or, for large launches, TF32 + BF16 (a_hi*b_hi in TF32, a_lo*b + a_hi*b_lo in
- * one BF16 MMA; giga_product_scheme) -- with partial sums promoted into fp32 registers, so
- * that per element
+ * hi / lo parts with 11-bit significands on the tcgen05 tensor cores (a_lo*b_hi + a_hi*b_lo +
+ * a_hi*b_hi) -- 3xTF32, or for large launches 3xFP16 (the same split on fp16 operands of
+ * power-of-two scaled rows of A / columns of B; the few elements fp16 cannot carry are fixed
+ * in fp64) or TF32 + BF16 (a_hi*b_hi in TF32, a_lo*b + a_hi*b_lo in one BF16 MMA);
+ * giga_product_scheme -- with partial sums promoted into fp32 registers, so that per
+ * element
  *     |C - C_exact| <= 1e-5 * sum_k |A_ik| |B_kj|          (BASELINE.json north_star)
  * and integer-valued inputs whose partial sums stay below 2^24 give bit-exact results.
- * Non-finite inputs: NaN propagates; Inf may turn into NaN (Inf - Inf in the split).
+ * Non-finite inputs: NaN propagates; Inf may turn into NaN (Inf - Inf in the split; a row of
+ * A / column of B holding Inf or NaN gives Inf or NaN in its row / column of C under 3xFP16).
  *
  * Errors: every function returns GIGA_OK (0) or a negative giga_status; the message of the
  * last failure on the calling thread is in giga_last_error(). After a failed call the
@@ -34,8 +37,9 @@
  *
  * Ownership: the caller owns every pointer passed in; the library never keeps a caller
  * pointer after returning. The library owns its streams, events, communicators and
- * workspace (padded copies, host-path staging buffers, the TF32 + BF16 prepared operands,
- * the pre-split low parts in that comparison mode), freed in giga_finalize().
+ * workspace (padded copies, host-path staging buffers, the TF32 + BF16 and 3xFP16 prepared
+ * operands, scales and exception bitmaps, the pre-split low parts in that comparison mode),
+ * freed in giga_finalize().
  *
  * Threading: calls are serialised by an internal mutex (one call at a time per process).
  *
@@ -256,11 +260,18 @@ int giga_gemm_3xtf32(const float *A, const float *A_lo, const float *B, const fl
  * K=16 BF16 MMA per k8 step, split error <= 3 * 2^-19 |a||b| (5.7e-6) per product with the
  * default RN hi (5.3e-6 reached by constructed inputs, tests/adversarial.py); $GIGA_HI_RN=0
  * truncates hi, a measurement mode whose split error reaches ~3 * 2^-18 = 1.1e-5 and can
- * exceed the bound; A_lo and B_lo must be NULL) or 1 (plain TF32: a_hi*b_hi only; A_lo/B_lo
- * ignored). The product path picks 3 or 2 per launch (giga_product_scheme);
- * promote_kblocks = number of 16-wide k-blocks accumulated in TMEM before the partial sum
- * is added into the fp32 register sum; 0 = never promote (one TMEM accumulation over K);
- * -1 = the library default;
+ * exceed the bound; A_lo and B_lo must be NULL), 4 (3xFP16: row i of A scaled by 2^-ea_i and
+ * column j of B by 2^-eb_j (exact) so their maxima lie in [2^15, 65504), x' = hi + lo in fp16
+ * (RN), three K=16 kind::f16 MMAs per k16 step (a_lo b_hi, a_hi b_lo, a_hi b_hi), the
+ * epilogue multiplies by 2^(ea_i + eb_j); elements whose fp16 split is off by more than
+ * 2^-20 of themselves (far below their row's / column's maximum) are exceptions whose
+ * remainders two fix kernels add in fp64 (deterministic); split error <= 2 * 2^-20 + 2^-22
+ * per product; operands prepared once per launch in library-owned HBM scratch; A_lo and B_lo
+ * must be NULL) or 1 (plain TF32: a_hi*b_hi only; A_lo/B_lo ignored). The product path
+ * picks 4, 3 or 2 per launch (giga_product_scheme);
+ * promote_kblocks = number of k-blocks (16 deep; 32 for terms = 4) accumulated in TMEM before
+ * the partial sum is added into the fp32 register sum; 0 = never promote (one TMEM
+ * accumulation over K); -1 = the library default (8);
  * cta_group = 1 (one CTA per 128 x 256 tile), 2 (a CTA pair per 256 x 256 tile, UMMA
  * cta_group::2), 0 = chosen from the shape. */
 int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const float *B_lo,
@@ -283,7 +294,8 @@ int giga_rank_compute_only(const float *A_shard, const float *B, float *C_full, 
  * over an M x N x K product on `num_sms` SMs (<= 0: 148), computed on the host exactly as
  * the launch computes it (no GPU needed). out must hold 8 values:
  * out[0] = CTA-group size (1: 128 x 256 tiles, 2: 256 x 256 tiles on CTA pairs),
- * out[1] = tiles, out[2] = concurrent tiles (clusters), out[3] = k-blocks (16 deep) per tile,
+ * out[1] = tiles, out[2] = concurrent tiles (clusters), out[3] = k-blocks per tile (16 deep;
+ * 32 when the launch runs 3xFP16),
  * out[4] = first_split: tiles [0, first_split) run whole, out[5] = s: every later tile runs
  * as s units over consecutive k-block ranges [n_kb*q/s, n_kb*(q+1)/s), out[6] = work units,
  * out[7] = how the parts combine, both deterministic (the same bits on every launch of the
@@ -294,13 +306,14 @@ int giga_rank_compute_only(const float *A_shard, const float *B, float *C_full, 
 int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *out);
 
 /* The fp32-accurate scheme the product path uses for one M x N x K GEMM launch (host-only,
- * DESIGN.md 6.7): *terms = 3 (3xTF32: three kind::tf32 MMAs per k8 step) or 2 (TF32 + BF16:
- * a_hi*b_hi as one kind::tf32 MMA plus a_lo*b + a_hi*b_lo as one K=16 kind::f16 MMA, with
- * hi = RN tf32(x); A_hi, A', B_hi, B' prepared once per launch in library-owned HBM scratch
- * by two elementwise kernels; per-product split error <= 3 * 2^-19 |a||b|). 2 when M >= 4096,
- * N >= 8192 and either K >= 2048 with M N K >= 2^37 or K >= 512 with M N K >= 2^38 (the
- * preparation is then amortised: measured crossover), else 3;
- * $GIGA_SCHEME = 3xtf32 | tf32bf16 forces one. Errors: INVALID_ARG. */
+ * DESIGN.md 6.7, 6.8): *terms = 4 (3xFP16, see giga_gemm_3xtf32_ex: per-product split error
+ * <= 2 * 2^-20 + 2^-22 |a||b|; 4 preparation kernels and 2 exception-fix kernels per launch)
+ * when M >= 2048, N >= 1024, K >= 1024 and M N K >= 2^37; else 2 (TF32 + BF16: a_hi*b_hi
+ * as one kind::tf32 MMA plus a_lo*b + a_hi*b_lo as one K=16 kind::f16 MMA, hi = RN tf32(x),
+ * operands prepared once per launch; split error <= 3 * 2^-19 |a||b|) when M >= 4096,
+ * N >= 8192, K >= 512 and M N K >= 2^38; else 3 (3xTF32: three kind::tf32 MMAs per k8
+ * step, no preparation). The thresholds are measured crossovers (preparation included);
+ * $GIGA_SCHEME = 3xtf32 | tf32bf16 | 3xfp16 forces one. Errors: INVALID_ARG. */
 int giga_product_scheme(int64_t M, int64_t N, int64_t K, int *terms);
 
 /* ------------------------------------------------------------------------------------ */

@@ -83,6 +83,7 @@ constexpr uint32_t EPI_BYTES = NUM_EPI_WARPS * EPI_STAGE_BYTES;  // 32 KiB C sta
 constexpr size_t EPI_SLOT_BYTES = 32 * 128 * 4;  // K-split partial of one epilogue warp
 constexpr int SCHED_SLOTS = 8;                   // ring of claimed work units (power of 2)
 }  // namespace cfg
+constexpr int kBList = 64;  // 3xFP16: B exceptions listed per 32-column strip
 
 template <int CG>
 struct Tile {
@@ -132,6 +133,19 @@ struct GemmParams {
   // terms == 4 (3xFP16): the accumulator holds sum_k a'_ik b'_kj of the scaled operands
   // a' = a 2^-ea[i], b' = b 2^-eb[j]; the epilogue stores ldexp(sum, ea[i] + eb[j])
   const int *ea, *eb;
+  // ... and adds sum_k a_ik (b_kj - rep(b_kj)) for the exceptions of B in its columns (fused
+  // B-side fix; nullptr xb: none): the original A / B, the fp16 B_hi / B_lo, B's exception
+  // bitmap (strip-major), its summary and the per-column flags
+  const float *fA, *fB;
+  int64_t flda, fldb, fldbh;
+  const uint16_t *fBh, *fBl;
+  const unsigned *xb, *sb2;
+  const int *fb;
+  int w2b;
+  // per strip of 32 columns: the number of B exceptions and (up to kBList of them) the list
+  // (k, column in the strip, b - rep(b) as fp64 halves) in column-then-k order (compact16_b)
+  const int *bcnt;
+  const int4 *blist;
 };
 
 // C tensor maps: [0] this GPU's C, [1..] the same rows of the peers' C_full buffers.
@@ -180,6 +194,94 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int m, int n) {
 __host__ __device__ constexpr uint32_t make_idesc_f16(int m, int n) {
   return (1u << 4) | (0u << 7) | (0u << 10) | (0u << 15) | (1u << 16) |
          (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+
+// The B-side exception fix of one 32 x 32 block of C from its strip's exception list (the
+// common path): lanes (= rows of C) read the list entries by broadcast, sum a_ik d_kj in fp64
+// per column in ascending k (4 entries' A loads in flight at a time) and add each column's sum,
+// rounded once, to the staged value.
+__device__ __forceinline__ void fix_b_list(const GemmParams &p, float *stg, int row, int strip,
+                                           int cnt, int lane) {
+  const int4 *Lst = p.blist + int64_t(strip) * kBList;
+  const bool live = row < p.M;
+  const float *arow = p.fA + int64_t(live ? row : 0) * p.flda;
+  int cur = -1;
+  double t = 0.0;
+  for (int q0 = 0; q0 < cnt; q0 += 4) {
+    int4 en[4];
+    float av[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) en[u] = q0 + u < cnt ? Lst[q0 + u] : make_int4(0, -1, 0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) av[u] = (live && q0 + u < cnt) ? arow[en[u].x] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (q0 + u >= cnt) break;
+      if (en[u].y != cur) {
+        if (cur >= 0) {
+          float *v = stg + lane * 32 + (((cur >> 2) ^ (lane & 7)) << 2) + (cur & 3);
+          *v = float(double(*v) + t);
+        }
+        cur = en[u].y;
+        t = 0.0;
+      }
+      t = fma(double(av[u]), __hiloint2double(en[u].w, en[u].z), t);
+    }
+  }
+  if (cur >= 0) {
+    float *v = stg + lane * 32 + (((cur >> 2) ^ (lane & 7)) << 2) + (cur & 3);
+    *v = float(double(*v) + t);
+  }
+}
+
+// The B-side exception fix of one 32 x 32 block of C in the epilogue's staging tile (3xFP16),
+// by scanning the strip's bitmap (strips whose list overflowed kBList: pathological inputs):
+// for each column of the block (a strip of B) flagged with exceptions, every lane (= one row
+// of C) sums a_ik (b_kj - rep(b_kj)) in fp64 over the column's exceptions in ascending k and
+// adds it, rounded once, to its staged value. Columns without exceptions cost one flag read
+// per block; the common case (uniform data: ~1e-6 of B's elements) touches nothing else.
+__device__ __forceinline__ void fix_b_block(const GemmParams &p, float *stg, int row, int col0,
+                                         int lane) {
+  const int j = col0 + lane;
+  unsigned cols = __ballot_sync(0xffffffffu, j < p.N && p.fb[j] != 0);
+  if (!cols) return;
+  const int strip = col0 >> 5;
+  const unsigned *S = p.sb2 + int64_t(strip) * p.w2b;
+  const unsigned *L = p.xb + int64_t(strip) * p.K;
+  const bool live = row < p.M;
+  while (cols) {
+    const int jb = __ffs(cols) - 1;
+    cols &= cols - 1;
+    const int jj = col0 + jb;
+    const int e = p.eb[jj];
+    double t = 0.0;
+    for (int c0 = 0; c0 < p.w2b; c0 += 32) {
+      const unsigned sw = c0 + lane < p.w2b ? S[c0 + lane] : 0u;
+      unsigned nz = __ballot_sync(0xffffffffu, sw != 0u);
+      while (nz) {
+        const int src = __ffs(nz) - 1;
+        nz &= nz - 1;
+        const unsigned swv = __shfl_sync(0xffffffffu, sw, src);
+        const int k = (c0 + src) * 32 + lane;
+        const bool hit = ((swv >> lane) & 1u) && k < p.K && ((L[k] >> jb) & 1u);
+        unsigned hits = __ballot_sync(0xffffffffu, hit);
+        while (hits) {
+          const int q = __ffs(hits) - 1;
+          hits &= hits - 1;
+          const int kk = (c0 + src) * 32 + q;
+          const int64_t o = int64_t(kk) * p.fldbh + jj;
+          const double rb =
+              ldexp(double(__half2float(__ushort_as_half(p.fBh[o]))) +
+                        double(__half2float(__ushort_as_half(p.fBl[o]))), e);
+          const double d = double(p.fB[int64_t(kk) * p.fldb + jj]) - rb;
+          if (live) t = fma(double(p.fA[int64_t(row) * p.flda + kk]), d, t);
+        }
+      }
+    }
+    // staging tile: row `lane`, 16-byte chunk (jb / 4) ^ (lane & 7), 128-byte rows
+    float *v = stg + lane * 32 + (((jb >> 2) ^ (lane & 7)) << 2) + (jb & 3);
+    *v = float(double(*v) + t);
+  }
 }
 
 // ---- split: lo = x - tf32(x) ------------------------------------------------------------
@@ -902,6 +1004,18 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
           ptx::st_shared_v4(stg + off, sum[c * 32 + 4 * j], sum[c * 32 + 4 * j + 1],
                             sum[c * 32 + 4 * j + 2], sum[c * 32 + 4 * j + 3]);
         }
+        // 3xFP16: the B-side exceptions of these 32 columns (once per tile: not in the
+        // second half of a reduce-split tile)
+        // (blocks right of N -- clipped by the TMA store -- have no strip)
+        if (p.xb && ccol0 + 32 * c < p.N && !(part > 0 && p.split_mode == kSplitReduce)) {
+          const int strip = (ccol0 + 32 * c) >> 5;
+          const int cnt = p.bcnt[strip];
+          float *stgf = reinterpret_cast<float *>(epi_stage + e * EPI_STAGE_BYTES);
+          if (cnt > kBList)
+            fix_b_block(p, stgf, crow0 + lane, ccol0 + 32 * c, lane);
+          else if (cnt > 0)
+            fix_b_list(p, stgf, crow0 + lane, strip, cnt, lane);
+        }
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -1229,6 +1343,56 @@ __global__ void __launch_bounds__(256) prep16_bmax_kernel(const float *__restric
   }
 }
 
+// B pass 4 (after the writes): the exception list of every strip of 32 columns, one warp per
+// strip: for each flagged column (ascending) its exceptions in ascending k, as (k, column in
+// the strip, b - rep(b) in fp64), up to kBList entries; bcnt = the strip's total (a total above
+// kBList sends the epilogue to the bitmap scan instead).
+__global__ void __launch_bounds__(256) compact16_b_kernel(
+    const float *__restrict__ B, int64_t ldb, int N, int K, const uint16_t *__restrict__ Bh,
+    const uint16_t *__restrict__ Bl, int64_t ldbh, const int *__restrict__ eb,
+    const unsigned *__restrict__ bits, const unsigned *__restrict__ summ, int w2,
+    const int *__restrict__ flag, int *__restrict__ bcnt, int4 *__restrict__ blist) {
+  const int lane = threadIdx.x & 31;
+  const int strip = blockIdx.x * 8 + int(threadIdx.x >> 5);
+  if (strip * 32 >= N) return;
+  const int j = strip * 32 + lane;
+  unsigned cols = __ballot_sync(0xffffffffu, j < N && flag[j] != 0);
+  const unsigned *S = summ + int64_t(strip) * w2;
+  const unsigned *L = bits + int64_t(strip) * K;
+  int4 *out = blist + int64_t(strip) * kBList;
+  int n = 0;
+  while (cols) {
+    const int jb = __ffs(cols) - 1;
+    cols &= cols - 1;
+    const int jj = strip * 32 + jb;
+    const int e = eb[jj];
+    for (int c0 = 0; c0 < w2; c0 += 32) {
+      const unsigned sw = c0 + lane < w2 ? S[c0 + lane] : 0u;
+      unsigned nz = __ballot_sync(0xffffffffu, sw != 0u);
+      while (nz) {
+        const int src = __ffs(nz) - 1;
+        nz &= nz - 1;
+        const unsigned swv = __shfl_sync(0xffffffffu, sw, src);
+        const int k = (c0 + src) * 32 + lane;
+        const bool hit = ((swv >> lane) & 1u) && k < K && ((L[k] >> jb) & 1u);
+        const unsigned hits = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int pos = n + __popc(hits & ((1u << lane) - 1u));
+          if (pos < kBList) {
+            const int64_t o = int64_t(k) * ldbh + jj;
+            const double d = double(B[int64_t(k) * ldb + jj]) -
+                             ldexp(double(__half2float(__ushort_as_half(Bh[o]))) +
+                                       double(__half2float(__ushort_as_half(Bl[o]))), e);
+            out[pos] = make_int4(k, jb, __double2loint(d), __double2hiint(d));
+          }
+        }
+        n += __popc(hits);
+      }
+    }
+  }
+  if (lane == 0) bcnt[strip] = n;
+}
+
 // B pass 2: eb[j] for every padded column (bmax of padding columns is 0 -> exponent 0).
 __global__ void prep16_bexp_kernel(const unsigned *__restrict__ bmax, int n_pad,
                                    int *__restrict__ eb) {
@@ -1291,13 +1455,14 @@ __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__
 
 // ---- 3xFP16 exceptions: C += the remainders the split could not carry -----------------------
 // a b = rep(a) rep(b) + (a - rep(a)) rep(b) + a (b - rep(b)) exactly, rep(x) = 2^e (hi + lo).
-// The GEMM computes rep(a) rep(b); fix16_a adds (a - rep(a)) rep(b) for the exceptions of A
-// (row by row: rep(b) rows are contiguous), fix16_b adds a (b - rep(b)) for those of B (column
-// strip by column strip, reading A's fp32 column: one sector per row and exception). Both
-// sum in fp64 in ascending k and round once into C (deterministic), mirror the new value to
-// the peers' copies when the epilogue also wrote those (fused gather), and do nothing for rows /
-// strips without exceptions -- the common case: uniform data has ~1e-6 of its elements more
-// than 2^20 below their row / column maximum.
+// The GEMM computes rep(a) rep(b) and, in its epilogue, adds a (b - rep(b)) for the exceptions
+// of B in each block's columns (fix_b_block: C is still on chip, the A reads overlap the next
+// tile's MMAs); fix16_a (after the GEMM) adds (a - rep(a)) rep(b) for those of A row by row
+// (rep(b) rows are contiguous). Both sum in fp64 in ascending k and round once into C
+// (deterministic); fix16_a mirrors the new values to the peers' copies when the epilogue also
+// wrote those (fused gather), and skips rows without exceptions -- the common case: float
+// data has ~1e-6 of its elements more than 2^20 below their row / column maximum (the synth
+// distributions, fixed-point grids, have none).
 struct PeerC {
   float *p[kMaxCDst - 1];
   int n;
@@ -1362,6 +1527,9 @@ __global__ void __launch_bounds__(256) fix16_a_kernel(
   __shared__ double ds[kFixCap];
   __shared__ int n_sh, s_sh, nrows;
   __shared__ int rows[256];
+  // this block's columns: chunk blockIdx.y of gridDim.y (multiples of 4)
+  const int chunk = ((N + int(gridDim.y) - 1) / int(gridDim.y) + 3) & ~3;
+  const int jlo = int(blockIdx.y) * chunk, jhi = min(N, jlo + chunk);
   for (int base = blockIdx.x * 32; base < M; base += gridDim.x * 32) {
     // the flags of 256 rows at once; the rows holding exceptions (any order: rows are
     // independent)
@@ -1403,7 +1571,7 @@ __global__ void __launch_bounds__(256) fix16_a_kernel(
         // 4 columns per thread and step (N, ldc, ldbh are multiples of 4: float4 / 8-byte
         // loads), all loads of a step issued before the stores
         float *__restrict__ crow = C + int64_t(i) * ldc;
-        for (int j = 4 * int(threadIdx.x); j < N && n > 0; j += 4 * int(blockDim.x)) {
+        for (int j = jlo + 4 * int(threadIdx.x); j < jhi && n > 0; j += 4 * int(blockDim.x)) {
           const int4 ev = *reinterpret_cast<const int4 *>(eb + j);
           double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
           for (int q = 0; q < n; ++q) {
@@ -1425,103 +1593,6 @@ __global__ void __launch_bounds__(256) fix16_a_kernel(
         }
         __syncthreads();  // the next pass overwrites the staged exceptions
       }
-    }
-  }
-}
-
-// Blocks take strips of 32 columns of B (grid-strided; strips without exceptions cost one flag
-// read) times a chunk of the rows of C (blockIdx.y). Warp 0 stages the strip's exceptions in
-// ascending k (then j) through the strip's summary words, counting-sorts them by column, then
-// every thread takes rows i and adds sum_k a_ik delta_kj to C[i][j] per column.
-__global__ void __launch_bounds__(256) fix16_b_kernel(
-    const float *__restrict__ A, int64_t lda, const float *__restrict__ B, int64_t ldb, int M,
-    int N, int K, const uint16_t *__restrict__ Bh, const uint16_t *__restrict__ Bl, int64_t ldbh,
-    const int *__restrict__ eb, const unsigned *__restrict__ bits,
-    const unsigned *__restrict__ summ, int w2, const int *__restrict__ flag,
-    float *__restrict__ C, int64_t ldc, const PeerC peers) {
-  __shared__ int ks[kFixCap];
-  __shared__ unsigned char js[kFixCap];
-  __shared__ double ds[kFixCap];
-  __shared__ int sk[kFixCap];
-  __shared__ double sd[kFixCap];
-  __shared__ int seg[33];
-  __shared__ int n_sh, s_sh, any_sh;
-  const int rows_per = (M + int(gridDim.y) - 1) / int(gridDim.y);
-  const int i0 = int(blockIdx.y) * rows_per, i1 = min(M, i0 + rows_per);
-  for (int st = blockIdx.x; st * 32 < N; st += gridDim.x) {
-    const int j0 = st * 32;
-    if (threadIdx.x < 32) {
-      const int j = j0 + int(threadIdx.x);
-      const unsigned any = __ballot_sync(0xffffffffu, j < N && flag[j] != 0);
-      if (threadIdx.x == 0) any_sh = any != 0u;
-    }
-    __syncthreads();
-    const bool any = any_sh;
-    __syncthreads();  // any_sh is rewritten for the next strip
-    if (!any) continue;
-    for (int s = 0; s < w2;) {
-      if (threadIdx.x < 32) {
-        const int2 r = stage_exceptions(
-            summ + int64_t(st) * w2, w2, bits + int64_t(st) * K, K, s,
-            [&](int pos, int k, int jb) {
-              const int j = j0 + jb;
-              const int64_t o = int64_t(k) * ldbh + j;
-              ks[pos] = k;
-              js[pos] = (unsigned char)jb;
-              ds[pos] = double(B[int64_t(k) * ldb + j]) - rep16(Bh[o], Bl[o], eb[j]);
-            });
-        const int n = r.x;
-        // counting sort by column (stable: ascending k within a column)
-        int cnt = 0;
-        for (int q = 0; q < n; ++q) cnt += js[q] == threadIdx.x;
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (threadIdx.x >= unsigned(o)) incl += y;
-        }
-        int pos = incl - cnt;
-        seg[threadIdx.x] = pos;
-        if (threadIdx.x == 31) seg[32] = incl;
-        for (int q = 0; q < n; ++q)
-          if (js[q] == threadIdx.x) {
-            sk[pos] = ks[q];
-            sd[pos++] = ds[q];
-          }
-        if (threadIdx.x == 0) {
-          n_sh = n;
-          s_sh = r.y;
-        }
-      }
-      __syncthreads();
-      const int n = n_sh;
-      s = s_sh;
-      // 4 rows per thread and step (their loads independent of each other and of the stores)
-      const int step = 4 * int(blockDim.x);
-      for (int ib = i0 + int(threadIdx.x); ib < i1 && n > 0; ib += step) {
-        for (int jb = 0; jb < 32; ++jb) {
-          const int q0 = seg[jb], q1 = seg[jb + 1];
-          if (q0 == q1) continue;
-          double t[4] = {0.0, 0.0, 0.0, 0.0};
-          for (int q = q0; q < q1; ++q) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int i = ib + u * int(blockDim.x);
-              if (i < i1) t[u] = fma(double(A[int64_t(i) * lda + sk[q]]), sd[q], t[u]);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = ib + u * int(blockDim.x);
-            if (i >= i1) continue;
-            const int64_t c = int64_t(i) * ldc + j0 + jb;
-            const float v = float(double(C[c]) + t[u]);
-            C[c] = v;
-            for (int pi = 0; pi < peers.n; ++pi) peers.p[pi][c] = v;
-          }
-        }
-      }
-      __syncthreads();
     }
   }
 }
@@ -1973,8 +2044,9 @@ cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, T
     // b_prep_reuse), [xa | sa2 | fa] to A
     const int64_t w2a = (wa + 31) / 32, w2b = (K + 31) / 32;
     const size_t xbb = up(size_t(K) * wb * 4 + size_t(wb) * w2b * 4 + size_t(n_pad) * 4);
+    const size_t blb = up(size_t(wb) * 4) + up(size_t(wb) * kBList * 16);  // bcnt + blist
     const size_t xab = up(size_t(M) * wa * 4 + size_t(M) * w2a * 4 + size_t(m_pad) * 4);
-    const size_t b_part = 2 * bh + 2 * ebb + xbb;
+    const size_t b_part = 2 * bh + 2 * ebb + xbb + blb;
     ScratchBuf *sb = bpre_scratch(st, b_part + 2 * ah + eab + xab);
     if (!sb) return cudaSuccess;
     uint8_t *scr = static_cast<uint8_t *>(sb->p);
@@ -1985,6 +2057,8 @@ cudaError_t terms_prep_alloc(int64_t M, int64_t N, int64_t K, cudaStream_t st, T
     tp->xb = reinterpret_cast<unsigned *>(scr + 2 * bh + 2 * ebb);
     tp->sb2 = tp->xb + size_t(K) * wb;
     tp->fb = reinterpret_cast<int *>(tp->sb2 + size_t(wb) * w2b);
+    tp->bcnt = reinterpret_cast<int *>(scr + 2 * bh + 2 * ebb + xbb);
+    tp->blist = reinterpret_cast<int4 *>(scr + 2 * bh + 2 * ebb + xbb + up(size_t(wb) * 4));
     tp->xa = reinterpret_cast<unsigned *>(scr + b_part + 2 * ah + eab);
     tp->sa2 = tp->xa + size_t(M) * wa;
     tp->fa = reinterpret_cast<int *>(tp->sa2 + size_t(M) * w2a);
@@ -2065,6 +2139,9 @@ cudaError_t launch_prep16_b(const float *B, int64_t ldb, int64_t N, int64_t K, T
   prep16_b_kernel<<<unsigned(std::max<int64_t>(blocks, 1)), 256, 0, st>>>(
       B, ldb, int(K), int(N), tp->eb, const_cast<uint16_t *>(tp->Bh),
       const_cast<uint16_t *>(tp->Bl), tp->ldbh, tp->xb, tp->sb2, tp->w2b, tp->fb);
+  compact16_b_kernel<<<unsigned((tp->wb + 7) / 8), 256, 0, st>>>(
+      B, ldb, int(N), int(K), tp->Bh, tp->Bl, tp->ldbh, tp->eb, tp->xb, tp->sb2, tp->w2b, tp->fb,
+      tp->bcnt, tp->blist);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   sb->key_b = tp->key_b = B;
@@ -2105,15 +2182,12 @@ cudaError_t launch_fix16(const float *A, int64_t lda, const float *B, int64_t ld
   for (int i = 0; i < peers.n; ++i) peers.p[i] = ex->peer_c[i];
   // grid-strided rows / strips: blocks of rows or strips without exceptions only read a flag
   const int64_t cap = int64_t(num_sms_current()) * 4;
-  fix16_a_kernel<<<unsigned(std::min<int64_t>((M + 31) / 32, cap)), 256, 0, st>>>(
+  // row windows x column chunks (each flagged row is fixed by gridDim.y blocks side by side)
+  const dim3 ga(unsigned(std::min<int64_t>((M + 31) / 32, cap)),
+                unsigned(std::max<int64_t>(1, std::min<int64_t>(8, N / 4096))));
+  fix16_a_kernel<<<ga, 256, 0, st>>>(
       A, lda, int(M), int(N), tp->Ah, tp->Al, tp->ldah, tp->ea, tp->Bh, tp->Bl, tp->ldbh, tp->eb,
       tp->xa, tp->wa, tp->sa2, tp->w2a, tp->fa, C, ldc, peers);
-  // strips x row chunks (a strip's exceptions are applied by all its row-chunk blocks)
-  const dim3 gb(unsigned(std::min<int64_t>((N + 31) / 32, cap)),
-                unsigned(std::max<int64_t>(1, std::min<int64_t>(64, M / 2048))));
-  fix16_b_kernel<<<gb, 256, 0, st>>>(
-      A, lda, B, ldb, int(M), int(N), int(K), tp->Bh, tp->Bl, tp->ldbh, tp->eb, tp->xb, tp->sb2,
-      tp->w2b, tp->fb, C, ldc, peers);
   return cudaGetLastError();
 }
 
@@ -2207,6 +2281,14 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.a_pre = 0;
   p.ea = nullptr;
   p.eb = nullptr;
+  p.fA = p.fB = nullptr;
+  p.flda = p.fldb = p.fldbh = 0;
+  p.fBh = p.fBl = nullptr;
+  p.xb = p.sb2 = nullptr;
+  p.fb = nullptr;
+  p.w2b = 0;
+  p.bcnt = nullptr;
+  p.blist = nullptr;
   // k-block width in elements of K: 16 (tf32 schemes), 32 (3xFP16)
   const int bk = terms == 4 ? 32 : BK;
   TermsPrep local4;
@@ -2235,6 +2317,20 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
       return cudaErrorInvalidValue;
     p.ea = tp->ea;
     p.eb = tp->eb;
+    // the B-side exception fix runs in the epilogue (fix_b_block)
+    p.fA = A;
+    p.flda = lda;
+    p.fB = B;
+    p.fldb = ldb;
+    p.fBh = tp->Bh;
+    p.fBl = tp->Bl;
+    p.fldbh = tp->ldbh;
+    p.xb = tp->xb;
+    p.sb2 = tp->sb2;
+    p.fb = tp->fb;
+    p.w2b = tp->w2b;
+    p.bcnt = tp->bcnt;
+    p.blist = tp->blist;
     tp4 = tp;
   }
   if (terms == 2) {

@@ -77,6 +77,9 @@ struct TermsPrep {
   // A per row (w2a words), B per 32-column strip (w2b words over its K words)
   unsigned *sa2 = nullptr, *sb2 = nullptr;
   int w2a = 0, w2b = 0;
+  // per strip of 32 columns of B: its exception count and list (compact16_b_kernel)
+  int *bcnt = nullptr;
+  int4 *blist = nullptr;
   int scheme = 2;
   void *owner = nullptr;
   const float *key_b = nullptr;
@@ -115,12 +118,13 @@ struct GemmExtra {
   // on the same stream; run_gemm does, to time them apart from the GEMM)
   int defer_fix = 0;
 };
-// The 3xFP16 exception fixes of a launch whose GEMM ran with defer_fix (same arguments).
+// The 3xFP16 A-side exception fix of a launch whose GEMM ran with defer_fix (same arguments;
+// the B-side fix runs inside the GEMM's epilogue).
 cudaError_t launch_fix16(const float *A, int64_t lda, const float *B, int64_t ldb, int64_t M,
                          int64_t N, int64_t K, const TermsPrep *tp, float *C, int64_t ldc,
                          const GemmExtra *ex, cudaStream_t st);
 // Kernels launch_prep16_b / launch_prep16_a / launch_fix16 issue (bench.py's launch count).
-constexpr int kPrep16BLaunches = 3, kPrep16ALaunches = 1, kFix16Launches = 2;
+constexpr int kPrep16BLaunches = 4, kPrep16ALaunches = 1, kFix16Launches = 1;
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
                                const float *B_lo, float *C, int64_t M, int64_t N, int64_t K,
                                int64_t ldc, int terms, int promote_kblocks, cudaStream_t st,

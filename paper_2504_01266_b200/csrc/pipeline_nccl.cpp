@@ -197,7 +197,7 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
     for (auto &p : parts) {
       CK(cudaSetDevice(p.d->dev));
       CK(cudaEventRecord(p.d->ev_kchunk[c], p.d->comm));
-      TRY(tr[&p - &parts[0]].mark("bcast", p.d->comm));
+      TRY(tr[&p - &parts[0]].mark("bcast", p.d->comm, 4.0 * double(kb[c + 1] - kb[c]) * N));
     }
   }
   // 2. compute: K-chunks accumulate into C; the last one in row chunks
@@ -259,7 +259,13 @@ int run_pipeline(std::vector<Part> &parts, int world, int64_t M, int64_t N, int6
     TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
     for (auto &p : parts) {
       CK(cudaSetDevice(p.d->dev));
-      TRY(tr[&p - &parts[0]].mark("gather", p.d->comm));
+      double rows_in = 0;  // rows of C this GPU receives in round q
+      for (int o = 0; o < world; ++o) {
+        int64_t b0, brows;
+        plan_block(M, world, pc, o, q, &b0, &brows);
+        if (o != p.rank && brows > 0) rows_in += double(brows);
+      }
+      TRY(tr[&p - &parts[0]].mark("gather", p.d->comm, 4.0 * rows_in * N));
     }
   }
   // 4. the caller's stream resumes after the gather

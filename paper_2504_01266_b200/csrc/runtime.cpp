@@ -250,6 +250,10 @@ int shard_compute(DevCtx &d, cudaStream_t st, const float *A, int64_t rows, cons
   CK(cudaMemsetAsync(d.B_pad.p, 0, size_t(K4 * N4) * 4, st));
   CK(cudaMemcpy2DAsync(d.B_pad.p, N4 * 4, B, N * 4, N * 4, K, cudaMemcpyDeviceToDevice, st));
   TRY(split(fptr(d.B_pad), lo_at(d.B_lo), K4 * N4, st));
+  // C_pad is fully written by the GEMM's TMA bulk stores; compute-sanitizer's initcheck does
+  // not see those as initialising it and flags the copy-out below, so the (cold) padded path
+  // zero-fills it first
+  CK(cudaMemsetAsync(d.C_pad.p, 0, size_t(rows * N4) * 4, st));
   TRY(gemm(fptr(d.A_pad), lo_at(d.A_lo), fptr(d.B_pad), lo_at(d.B_lo), fptr(d.C_pad), rows, N4,
            K4, N4, st));
   CK(cudaMemcpy2DAsync(C, ldc * 4, d.C_pad.p, N4 * 4, N * 4, rows, cudaMemcpyDeviceToDevice,
@@ -405,7 +409,16 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, int world, bool aligned) {
   pl.kb[1] = K;
   if (!aligned) return pl;
   const bool p2p = transport_p2p();
-  const double bw = p2p ? 770e9 : 600e9, R = 255e12;
+  // transfer rate: the copy-engine chain at the NVLink peer-copy rate (770 GB/s measured,
+  // B200_PROFILING.md); NCCL's kernels capped at $GIGA_NCCL_MAX_CTAS (= $GIGA_COMM_SMS, 8) CTAs
+  // at an assumed $GIGA_NCCL_CTA_GBPS (50) GB/s each, at most 600 GB/s -- a model input to be
+  // calibrated with GIGA_TRACE's per-chunk GB/s on a multi-GPU box.
+  const double nccl_ctas = std::max(1, env_int("GIGA_NCCL_MAX_CTAS", env_int("GIGA_COMM_SMS", 8)));
+  const double bw = p2p ? 770e9
+                        : std::min(600e9, nccl_ctas * std::max(1, env_int("GIGA_NCCL_CTA_GBPS", 50)) * 1e9);
+  // the shard GEMM's rate by the scheme its launches run (measured)
+  const int terms = product_terms(nullptr, rows_max, N, K);
+  const double R = terms == 4 ? 400e12 : terms == 2 ? 265e12 : 250e12;
   const double O = std::max(0, env_int("GIGA_LAUNCH_US", 20)) * 1e-6;
   const double r_max = std::min(4.0, std::max(1.0, 0.8 * double(rows_max) * bw / (2.0 * R)));
   const int hops = p2p ? std::max(1, world - 1) : 1;
@@ -482,8 +495,9 @@ Trace::Trace(DevCtx &d, const char *what) : d_(d), what_(what) {
 
 int Trace::start(cudaStream_t st) { return on_ ? mark("", st) : GIGA_OK; }
 
-int Trace::mark(const char *series, cudaStream_t st) {
+int Trace::mark(const char *series, cudaStream_t st, double bytes) {
   if (!on_) return GIGA_OK;
+  bytes_.push_back(bytes);
   if (n_ >= d_.ev_trace.size()) {
     cudaEvent_t e = nullptr;
     CK(cudaEventCreate(&e));
@@ -504,14 +518,23 @@ void Trace::meta(const char *key, double v) {
 int Trace::finish() {
   if (!on_ || marks_.empty()) return GIGA_OK;
   for (auto &m : marks_) CK(cudaEventSynchronize(d_.ev_trace[m.second]));
-  std::map<std::string, std::string> series;
+  std::map<std::string, std::string> series, rates;
+  std::map<std::string, float> last;  // previous mark of each series (ms)
   for (size_t i = 1; i < marks_.size(); ++i) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, d_.ev_trace[marks_[0].second], d_.ev_trace[marks_[i].second]));
     std::string &v = series[marks_[i].first];
-    char buf[32];
+    char buf[48];
     snprintf(buf, sizeof buf, "%s%.4f", v.empty() ? "" : ", ", ms);
     v += buf;
+    if (bytes_[i] > 0) {  // achieved rate of the interval since this series' previous mark
+      const float t0 = last.count(marks_[i].first) ? last[marks_[i].first] : 0.0f;
+      std::string &r = rates[marks_[i].first];
+      snprintf(buf, sizeof buf, "%s%.1f", r.empty() ? "" : ", ",
+               ms > t0 ? bytes_[i] / ((ms - t0) * 1e-3) / 1e9 : 0.0);
+      r += buf;
+    }
+    last[marks_[i].first] = ms;
   }
   std::string out = "{\"trace\": \"" + std::string(what_) + "\", \"device\": " +
                     std::to_string(d_.dev) + ", \"meta\": {" + meta_ + "}, \"ms\": {";
@@ -520,7 +543,17 @@ int Trace::finish() {
     out += (first ? "\"" : ", \"") + kv.first + "\": [" + kv.second + "]";
     first = false;
   }
-  out += "}}\n";
+  out += "}";
+  if (!rates.empty()) {
+    out += ", \"GBps\": {";
+    first = true;
+    for (auto &kv : rates) {
+      out += (first ? "\"" : ", \"") + kv.first + "\": [" + kv.second + "]";
+      first = false;
+    }
+    out += "}";
+  }
+  out += "}\n";
   fputs(out.c_str(), stderr);
   return GIGA_OK;
 }

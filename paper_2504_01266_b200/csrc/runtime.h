@@ -188,7 +188,9 @@ class Trace {
   Trace(DevCtx &d, const char *what);
   bool on() const { return on_; }
   int start(cudaStream_t st);                  // the zero of the timeline
-  int mark(const char *series, cudaStream_t st);
+  // bytes > 0: the bytes the stream moved since its previous mark of this series (or since
+  // start); finish() then also reports the achieved GB/s of each such interval
+  int mark(const char *series, cudaStream_t st, double bytes = 0);
   void meta(const char *key, double v);
   int finish();                                // waits for the last marks, prints the line
 
@@ -198,6 +200,7 @@ class Trace {
   bool on_ = false;
   size_t n_ = 0;
   std::vector<std::pair<std::string, size_t>> marks_;
+  std::vector<double> bytes_;
   std::string meta_;
 };
 

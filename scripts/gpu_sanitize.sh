@@ -1,7 +1,7 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || tail -5 gpurun_out/build.log
 : > gpurun_out/compute_sanitizer.txt
-for tool in memcheck racecheck synccheck; do
+for tool in memcheck racecheck synccheck initcheck; do
   timeout -s KILL 900 compute-sanitizer --tool $tool python scripts/sanitize_small.py > gpurun_out/san_$tool.log 2>&1
   echo "$tool rc=$?: $(grep -E 'sanitize script ok' gpurun_out/san_$tool.log | head -1)" >> gpurun_out/compute_sanitizer.txt
   grep -E "ERROR SUMMARY|RACECHECK SUMMARY|Error:|access at" gpurun_out/san_$tool.log | sed "s/^/$tool: /" | head -8 >> gpurun_out/compute_sanitizer.txt

@@ -1,4 +1,6 @@
-"""Small GEMM / split / dot calls for compute-sanitizer runs (memcheck, racecheck, synccheck)."""
+"""Small GEMM / split / dot calls for compute-sanitizer runs (memcheck, racecheck, synccheck,
+initcheck): every scheme (3xTF32, TF32 + BF16, 3xFP16 with exceptions), both tile variants,
+the host-buffer path, the dot product and the peer-to-peer transport."""
 import os, sys
 import numpy as np
 import torch
@@ -40,6 +42,26 @@ for cg in (1, 2):
     giga.gemm_3xtf32(dAi, None, dBi, None, C3, M, N, K, terms=2, cta_group=cg)
     torch.cuda.synchronize()
     assert torch.equal(C3, ref), ("terms 2", cg)
+# 3xFP16 (terms 4): scaled fp16 operands prepared in HBM, f16 MMAs, exception bitmaps, the
+# B-side fix in the epilogue (per-strip lists) and the A-side fix kernel: integer inputs exact;
+# inputs made of exceptions (each row's / column's maximum meets the other operand's zeros)
+for cg in (1, 2):
+    C4 = torch.full((M, N), float("nan"), device="cuda")
+    giga.gemm_3xtf32(dAi, None, dBi, None, C4, M, N, K, terms=4, cta_group=cg)
+    torch.cuda.synchronize()
+    assert torch.equal(C4, ref), ("terms 4", cg)
+rng = np.random.default_rng(3)
+Ae = rng.uniform(0.5, 1.0, (M, K)).astype(np.float32) * np.float32(2.0 ** -25)
+Be = rng.uniform(0.5, 1.0, (K, N)).astype(np.float32) * np.float32(2.0 ** -22)
+Ae[:, 0] = 1.0; Be[0, :] = 0.0; Be[1, :] = 1.0; Ae[:, 1] = 0.0
+Be[5:9, 3] *= np.float32(2.0 ** -30)  # a few list entries in strip 0 next to the heavy ones
+C4 = torch.full((M, N), float("nan"), device="cuda")
+giga.gemm_3xtf32(torch.from_numpy(Ae).cuda(), None, torch.from_numpy(Be).cuda(), None, C4,
+                 M, N, K, terms=4)
+torch.cuda.synchronize()
+ex = Ae.astype(np.float64) @ Be.astype(np.float64)
+S = np.abs(Ae.astype(np.float64)) @ np.abs(Be.astype(np.float64))
+assert np.all(np.abs(C4.cpu().numpy() - ex) <= 1e-5 * S), "terms 4 exceptions"
 x = synth.gen_vector(100003, 3, "d3"); y = synth.gen_vector(100003, 4, "d3")
 print("dot", giga.dot(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()))
 giga.finalize()

@@ -76,3 +76,31 @@ WORST_PAIRS = [
     (float.fromhex("0x1.091fd0p+0"), float.fromhex("0x1.00dfeep+0"), 5.173312239796809e-06),
     (float.fromhex("0x1.0d1fd0p+0"), float.fromhex("0x1.00dfeep+0"), 5.108781622431647e-06),
 ]
+
+
+# ---- the 3xFP16 scheme ------------------------------------------------------
+# Its split error is largest just above the exception threshold: an element 2^-20 below its
+# row's maximum. With the maximum at 1.0 the row is scaled by 2^15 (max' = 2^15), so x' =
+# x 2^15; for x' just above 2^-5, hi = RN fp16(x') = 2^-5 and lo = RN fp16(x' - hi) lands on
+# fp16's subnormal grid (2^-24), where the fp32 grid of x' is 2^-28. x' = 2^-5 + 2^-25 puts
+# r = x' - hi exactly half-way between 0 and 2^-24: RN-even gives lo = 0, the split
+# undershoots by 2^-25 = (1 - 2^-20) 2^-20 |x'| -- the largest error an element can have
+# without being an exception (the GEMM carries it, not the fix kernels). Both operands at
+# this value: every product undershoots by ~2 * 2^-20 (1.9e-6), the same sign as the
+# truncating TMEM accumulation.
+FP16_ROW_MAX = 1.0
+FP16_WORST_X = float(np.float32((2.0 ** -5 + 2.0 ** -25) * 2.0 ** -15))
+
+
+def split16_rel_error(x, row_max=FP16_ROW_MAX):
+    """(x - rep(x)) / |x| of the 3xFP16 split for an element of a row whose maximum is
+    row_max (emulated: scale to [2^15, 65504), fp16 RN hi, fp16 RN lo)."""
+    mx = np.float64(row_max)
+    e = int(np.frexp(mx)[1] - 1) - 15
+    if mx * 2.0 ** -e >= 65504.0:
+        e += 1
+    xs = np.float32(np.float64(np.float32(x)) * 2.0 ** -e)
+    hi = np.float16(xs)
+    lo = np.float16(np.float32(xs - np.float32(hi)))
+    rep = (np.float64(hi) + np.float64(lo)) * 2.0 ** e
+    return (np.float64(np.float32(x)) - rep) / abs(np.float64(np.float32(x)))

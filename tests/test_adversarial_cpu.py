@@ -45,3 +45,16 @@ def test_split_error_within_analytic_bound():
     assert e.max() <= bound
     for a0, b0, _ in adv.WORST_PAIRS:
         assert abs(adv.split_rel_error(np.float32(a0), np.float32(b0))) <= bound
+
+
+def test_fp16_worst_element_is_just_under_the_exception_threshold():
+    """The constructed 3xFP16 worst case (tests/adversarial.py): undershoot 2^-25 / x',
+    below the 2^-20 exception threshold (so the GEMM carries it, not the fix kernels), and the
+    largest error any element of that binade reaches (fp32 grid 2^-28 there in scaled units,
+    lo's subnormal grid 2^-24: at most half a step)."""
+    e = adv.split16_rel_error(adv.FP16_WORST_X)
+    assert e == 2.0 ** -25 / (2.0 ** -5 + 2.0 ** -25)
+    assert 0 < e < 2.0 ** -20
+    xs = (2.0 ** -5 + np.arange(0, 1 << 12) * 2.0 ** -28) * 2.0 ** -15
+    errs = np.array([adv.split16_rel_error(v) for v in xs])
+    assert np.abs(errs).max() <= e

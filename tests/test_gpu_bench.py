@@ -1,6 +1,7 @@
 """bench.py's GPU arm prints one contract line (metric, value, roofline of the dominant kernel,
 cpu_baseline, e2e through the C ABI with host buffers, clocks, gpu_launches) for a 3xTF32
-workload and for a TF32 + BF16 one (whose roofline also carries the TMA-feed bound)."""
+workload, a 3xFP16 one (the product scheme at c3 and c5) and a forced TF32 + BF16 one (those
+two carry the TMA-feed bound too)."""
 import json
 import os
 import subprocess
@@ -12,9 +13,10 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _line(args):
+def _line(args, env=None):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args],
-                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+                         capture_output=True, text=True, timeout=900, cwd=ROOT,
+                         env=dict(os.environ, **(env or {})))
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1, out.stdout
@@ -44,13 +46,25 @@ def test_bench_line_3xtf32_workload():
     assert d["gpu_launches"] == 3  # one GEMM launch per step, no preparation
 
 
-def test_bench_line_tf32bf16_workload_with_cpu_baseline():
+def test_bench_line_3xfp16_workload_with_cpu_baseline():
     d = _line(["--config", "c3_16384", "--steps", "3", "--warmup", "3", "--e2e-steps", "1",
                "--cpu-budget", "2"])
+    _common(d, 3, 3)
+    r = d["roofline"]
+    assert r["scheme"] == "3xFP16" and r["dtype"] == "f16"
+    # per step: 3 + 1 operand-preparation kernels and 2 exception-fix kernels beside the GEMM
+    assert r["prep_launches_per_step"] == 6.0
+    assert r["feed"]["bound"] == "l2_to_smem_tma" and 0 < r["feed"]["frac"] < 1.2
+    assert d["gpu_launches"] == 21
+    c = d["cpu_baseline"]
+    assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0
+
+
+def test_bench_line_tf32bf16_forced():
+    d = _line(["--config", "c3_16384", "--steps", "3", "--warmup", "3", "--e2e-steps", "1",
+               "--no-cpu-baseline"], env={"GIGA_SCHEME": "tf32bf16"})
     _common(d, 3, 3)
     r = d["roofline"]
     assert r["scheme"] == "TF32+BF16" and r["prep_launches_per_step"] == 2.0
     assert r["feed"]["bound"] == "l2_to_smem_tma" and 0 < r["feed"]["frac"] < 1.2
     assert d["gpu_launches"] == 9  # per step: two preparation launches and the GEMM
-    c = d["cpu_baseline"]
-    assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0

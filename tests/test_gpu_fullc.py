@@ -5,12 +5,15 @@
   partial sums are integers below 2^53, so fp64 matrix-vector products are exact whatever
   their summation order; a single wrong element of C changes C r unless r's entry at its
   column is 0 (probability 1/2049 per vector; two vectors are used).
-* Constructed worst case of the product path's TF32 + BF16 scheme (tests/adversarial.py):
-  every row of A and column of B is constant at an (a, b) pair on which the split is least
-  accurate and undershoots (5.1-5.3e-6 of |a||b| per product), so every product's error has
-  the same sign as the truncating TMEM accumulation's. Expected value: the closed form
-  C_ij = K a_i b_j (exact in fp64), S_ij = the same. Asserted <= 1e-5 S; the margin is
-  printed and written to gpurun_out/adversarial.json.
+* Constructed worst cases (tests/adversarial.py), each scheme on the inputs where its split
+  is least accurate and undershoots, so every product's error has the same sign as the
+  truncating TMEM accumulation's: the product path's 3xFP16 (every row of A / column of B:
+  its maximum 1.0 meeting a zero of the other operand, every other element at 2^-20 of it
+  with a split error just under the exception threshold: ~2 * 2^-20 per product), and the
+  TF32 + BF16 and 3xTF32 building blocks (rows / columns constant at the (a, b) pairs of
+  largest TF32 + BF16 split error, 5.1-5.3e-6). Expected value: a closed form exact in fp64
+  (C_ij = K' a_i b_j, S_ij the same). Asserted <= 1e-5 S; the margins are printed and
+  written to gpurun_out/adversarial.json.
 """
 import json
 import os
@@ -72,7 +75,7 @@ def test_freivalds_whole_c_integer_inputs(torch_cuda, M, N, K):
             g.matmul_rank(A, B, C, M, N, K, stream=s)
         s.synchronize()
         assert not torch.isnan(C).any().item()
-        assert g.product_scheme(M, N, K) == 2  # the TF32 + BF16 product path at both sizes
+        assert g.product_scheme(M, N, K) == 4  # the 3xFP16 product path at both sizes
         worst = _freivalds(torch, A, B, C)
         assert worst == 0.0, worst
         # the check itself: one wrong element anywhere must be caught
@@ -86,11 +89,35 @@ _ADV_SHAPES = {2048: (8192, 8192, 2048), 8192: (4096, 8192, 8192), 32768: (4096,
 
 
 @pytest.mark.parametrize("K", sorted(_ADV_SHAPES))
-def test_constructed_worst_case_product_path(torch_cuda, K):
+def test_constructed_worst_cases(torch_cuda, K):
     torch = torch_cuda
     from paper_2504_01266_b200 import giga as g
     M, N, _ = _ADV_SHAPES[K]
-    assert g.product_scheme(M, N, K) == 2
+    assert g.product_scheme(M, N, K) == 4
+    out = {}
+    # the 3xFP16 product path: A rows [1, 0, x, x, ...], B columns [0, 1, x, x, ...]^T
+    x = adv.FP16_WORST_X
+    A = torch.full((M, K), x, dtype=torch.float32, device="cuda")
+    A[:, 0] = adv.FP16_ROW_MAX
+    A[:, 1] = 0.0
+    B = torch.full((K, N), x, dtype=torch.float32, device="cuda")
+    B[0, :] = 0.0
+    B[1, :] = adv.FP16_ROW_MAX
+    exact = (K - 2) * float(np.float64(x) * np.float64(x))
+    g.finalize()
+    g.init(1)
+    try:
+        C = torch.full((M, N), float("nan"), device="cuda")
+        g.matmul_sharded([A], [B], [C], M, N, K)
+        torch.cuda.synchronize()
+        rel = (C.double() - exact) / exact
+        out["product_3xfp16"] = {"max_rel": float(rel.abs().max()),
+                                 "mean_signed_rel": float(rel.mean()),
+                                 "margin_to_1e-5": 1e-5 - float(rel.abs().max()),
+                                 "split_error_emulated": 2 * adv.split16_rel_error(x)}
+        del A, B, C, rel
+    finally:
+        g.finalize()
     pairs = adv.WORST_PAIRS
     avals = torch.tensor([p[0] for p in pairs], dtype=torch.float32, device="cuda")
     b = float(np.float32(pairs[0][1]))
@@ -98,16 +125,12 @@ def test_constructed_worst_case_product_path(torch_cuda, K):
     A = avals[torch.arange(M, device="cuda") % len(pairs)].unsqueeze(1).expand(M, K).contiguous()
     B = torch.full((K, N), b, dtype=torch.float32, device="cuda")
     exact = (K * b) * A[:, :1].double()  # C_ij = K a_i b, exact in fp64; S_ij equal (all > 0)
-    out = {}
     g.finalize()
     g.init(1)
     try:
-        for label in ("product", "3xtf32"):
+        for label, terms in (("tf32bf16", 2), ("3xtf32", 3)):
             C = torch.full((M, N), float("nan"), device="cuda")
-            if label == "product":
-                g.matmul_sharded([A], [B], [C], M, N, K)
-            else:
-                g.gemm_3xtf32(A, None, B, None, C, M, N, K, terms=3)
+            g.gemm_3xtf32(A, None, B, None, C, M, N, K, terms=terms)
             torch.cuda.synchronize()
             rel = ((C.double() - exact) / exact)
             out[label] = {"max_rel": float(rel.abs().max()), "mean_signed_rel": float(rel.mean()),
@@ -123,5 +146,6 @@ def test_constructed_worst_case_product_path(torch_cuda, K):
     with open(path, "w") as f:
         json.dump(allres, f, indent=1)
     print(f"adversarial {M}x{N}x{K}: {out}")
-    assert out["product"]["max_rel"] <= 1e-5, out
+    assert out["product_3xfp16"]["max_rel"] <= 1e-5, out
+    assert out["tf32bf16"]["max_rel"] <= 1e-5, out
     assert out["3xtf32"]["max_rel"] <= 1e-5, out
