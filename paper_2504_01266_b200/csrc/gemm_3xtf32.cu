@@ -146,6 +146,7 @@ struct GemmParams {
   // (k, column in the strip, b - rep(b) as fp64 halves) in column-then-k order (compact16_b)
   const int *bcnt;
   const int4 *blist;
+  uint64_t *cta_ns;  // $GIGA_TRACE: [2 blockIdx.x] = this CTA's start, [+1] = its end (ns)
 };
 
 // C tensor maps: [0] this GPU's C, [1..] the same rows of the peers' C_full buffers.
@@ -490,6 +491,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (p.cta_ns && threadIdx.x == 0) p.cta_ns[2 * blockIdx.x] = ptx::globaltimer_ns();
   const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0;  // rank in the CTA pair
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x / CG;
@@ -1048,6 +1050,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
     else
       ptx::tmem_dealloc(tmem_base, TMEM_COLS);
   }
+  if (p.cta_ns && threadIdx.x == 0) p.cta_ns[2 * blockIdx.x + 1] = ptx::globaltimer_ns();
   if (threadIdx.x == 0 && p.sched) {
     // thread 0 made every claim and issued-count of this CTA; the last CTA of the grid to
     // finish returns the counters to zero for the next launch on this stream
@@ -1240,6 +1243,7 @@ __global__ void __launch_bounds__(512) prep16_a_kernel(const float *__restrict__
     const float *row = A + int64_t(live ? m : 0) * lda;
     uint32_t mx = 0;
     if (live) {
+#pragma unroll 4
       for (int i = t; i < k4; i += TPR) {
         const float4 v = __ldg(reinterpret_cast<const float4 *>(row) + i);
         mx = max(mx, max(max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu),
@@ -1265,6 +1269,7 @@ __global__ void __launch_bounds__(512) prep16_a_kernel(const float *__restrict__
     if (t == 0) ea[m] = e;
     if (!live) continue;
     uint16_t *hd = Ah + int64_t(m) * ldh, *ld = Al + int64_t(m) * ldh;
+#pragma unroll 4
     for (int i = t; i < k4; i += TPR) {
       const float4 v = __ldg(reinterpret_cast<const float4 *>(row) + i);
       uint16_t h[4], l[4];
@@ -1308,6 +1313,7 @@ __global__ void __launch_bounds__(256) prep16_bmax_kernel(const float *__restric
   const int r1 = min(K, r0 + rows);
   uint4 mx = make_uint4(0, 0, 0, 0);
   if (n < N) {
+#pragma unroll 4
     for (int r = r0 + rl; r < r1; r += 8) {
       const float *src = B + int64_t(r) * ldb + n;
       float4 v;
@@ -1401,7 +1407,7 @@ __global__ void prep16_bexp_kernel(const unsigned *__restrict__ bmax, int n_pad,
 }
 
 // B pass 3: B_hi / B_lo (fp16, K x N row-major, row stride ldh). Thread = 4 columns x 8 rows.
-__global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__ B, int64_t ldb,
+__global__ void __launch_bounds__(256, 2) prep16_b_kernel(const float *__restrict__ B, int64_t ldb,
                                                        int K, int N, const int *__restrict__ eb,
                                                        uint16_t *__restrict__ Bh,
                                                        uint16_t *__restrict__ Bl, int64_t ldh,
@@ -1414,11 +1420,22 @@ __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__
        i += int64_t(gridDim.x) * blockDim.x) {
     const int kb = int(i / n4), n = int(i - int64_t(kb) * n4) * 4;
     const int4 e = *reinterpret_cast<const int4 *>(eb + n);  // eb is padded to 256 columns
-    for (int k = kb * 8; k < min(K, kb * 8 + 8); ++k) {
+    // the 8 rows' loads first (independent: 8 x 16 B in flight per thread)
+    float4 pre[8];
+    const bool full8 = n + 3 < N && kb * 8 + 8 <= K;
+    if (full8) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        pre[r] = __ldcs(reinterpret_cast<const float4 *>(B + int64_t(kb * 8 + r) * ldb + n));
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int k = kb * 8 + r;
+      if (k >= K) break;
       const float *src = B + int64_t(k) * ldb + n;
       uint16_t h[4], l[4];
       if (n + 3 < N) {
-        const float4 v = __ldcs(reinterpret_cast<const float4 *>(src));
+        const float4 v = full8 ? pre[r] : __ldcs(reinterpret_cast<const float4 *>(src));
         const bool x0 = split_f16(v.x, e.x, h[0], l[0]);
         const bool x1 = split_f16(v.y, e.y, h[1], l[1]);
         const bool x2 = split_f16(v.z, e.z, h[2], l[2]);
@@ -1595,6 +1612,13 @@ __global__ void __launch_bounds__(256) fix16_a_kernel(
       }
     }
   }
+}
+
+__global__ void stamp_kernel(uint64_t *slot) { *slot = ptx::globaltimer_ns(); }
+
+cudaError_t launch_stamp(uint64_t *slot, cudaStream_t st) {
+  stamp_kernel<<<1, 1, 0, st>>>(slot);
+  return cudaGetLastError();
 }
 
 // ---- host side ----------------------------------------------------------------------------
@@ -2289,6 +2313,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.w2b = 0;
   p.bcnt = nullptr;
   p.blist = nullptr;
+  p.cta_ns = ex->cta_ns;
   // k-block width in elements of K: 16 (tf32 schemes), 32 (3xFP16)
   const int bk = terms == 4 ? 32 : BK;
   TermsPrep local4;

@@ -19,6 +19,8 @@
 #include "host_plan.h"
 
 #include <math.h>
+
+#include "kernels.h"
 #include <stdlib.h>
 
 #include <algorithm>
@@ -29,13 +31,23 @@ namespace {
 
 // One launch: waves of 256 x 256 tiles, each wave ~2 us of pipeline fill / epilogue beyond its
 // MMAs (measured: a 576-deep 20480 x 32768 chunk runs at 241 TF/s against 248 for 32768^3),
-// accumulate-mode launches (TMA reduce-add of C) ~10% slower (measured in the e2e timeline).
-double gemm_time(int64_t m, int64_t n, int64_t k, const HostRates &r, bool accumulate) {
+// accumulate-mode launches (TMA reduce-add of C) ~10% slower (measured in the e2e timeline),
+// at the rate of the scheme the launch runs (chosen on scheme_rows rows, the rows sharing B's
+// preparation), plus the operand preparation of the TF32 + BF16 / 3xFP16 schemes (~12 B per
+// element of A, and of B unless b_prepared).
+double gemm_time(int64_t m, int64_t n, int64_t k, const HostRates &r, bool accumulate,
+                 int64_t scheme_rows, bool b_prepared) {
   if (m <= 0 || n <= 0 || k <= 0) return 0.0;
+  const int terms = product_terms(nullptr, std::max(m, scheme_rows), n, k);
+  const double rate = terms == 4 ? r.gemm4 : terms == 2 ? r.gemm2 : r.gemm;
   const int64_t tiles = ((m + 255) / 256) * ((n + 255) / 256);
   const int64_t waves = (tiles + r.clusters - 1) / r.clusters;
-  const double t_wave = 2e-6 + 2.0 * 256.0 * 256.0 * double(k) / (r.gemm / r.clusters);
-  return 10e-6 + double(waves) * t_wave * (accumulate ? 1.1 : 1.0);  // + launch
+  const double t_wave = 2e-6 + 2.0 * 256.0 * 256.0 * double(k) / (rate / r.clusters);
+  const double prep = (terms == 4 || terms == 2)
+                          ? 12.0 * (double(m) * double(k) + (b_prepared ? 0.0 : double(k) * double(n))) /
+                                r.prep
+                          : 0.0;
+  return 10e-6 + prep + double(waves) * t_wave * (accumulate ? 1.1 : 1.0);  // + launch
 }
 
 // bounds[0..n]: start .. start + total split into n pieces with weights ratio^i, interior
@@ -70,6 +82,7 @@ HostRates host_rates_default() {
   r.h2d = env_double("GIGA_HOST_H2D_GBS", r.h2d / 1e9) * 1e9;
   r.d2h = env_double("GIGA_HOST_D2H_GBS", r.d2h / 1e9) * 1e9;
   r.gemm = env_double("GIGA_HOST_GEMM_TFLOPS", r.gemm / 1e12) * 1e12;
+  r.gemm4 = env_double("GIGA_HOST_GEMM4_TFLOPS", r.gemm4 / 1e12) * 1e12;
   return r;
 }
 
@@ -88,14 +101,17 @@ double host_plan_model(const HostPlan &p, int64_t /*M: rows are in p.rb*/, int64
   }
   if (p.Me > 0) {
     for (int c = 0; c < p.P; ++c)
-      tc = std::max(tc, arrive_k[c]) + gemm_time(p.Me, N, p.kb[c + 1] - p.kb[c], r, c > 0);
+      tc = std::max(tc, arrive_k[c]) +
+           gemm_time(p.Me, N, p.kb[c + 1] - p.kb[c], r, c > 0, 0, false);
     td = tc + 4.0 * double(p.Me * N) / r.d2h;
   }
   const double b_all = arrive_k[p.P - 1];
+  const int64_t late = p.Q > 0 ? p.rb[p.Q] - p.rb[0] : 0;
   for (int q = 0; q < p.Q; ++q) {
     const int64_t rows = p.rb[q + 1] - p.rb[q];
     if (rows <= 0) continue;
-    tc = std::max({tc, arrive_r[q], b_all}) + gemm_time(rows, N, K, r, false);
+    // the late row blocks share B's preparation (GemmExtra::b_prep_reuse, rows_hint)
+    tc = std::max({tc, arrive_r[q], b_all}) + gemm_time(rows, N, K, r, false, late, q > 0);
     td = std::max(td, tc) + 4.0 * double(rows * N) / r.d2h;
   }
   return std::max(tc, td);

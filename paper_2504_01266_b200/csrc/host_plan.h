@@ -19,7 +19,10 @@ struct HostPlan {
 struct HostRates {
   double h2d = 50e9;     // bytes/s host -> device (pinned, measured 55.6 alone, 49 in duplex)
   double d2h = 50e9;     // bytes/s device -> host
-  double gemm = 255e12;  // logical fp32-accurate flop/s of the shard GEMM (measured 255-265)
+  // logical fp32-accurate flop/s of the shard GEMM by the scheme a launch runs
+  // (giga_product_scheme; measured): 3xTF32, TF32 + BF16, 3xFP16
+  double gemm = 250e12, gemm2 = 265e12, gemm4 = 400e12;
+  double prep = 5e12;    // bytes/s of the operand preparation (~12 B per element, HBM-bound)
   int clusters = 74;     // concurrent 256 x 256 tiles (CTA pairs on 148 SMs)
 };
 

@@ -117,7 +117,11 @@ struct GemmExtra {
   // terms = 4: 1 = the caller launches the exception fixes itself (launch_fix16, after the GEMM
   // on the same stream; run_gemm does, to time them apart from the GEMM)
   int defer_fix = 0;
+  // $GIGA_TRACE: 2 x (grid size) slots; each CTA writes %globaltimer at its start and its end
+  uint64_t *cta_ns = nullptr;
 };
+// One thread writes %globaltimer (ns) to *slot when `st` reaches it (trace stamps).
+cudaError_t launch_stamp(uint64_t *slot, cudaStream_t st);
 // The 3xFP16 A-side exception fix of a launch whose GEMM ran with defer_fix (same arguments;
 // the B-side fix runs inside the GEMM's epilogue).
 cudaError_t launch_fix16(const float *A, int64_t lda, const float *B, int64_t ldb, int64_t M,

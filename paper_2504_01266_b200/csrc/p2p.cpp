@@ -59,9 +59,19 @@ int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K, bool gath
   if (!aligned)
     return fail(GIGA_ERR_UNSUPPORTED, "p2p transport needs K %% 4 == N %% 4 == 0, aligned");
   const Plan plan = make_plan(M, N, K, world, true);
+  // $GIGA_TRACE=1: per-GPU timeline; %globaltimer stamps around every chain copy and the CTA
+  // intervals of every GEMM launch show the copy engines working under the GEMMs
+  std::vector<Trace> tr;
+  for (auto &p : parts) {
+    tr.emplace_back(*p.d, "p2p");
+    tr.back().meta("rank", p.rank);
+    tr.back().meta("world", world);
+    tr.back().meta("kchunks", plan.pb);
+  }
   // 0. join the callers' streams, workspace, split A
   for (auto &p : parts) {
     CK(cudaSetDevice(p.d->dev));
+    TRY(tr[&p - &parts[0]].start(p.st));
     CK(cudaEventRecord(p.d->ev_start, p.st));
     CK(cudaStreamWaitEvent(p.d->comm, p.d->ev_start, 0));
     int64_t r0, rows;
@@ -79,10 +89,13 @@ int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K, bool gath
       if (i > 0) {
         Part &up = parts[i - 1];
         CK(cudaStreamWaitEvent(p.d->comm, up.d->ev_kchunk[c], 0));
+        TRY(tr[i].stamp("copy_begin", p.d->comm));
         CK(cudaMemcpyPeerAsync(p.B + off, p.d->dev, up.B + off, up.d->dev, size_t(cnt) * 4,
                                p.d->comm));
+        TRY(tr[i].stamp("copy_end", p.d->comm));
       }
       CK(cudaEventRecord(p.d->ev_kchunk[c], p.d->comm));
+      TRY(tr[i].mark("bcast", p.d->comm, i > 0 ? 4.0 * double(cnt) : 0.0));
     }
   }
   // 2. GEMMs over the K-chunks; every tile also goes to the peers' C_full
@@ -106,19 +119,25 @@ int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K, bool gath
       CK(cudaStreamWaitEvent(p.st, p.d->ev_kchunk[c], 0));
       TRY(split(p.B + plan.kb[c] * N, lo_at(p.d->B_lo, plan.kb[c] * N), Kc * N, p.st));
       if (rows == 0) continue;
+      GemmExtra ec = chunk_extra(ex, c, plan.pb);
+      ec.cta_ns = tr[&p - &parts[0]].cta_slots("gemm_cta", p.st);
       TRY(gemm_chunk(p.A + plan.kb[c], lo_at(p.d->A_lo, plan.kb[c]), p.B + plan.kb[c] * N,
-                     lo_at(p.d->B_lo, plan.kb[c] * N), Cr, rows, N, Kc,
-                     chunk_extra(ex, c, plan.pb), p.st));
+                     lo_at(p.d->B_lo, plan.kb[c] * N), Cr, rows, N, Kc, ec, p.st));
+      TRY(tr[&p - &parts[0]].mark("gemm", p.st));
     }
     CK(cudaEventRecord(p.d->ev_c, p.st));
   }
-  if (!gather) return GIGA_OK;  // every rank only needs its own rows
+  if (!gather) {  // every rank only needs its own rows
+    for (auto &t : tr) TRY(t.finish());
+    return GIGA_OK;
+  }
   // 3. a GPU's C_full is complete when every GPU's GEMMs are
   for (auto &p : parts) {
     CK(cudaSetDevice(p.d->dev));
     for (auto &q : parts)
       if (&q != &p) CK(cudaStreamWaitEvent(p.st, q.d->ev_c, 0));
   }
+  for (auto &t : tr) TRY(t.finish());
   return GIGA_OK;
 }
 

@@ -126,6 +126,7 @@ void ctx_destroy(DevCtx &d) {
   for (cudaEvent_t e : {d.ev_b, d.ev_c, d.ev_start, d.ev_last})
     if (e) cudaEventDestroy(e);
   if (d.res_pinned) cudaFreeHost(d.res_pinned);
+  if (d.trace_ns) cudaFree(d.trace_ns);
   for (auto *v : {&d.ev_kchunk, &d.ev_rchunk, &d.ev_done, &d.ev_trace})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
@@ -508,6 +509,46 @@ int Trace::mark(const char *series, cudaStream_t st, double bytes) {
   return GIGA_OK;
 }
 
+// %globaltimer slots: the device's buffer (allocated on first use, zeroed per Trace), handed
+// out in order; a trace that runs out of slots reports what it has.
+static uint64_t *ns_take(DevCtx &d, size_t &used, size_t n) {
+  if (!d.trace_ns) {
+    cudaSetDevice(d.dev);
+    if (cudaMalloc(&d.trace_ns, kTraceNsSlots * sizeof(uint64_t)) != cudaSuccess) {
+      cudaGetLastError();
+      d.trace_ns = nullptr;
+      return nullptr;
+    }
+  }
+  if (used + n > kTraceNsSlots) return nullptr;
+  uint64_t *p = d.trace_ns + used;
+  used += n;
+  return p;
+}
+
+int Trace::stamp(const char *series, cudaStream_t st) {
+  if (!on_) return GIGA_OK;
+  const size_t at = ns_used_;
+  uint64_t *slot = ns_take(d_, ns_used_, 1);
+  if (!slot) return GIGA_OK;
+  CK(launch_stamp(slot, st));
+  ns_.push_back({series, at});
+  return GIGA_OK;
+}
+
+uint64_t *Trace::cta_slots(const char *series, cudaStream_t st) {
+  if (!on_) return nullptr;
+  const size_t at = ns_used_;
+  uint64_t *p = ns_take(d_, ns_used_, 2 * size_t(kTraceMaxCtas));
+  if (!p) return nullptr;
+  if (cudaMemsetAsync(p, 0, 2 * size_t(kTraceMaxCtas) * sizeof(uint64_t), st) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  cta_.push_back({series, at});
+  return p;
+}
+
 void Trace::meta(const char *key, double v) {
   if (!on_) return;
   char buf[96];
@@ -548,6 +589,40 @@ int Trace::finish() {
     out += ", \"GBps\": {";
     first = true;
     for (auto &kv : rates) {
+      out += (first ? "\"" : ", \"") + kv.first + "\": [" + kv.second + "]";
+      first = false;
+    }
+    out += "}";
+  }
+  if (!ns_.empty() || !cta_.empty()) {
+    // %globaltimer values (ns, the device's clock): stamps and per-launch CTA intervals
+    std::vector<uint64_t> h(ns_used_);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(h.data(), d_.trace_ns, ns_used_ * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    std::map<std::string, std::string> ns;
+    char buf[64];
+    for (auto &s : ns_) {
+      std::string &v = ns[s.first];
+      snprintf(buf, sizeof buf, "%s%llu", v.empty() ? "" : ", ",
+               (unsigned long long)h[s.second]);
+      v += buf;
+    }
+    for (auto &c : cta_) {
+      uint64_t lo = ~0ull, hi = 0;
+      for (int b = 0; b < kTraceMaxCtas; ++b) {
+        const uint64_t s0 = h[c.second + 2 * b], s1 = h[c.second + 2 * b + 1];
+        if (s0 == 0 || s1 == 0) continue;  // no such CTA in the grid
+        lo = std::min(lo, s0);
+        hi = std::max(hi, s1);
+      }
+      std::string &v = ns[c.first];
+      snprintf(buf, sizeof buf, "%s[%llu, %llu]", v.empty() ? "" : ", ", (unsigned long long)lo,
+               (unsigned long long)hi);
+      v += buf;
+    }
+    out += ", \"ns\": {";
+    first = true;
+    for (auto &kv : ns) {
       out += (first ? "\"" : ", \"") + kv.first + "\": [" + kv.second + "]";
       first = false;
     }

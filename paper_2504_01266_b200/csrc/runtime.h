@@ -49,6 +49,9 @@ struct Buf {
 
 constexpr int kMaxChunks = 16;  // pipeline chunks per phase (B K-chunks, C row-chunks)
 
+constexpr size_t kTraceNsSlots = 1 << 15;  // per device: %globaltimer slots of class Trace
+constexpr int kTraceMaxCtas = 160;          // >= the SM count: CTA slots per traced launch
+
 struct DevCtx {
   int dev = -1;
   cudaStream_t compute = nullptr;  // splits + GEMM (+ H2D/D2H in host mode)
@@ -63,6 +66,7 @@ struct DevCtx {
   std::vector<cudaEvent_t> ev_rchunk;  // pipeline: C row-chunk q computed
   std::vector<cudaEvent_t> ev_done;    // host pipeline: late row block q computed
   std::vector<cudaEvent_t> ev_trace;   // timing events of class Trace ($GIGA_TRACE)
+  uint64_t *trace_ns = nullptr;        // Trace's %globaltimer slots (device; kTraceNsSlots)
   Buf A_lo, B_lo, A_pad, B_pad, C_pad, A_h, B_h, C_h;
   Buf vec_ws;  // dot: kDotMaxBlocks fp64 partials, the fp64 result, the ticket (zeroed once)
   double *res_pinned = nullptr;  // dot: pinned host landing slot of the fp64 result
@@ -191,6 +195,12 @@ class Trace {
   // bytes > 0: the bytes the stream moved since its previous mark of this series (or since
   // start); finish() then also reports the achieved GB/s of each such interval
   int mark(const char *series, cudaStream_t st, double bytes = 0);
+  // %globaltimer intervals on the device clock (comparable across streams): stamp() writes
+  // the time the stream reaches it (a 1-thread kernel) into the series; cta_slots() returns
+  // room for one GEMM launch's per-CTA (start, end) pairs (GemmExtra::cta_ns), reported as
+  // that launch's [first CTA start, last CTA end]. nullptr when tracing is off or full.
+  int stamp(const char *series, cudaStream_t st);
+  uint64_t *cta_slots(const char *series, cudaStream_t st);
   void meta(const char *key, double v);
   int finish();                                // waits for the last marks, prints the line
 
@@ -201,6 +211,9 @@ class Trace {
   size_t n_ = 0;
   std::vector<std::pair<std::string, size_t>> marks_;
   std::vector<double> bytes_;
+  std::vector<std::pair<std::string, size_t>> ns_;   // (series, first slot), 1 slot each
+  std::vector<std::pair<std::string, size_t>> cta_;  // (series, first slot), 2 x kMaxCtas
+  size_t ns_used_ = 0;
   std::string meta_;
 };
 
