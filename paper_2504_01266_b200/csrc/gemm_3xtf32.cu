@@ -1659,12 +1659,14 @@ int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K) {
   if (forced) return forced;
   const double mnk = double(M) * double(N) * double(K);
   // measured crossover, operand preparation and exception fixes included
-  // (profiles/r02_scheme_crossover*.jsonl, scripts/scheme_crossover.py): 3xFP16 wins from
-  // 8192 x 8192 x 2048 (+10%) and 2048 x 16384^2 (+5%) up to +52-58% at 16384^3 and
-  // 32768^3, and on 16384 x 32768 x 1024 (+8%); it loses where the preparation (~12 B per
-  // element of A and B) is not amortised: 4096^3 (-9%), 2048 x 4096^2, 32768 x 1024^2, and
+  // (profiles/r02_scheme_crossover*.jsonl, scripts/scheme_crossover.py, bench.py): 3xFP16 wins
+  // from 8192 x 8192 x 2048 (+10%), 2048 x 16384^2 (+5%) and 65536 x 2048^2 (+21%) up to
+  // +52-58% at 16384^3 and 32768^3, and on 16384 x 32768 x 1024 (+8%); it loses where the
+  // preparation (~12 B per element of A and B) is not amortised or the tiles are short:
+  // 4096^3 (-9%), 2048 x 4096^2, the tall 262144 x 1024^2 (-13%: 227 vs 262 in bench.py),
   // K = 576 (-19%)
-  if (M >= 2048 && N >= 1024 && K >= 1024 && mnk >= 0x1p37) return 4;
+  if (M >= 2048 && mnk >= 0x1p37 && ((K >= 2048 && N >= 2048) || (K >= 1024 && N >= 8192)))
+    return 4;
   // below that, TF32 + BF16 only ties 3xTF32 (16384 x 32768 x 576: 219 vs 217; r01: it won
   // 3-10% on 16384 x 32768 x (576..1792), the host schedule's K-chunks, before 3xFP16)
   return (M >= 4096 && N >= 8192 && K >= 512 && mnk >= 0x1p38) ? 2 : 3;

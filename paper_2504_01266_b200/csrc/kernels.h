@@ -23,7 +23,8 @@ int default_promote_kblocks(int terms = 3);
 // The product path's fp32-accurate scheme for an M x N x K launch:
 // 4 = 3xFP16 (the 3xTF32 split on fp16 operands of power-of-two scaled rows / columns, three
 // K=16 kind::f16 MMAs per k16 step, operands prepared once per launch in HBM, exceptions fixed)
-// where the preparation is amortised: M >= 2048, N >= 1024, K >= 1024, M N K >= 2^37;
+// where the preparation is amortised: M >= 2048, M N K >= 2^37 and either K, N >= 2048 or
+// K >= 1024 with N >= 8192;
 // else 2 = TF32 + BF16 (hi*hi as kind::tf32, both corrections as one K=16 kind::f16 MMA) for
 // M >= 4096, N >= 8192, K >= 512, M N K >= 2^38; else 3 = 3xTF32 (three kind::tf32 MMAs per
 // k8 step, no preparation). Measured crossovers. $GIGA_SCHEME = "3xtf32" / "tf32bf16" /

@@ -90,11 +90,11 @@ def test_product_scheme_selection():
     from paper_2504_01266_b200 import giga
     for shape in [(16384, 16384, 16384), (32768, 32768, 32768), (4096, 32768, 32768),
                   (8192, 8192, 2048), (2048, 16384, 16384), (16384, 32768, 1024),
-                  (262144, 1024, 1024), (8192, 16384, 1024)]:
+                  (65536, 2048, 2048), (8192, 16384, 1024)]:
         assert giga.product_scheme(*shape) == 4, shape
     for shape in [(16384, 32768, 576), (32768, 16384, 1000)]:
         assert giga.product_scheme(*shape) == 2, shape
-    for shape in [(512, 512, 512), (4096, 4096, 4096), (32768, 1024, 1024),
+    for shape in [(512, 512, 512), (4096, 4096, 4096), (32768, 1024, 1024), (262144, 1024, 1024),
                   (2048, 4096, 4096), (16384, 16384, 256), (65536, 4096, 512),
                   (1024, 32768, 32768), (4096, 32768, 768)]:
         assert giga.product_scheme(*shape) == 3, shape
