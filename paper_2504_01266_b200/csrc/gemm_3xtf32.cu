@@ -1300,53 +1300,45 @@ __global__ void __launch_bounds__(512) prep16_a_kernel(const float *__restrict__
   }
 }
 
-// B pass 1: per-column max |b| bits into bmax (zeroed before): a block covers 128 columns
-// (32 threads x 4) and `rows` rows (8 row lanes), reduces in shared memory, one atomicMax
-// per column per block. rows is chosen so the grid is ~8 blocks per SM.
+// B pass 1: per-column max |b| bits into bmax (zeroed before): a block covers 1024 columns
+// (256 threads x 4: every row it reads is one 4 KiB contiguous stretch) and `rows` rows (8 in
+// flight per thread), one atomicMax per column per block. rows is chosen so the grid is ~8
+// blocks per SM.
 __global__ void __launch_bounds__(256) prep16_bmax_kernel(const float *__restrict__ B, int64_t ldb,
                                                           int K, int N, int rows,
                                                           unsigned *__restrict__ bmax) {
-  __shared__ uint4 red[8][32];
-  const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;
-  const int n = (blockIdx.x * 32 + cg) * 4;
+  const int n = (blockIdx.x * 256 + int(threadIdx.x)) * 4;
+  if (n >= N) return;
   const int r0 = blockIdx.y * rows;
   const int r1 = min(K, r0 + rows);
   uint4 mx = make_uint4(0, 0, 0, 0);
-  if (n < N) {
-#pragma unroll 4
-    for (int r = r0 + rl; r < r1; r += 8) {
-      const float *src = B + int64_t(r) * ldb + n;
-      float4 v;
-      if (n + 3 < N) {
-        v = __ldg(reinterpret_cast<const float4 *>(src));
-      } else {
-        v.x = src[0];
-        v.y = n + 1 < N ? src[1] : 0.f;
-        v.z = n + 2 < N ? src[2] : 0.f;
-        v.w = 0.f;
-      }
-      mx.x = max(mx.x, __float_as_uint(v.x) & 0x7fffffffu);
-      mx.y = max(mx.y, __float_as_uint(v.y) & 0x7fffffffu);
-      mx.z = max(mx.z, __float_as_uint(v.z) & 0x7fffffffu);
-      mx.w = max(mx.w, __float_as_uint(v.w) & 0x7fffffffu);
-    }
-  }
-  red[rl][cg] = mx;
-  __syncthreads();
-  if (rl == 0 && n < N) {
+  auto take = [&](float4 v) {
+    mx.x = max(mx.x, __float_as_uint(v.x) & 0x7fffffffu);
+    mx.y = max(mx.y, __float_as_uint(v.y) & 0x7fffffffu);
+    mx.z = max(mx.z, __float_as_uint(v.z) & 0x7fffffffu);
+    mx.w = max(mx.w, __float_as_uint(v.w) & 0x7fffffffu);
+  };
+  if (n + 3 < N) {
+    int r = r0;
+    for (; r + 8 <= r1; r += 8) {
+      float4 v[8];
 #pragma unroll
-    for (int q = 1; q < 8; ++q) {
-      const uint4 o = red[q][cg];
-      mx.x = max(mx.x, o.x);
-      mx.y = max(mx.y, o.y);
-      mx.z = max(mx.z, o.z);
-      mx.w = max(mx.w, o.w);
+      for (int u = 0; u < 8; ++u)
+        v[u] = __ldg(reinterpret_cast<const float4 *>(B + int64_t(r + u) * ldb + n));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) take(v[u]);
     }
-    atomicMax(bmax + n, mx.x);
-    if (n + 1 < N) atomicMax(bmax + n + 1, mx.y);
-    if (n + 2 < N) atomicMax(bmax + n + 2, mx.z);
-    if (n + 3 < N) atomicMax(bmax + n + 3, mx.w);
+    for (; r < r1; ++r) take(__ldg(reinterpret_cast<const float4 *>(B + int64_t(r) * ldb + n)));
+  } else {
+    for (int r = r0; r < r1; ++r) {
+      const float *src = B + int64_t(r) * ldb + n;
+      take(make_float4(src[0], n + 1 < N ? src[1] : 0.f, n + 2 < N ? src[2] : 0.f, 0.f));
+    }
   }
+  atomicMax(bmax + n, mx.x);
+  if (n + 1 < N) atomicMax(bmax + n + 1, mx.y);
+  if (n + 2 < N) atomicMax(bmax + n + 2, mx.z);
+  if (n + 3 < N) atomicMax(bmax + n + 3, mx.w);
 }
 
 // B pass 4 (after the writes): the exception list of every strip of 32 columns, one warp per
@@ -2152,7 +2144,7 @@ cudaError_t launch_prep16_b(const float *B, int64_t ldb, int64_t N, int64_t K, T
                         size_t(K) * tp->wb * 4 + size_t(tp->wb) * tp->w2b * 4 + size_t(n_pad) * 4,
                         st);
   if (e != cudaSuccess) return e;
-  const int64_t bx = (N + 127) / 128;
+  const int64_t bx = (N + 1023) / 1024;
   const int64_t by = std::max<int64_t>(1, std::min<int64_t>((K + 7) / 8,
                                                             int64_t(num_sms_current()) * 8 / bx));
   const int64_t rows = ((K + by - 1) / by + 7) / 8 * 8;

@@ -39,7 +39,11 @@ double gemm_time(int64_t m, int64_t n, int64_t k, const HostRates &r, bool accum
                  int64_t scheme_rows, bool b_prepared) {
   if (m <= 0 || n <= 0 || k <= 0) return 0.0;
   const int terms = product_terms(nullptr, std::max(m, scheme_rows), n, k);
-  const double rate = terms == 4 ? r.gemm4 : terms == 2 ? r.gemm2 : r.gemm;
+  // 3xFP16's short-K launches run below its full rate (shorter tiles, per-tile epilogue and
+  // preparation weigh more): measured ~310-340 TFLOP/s at K = 2048, ~250 at K = 1024
+  const double rate = terms == 4 ? r.gemm4 * double(k) / double(k + 512)
+                      : terms == 2 ? r.gemm2
+                                   : r.gemm;
   const int64_t tiles = ((m + 255) / 256) * ((n + 255) / 256);
   const int64_t waves = (tiles + r.clusters - 1) / r.clusters;
   const double t_wave = 2e-6 + 2.0 * 256.0 * 256.0 * double(k) / (rate / r.clusters);

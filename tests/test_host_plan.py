@@ -27,7 +27,8 @@ def gemm_t(m, n, k, accumulate=False, scheme_rows=0, b_prepared=False):
         return 0.0
     terms = giga.product_scheme(max(m, scheme_rows), n, k)
     tiles = math.ceil(m / 256) * math.ceil(n / 256)
-    wave = 2e-6 + 2 * 256 * 256 * k / (RATE[terms] / CLUSTERS)
+    rate = RATE[terms] * (k / (k + 512) if terms == 4 else 1.0)  # 3xFP16's short-K rate
+    wave = 2e-6 + 2 * 256 * 256 * k / (rate / CLUSTERS)
     prep = 12.0 * (m * k + (0 if b_prepared else k * n)) / PREP if terms in (2, 4) else 0.0
     return 10e-6 + prep + math.ceil(tiles / CLUSTERS) * wave * (1.1 if accumulate else 1.0)
 
