@@ -117,22 +117,38 @@ int main() {
   mp.size = size;
   printf("{\"mc_granularity\": %zu, \"size\": %zu}\n", gran, size);
   CUmemGenericAllocationHandle mch, memh;
+  // creation alone with a team of 2 (never bound: binding would wait for a second device):
+  // tells whether a one-device team or multicast as such is what the driver refuses
+  for (unsigned nd = 2; nd <= 2; ++nd) {
+    CUmulticastObjectProp m2 = mp;
+    m2.numDevices = nd;
+    const CUmemAllocationHandleType hts2[3] = {CU_MEM_HANDLE_TYPE_NONE,
+                                               CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR,
+                                               CU_MEM_HANDLE_TYPE_FABRIC};
+    for (int h = 0; h < 3; ++h) {
+      m2.handleTypes = hts2[h];
+      CUmemGenericAllocationHandle t;
+      const CUresult r2 = cuMulticastCreate(&t, &m2);
+      const char *es = nullptr;
+      cuGetErrorString(r2, &es);
+      printf("{\"cuMulticastCreate_team\": %u, \"handle_type\": %d, \"result\": \"%s\"}\n", nd,
+             int(hts2[h]), es ? es : "?");
+      if (r2 == CUDA_SUCCESS) cuMemRelease(t);
+    }
+  }
   // the handle type the driver accepts varies by platform: try none, POSIX fd, fabric
   const CUmemAllocationHandleType hts[3] = {CU_MEM_HANDLE_TYPE_NONE,
                                             CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR,
                                             CU_MEM_HANDLE_TYPE_FABRIC};
   CUresult cr = CUDA_ERROR_INVALID_VALUE;
-  int hsel = -1;
   for (int h = 0; h < 3 && cr != CUDA_SUCCESS; ++h) {
     mp.handleTypes = hts[h];
     cr = cuMulticastCreate(&mch, &mp);
     const char *es = nullptr;
     cuGetErrorString(cr, &es);
     printf("{\"cuMulticastCreate_handle_type\": %d, \"result\": \"%s\"}\n", int(hts[h]), es ? es : "?");
-    if (cr == CUDA_SUCCESS) hsel = h;
   }
   if (cr != CUDA_SUCCESS) return 1;
-  (void)hsel;
   CK(cuMulticastAddDevice(mch, dev));
   CUmemAllocationProp ap = {};
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
