@@ -15,6 +15,11 @@ is unstated, reading R11):
 * ``"d1"``  x = (v + 1) * 2^-24            in (0, 1]   (cuRAND-uniform reading; all positive)
 * ``"d2"``  x = (v - 2^23) * 2^-23         in [-1, 1)  (zero-mean; used for throughput runs)
 * ``"d3"``  x = (v mod 17) - 8             in [-8, 8]  (integers: the bit-exact mode)
+* ``"d5"``  x = fp32 RN of (v 2^24 + w + 1) 2^-48 in (0, 1], w the next 24 bits of the word:
+            uniform values with FULL 24-bit significands at every magnitude (the others are
+            fixed-point grids, whose small values have few significant bits). Elements far
+            below 1 keep all their bits -- the inputs on which the 3xFP16 scheme's exception
+            path runs at a realistic rate (~2^-20 of the elements).
 
 Every value is an exact dyadic rational, so the numpy (host) and torch (device)
 implementations below agree bit for bit (tests/test_synth.py pins that), and any row
@@ -33,7 +38,7 @@ VECTOR_Y = 4
 _GOLDEN = 0x9E3779B97F4A7C15
 _MIX1 = 0xBF58476D1CE4E5B9
 _MIX2 = 0x94D049BB133111EB
-DISTS = ("d1", "d2", "d3", "d4")
+DISTS = ("d1", "d2", "d3", "d4", "d5")
 
 
 def gen_vector(n: int, vec_id: int, dist: str = "d4", seed: int = SEED) -> np.ndarray:
@@ -48,7 +53,10 @@ def _splitmix64_np(x: np.ndarray) -> np.ndarray:
     return z ^ (z >> np.uint64(31))
 
 
-def _to_dist_np(v: np.ndarray, dist: str) -> np.ndarray:
+def _to_dist_np(v: np.ndarray, dist: str, w=None) -> np.ndarray:
+    if dist == "d5":  # 48-bit dyadic in (0, 1], exact in fp64, one RN to fp32
+        return ((v.astype(np.float64) * 2.0 ** 24 + w.astype(np.float64) + 1.0) * 2.0 ** -48
+                ).astype(np.float32)
     if dist == "d4":  # uniform [-10, 10): the paper's vector benchmark values
         return ((v.astype(np.int64) - (1 << 23)).astype(np.float64) * (10 * 2.0 ** -23)
                 ).astype(np.float32)
@@ -73,8 +81,10 @@ def gen_rows(row0: int, nrows: int, cols: int, matrix_id: int, dist: str = "d2",
         for off in range(0, total, chunk):
             n = min(chunk, total - off)
             idx = np.arange(start + off, start + off + n, dtype=np.uint64)
-            v = _splitmix64_np(base ^ idx) >> np.uint64(40)
-            flat[off:off + n] = _to_dist_np(v, dist)
+            z = _splitmix64_np(base ^ idx)
+            v = z >> np.uint64(40)
+            w = (z >> np.uint64(16)) & np.uint64(0xFFFFFF)
+            flat[off:off + n] = _to_dist_np(v, dist, w)
     return out
 
 
@@ -125,7 +135,10 @@ def gen_rows_torch(row0: int, nrows: int, cols: int, matrix_id: int, dist: str =
         z = (z ^ _lsr(z, 27)) * _i64(_MIX2)
         z = z ^ _lsr(z, 31)
         v = _lsr(z, 40)
-        if dist == "d4":
+        if dist == "d5":
+            w = _lsr(z, 16) & 0xFFFFFF
+            vals = (v.to(torch.float64) * 2.0 ** 24 + w.to(torch.float64) + 1.0) * 2.0 ** -48
+        elif dist == "d4":
             vals = (v - (1 << 23)).to(torch.float64) * (10 * 2.0 ** -23)
         elif dist == "d1":
             vals = (v + 1).to(torch.float64) * 2.0 ** -24

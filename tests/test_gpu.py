@@ -405,11 +405,13 @@ def _sampled_rows(M, rng, extra=256):
 
 @pytest.mark.parametrize("M,N,K,dist", [(4096, 4096, 4096, "d2"), (16384, 16384, 16384, "d2"),
                                         (262144, 1024, 1024, "d2"), (32768, 32768, 32768, "d1"),
-                                        (16384, 16384, 16384, "d3")])
+                                        (16384, 16384, 16384, "d3"), (16384, 16384, 16384, "d5")])
 def test_full_size_sampled_rows(giga, torch_cuda, M, N, K, dist):
     """BASELINE configs at full size through the sharded device path bench.py times
     (ngpus = 1), oracle on sampled rows (every element of each sampled row). 32768^3 with the
-    all-positive d1 inputs is the hardest case for the truncating accumulator (K = 32768)."""
+    all-positive d1 inputs is the hardest case for the truncating accumulator (K = 32768);
+    d5 (full-significand floats) makes the 3xFP16 exception path run at scale (~2^-20 of the
+    elements of A and B, a few hundred per matrix at 16384^2)."""
     torch = torch_cuda
     dA = synth.gen_rows_torch(0, M, K, synth.MATRIX_A, dist, device="cuda")
     dB = synth.gen_rows_torch(0, K, N, synth.MATRIX_B, dist, device="cuda")

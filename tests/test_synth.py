@@ -26,6 +26,11 @@ def test_ranges(dist):
         assert x.min() >= -1 and x.max() < 1 and abs(float(x.mean())) < 0.01
     elif dist == "d4":
         assert x.min() >= -10 and x.max() <= 10 and abs(float(x.mean())) < 0.1
+    elif dist == "d5":
+        assert x.min() > 0 and x.max() <= 1 and abs(float(x.mean()) - 0.5) < 0.01
+        # full significands: small values keep bits below the 2^-24 grid of d1
+        small = x[x < 2.0 ** -8]
+        assert small.size and np.any(small != np.round(small * 2.0 ** 24) * 2.0 ** -24)
     else:
         assert np.array_equal(x, np.round(x)) and x.min() == -8 and x.max() == 8
 
