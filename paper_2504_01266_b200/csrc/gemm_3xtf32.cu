@@ -1398,68 +1398,75 @@ __global__ void prep16_bexp_kernel(const unsigned *__restrict__ bmax, int n_pad,
   if (j < n_pad) eb[j] = scale_exp(bmax[j]);
 }
 
-// B pass 3: B_hi / B_lo (fp16, K x N row-major, row stride ldh). Thread = 4 columns x 8 rows.
-__global__ void __launch_bounds__(256, 2) prep16_b_kernel(const float *__restrict__ B, int64_t ldb,
-                                                       int K, int N, const int *__restrict__ eb,
+// B pass 3: B_hi / B_lo (fp16, K x N row-major, row stride ldh) and B's exceptions. A block
+// covers 1024 columns (256 threads x 4: every row it touches is one 4 KiB stretch in, two 2 KiB
+// stretches out) and `rows` rows, 8 rows' loads in flight per thread (the pass-1 layout).
+__device__ __forceinline__ void prep16_b_put(const float4 v, int k, int n, int K, int4 e,
+                                             uint16_t *__restrict__ Bh,
+                                             uint16_t *__restrict__ Bl, int64_t ldh,
+                                             unsigned *__restrict__ bits,
+                                             unsigned *__restrict__ summ, int w2,
+                                             int *__restrict__ flag) {
+  uint16_t h[4], l[4];
+  const bool x0 = split_f16(v.x, e.x, h[0], l[0]);
+  const bool x1 = split_f16(v.y, e.y, h[1], l[1]);
+  const bool x2 = split_f16(v.z, e.z, h[2], l[2]);
+  const bool x3 = split_f16(v.w, e.w, h[3], l[3]);
+  if (x0 | x1 | x2 | x3) {
+    const unsigned nib = unsigned(x0) | unsigned(x1) << 1 | unsigned(x2) << 2 | unsigned(x3) << 3;
+    atomicOr(bits + int64_t(n >> 5) * K + k, nib << (n & 31));
+    atomicOr(summ + int64_t(n >> 5) * w2 + (k >> 5), 1u << (k & 31));
+    volatile int *f = flag + n;
+    if (x0) f[0] = 1;
+    if (x1) f[1] = 1;
+    if (x2) f[2] = 1;
+    if (x3) f[3] = 1;
+  }
+  __stcs(reinterpret_cast<uint2 *>(Bh + int64_t(k) * ldh + n),
+         make_uint2(h[0] | uint32_t(h[1]) << 16, h[2] | uint32_t(h[3]) << 16));
+  __stcs(reinterpret_cast<uint2 *>(Bl + int64_t(k) * ldh + n),
+         make_uint2(l[0] | uint32_t(l[1]) << 16, l[2] | uint32_t(l[3]) << 16));
+}
+
+__global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__ B, int64_t ldb,
+                                                       int K, int N, int rows,
+                                                       const int *__restrict__ eb,
                                                        uint16_t *__restrict__ Bh,
                                                        uint16_t *__restrict__ Bl, int64_t ldh,
                                                        unsigned *__restrict__ bits,
                                                        unsigned *__restrict__ summ, int w2,
                                                        int *__restrict__ flag) {
-  const int n4 = (N + 3) >> 2, kb8 = (K + 7) >> 3;
-  const int64_t total = int64_t(kb8) * n4;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int kb = int(i / n4), n = int(i - int64_t(kb) * n4) * 4;
-    const int4 e = *reinterpret_cast<const int4 *>(eb + n);  // eb is padded to 256 columns
-    // the 8 rows' loads first (independent: 8 x 16 B in flight per thread)
-    float4 pre[8];
-    const bool full8 = n + 3 < N && kb * 8 + 8 <= K;
-    if (full8) {
+  const int n = (blockIdx.x * 256 + int(threadIdx.x)) * 4;
+  if (n >= N) return;
+  const int r0 = blockIdx.y * rows;
+  const int r1 = min(K, r0 + rows);
+  const int4 e = *reinterpret_cast<const int4 *>(eb + n);  // eb is padded to 256 columns
+  if (n + 3 < N) {
+    int r = r0;
+    for (; r + 8 <= r1; r += 8) {
+      float4 v[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
-        pre[r] = __ldcs(reinterpret_cast<const float4 *>(B + int64_t(kb * 8 + r) * ldb + n));
-    }
+      for (int u = 0; u < 8; ++u)
+        v[u] = __ldcs(reinterpret_cast<const float4 *>(B + int64_t(r + u) * ldb + n));
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int k = kb * 8 + r;
-      if (k >= K) break;
-      const float *src = B + int64_t(k) * ldb + n;
-      uint16_t h[4], l[4];
-      if (n + 3 < N) {
-        const float4 v = full8 ? pre[r] : __ldcs(reinterpret_cast<const float4 *>(src));
-        const bool x0 = split_f16(v.x, e.x, h[0], l[0]);
-        const bool x1 = split_f16(v.y, e.y, h[1], l[1]);
-        const bool x2 = split_f16(v.z, e.z, h[2], l[2]);
-        const bool x3 = split_f16(v.w, e.w, h[3], l[3]);
-        if (x0 | x1 | x2 | x3) {
-          const unsigned nib =
-              unsigned(x0) | unsigned(x1) << 1 | unsigned(x2) << 2 | unsigned(x3) << 3;
-          atomicOr(bits + int64_t(n >> 5) * K + k, nib << (n & 31));
-          atomicOr(summ + int64_t(n >> 5) * w2 + (k >> 5), 1u << (k & 31));
-          volatile int *f = flag + n;
-          if (x0) f[0] = 1;
-          if (x1) f[1] = 1;
-          if (x2) f[2] = 1;
-          if (x3) f[3] = 1;
-        }
-        uint16_t *hd = Bh + int64_t(k) * ldh + n, *ld = Bl + int64_t(k) * ldh + n;
-        __stcs(reinterpret_cast<uint2 *>(hd),
-               make_uint2(h[0] | uint32_t(h[1]) << 16, h[2] | uint32_t(h[3]) << 16));
-        __stcs(reinterpret_cast<uint2 *>(ld),
-               make_uint2(l[0] | uint32_t(l[1]) << 16, l[2] | uint32_t(l[3]) << 16));
-      } else {
-        const int ev[4] = {e.x, e.y, e.z, e.w};
-        for (int q = 0; q < 4 && n + q < N; ++q) {
-          if (split_f16(src[q], ev[q], h[q], l[q]))
-            mark_exception(bits, int64_t((n + q) >> 5) * K + k, 1u << ((n + q) & 31), summ,
-                           int64_t((n + q) >> 5) * w2 + (k >> 5), k & 31, flag + n + q);
-          Bh[int64_t(k) * ldh + n + q] = h[q];
-          Bl[int64_t(k) * ldh + n + q] = l[q];
-        }
-      }
+      for (int u = 0; u < 8; ++u) prep16_b_put(v[u], r + u, n, K, e, Bh, Bl, ldh, bits, summ, w2, flag);
     }
+    for (; r < r1; ++r)
+      prep16_b_put(__ldcs(reinterpret_cast<const float4 *>(B + int64_t(r) * ldb + n)), r, n, K,
+                   e, Bh, Bl, ldh, bits, summ, w2, flag);
+    return;
   }
+  // the last, partial group of columns: scalar
+  const int ev[4] = {e.x, e.y, e.z, e.w};
+  for (int r = r0; r < r1; ++r)
+    for (int q = 0; q < 4 && n + q < N; ++q) {
+      uint16_t h, l;
+      if (split_f16(B[int64_t(r) * ldb + n + q], ev[q], h, l))
+        mark_exception(bits, int64_t((n + q) >> 5) * K + r, 1u << ((n + q) & 31), summ,
+                       int64_t((n + q) >> 5) * w2 + (r >> 5), r & 31, flag + n + q);
+      Bh[int64_t(r) * ldh + n + q] = h;
+      Bl[int64_t(r) * ldh + n + q] = l;
+    }
 }
 
 // ---- 3xFP16 exceptions: C += the remainders the split could not carry -----------------------
@@ -2152,11 +2159,10 @@ cudaError_t launch_prep16_b(const float *B, int64_t ldb, int64_t N, int64_t K, T
   prep16_bmax_kernel<<<g1, 256, 0, st>>>(B, ldb, int(K), int(N), int(rows), tp->bmax);
   prep16_bexp_kernel<<<unsigned((n_pad + 255) / 256), 256, 0, st>>>(
       tp->bmax, int(n_pad), const_cast<int *>(tp->eb));
-  const int64_t units = ((K + 7) / 8) * ((N + 3) / 4);
-  const int64_t blocks = std::min<int64_t>((units + 255) / 256, int64_t(num_sms_current()) * 8);
-  prep16_b_kernel<<<unsigned(std::max<int64_t>(blocks, 1)), 256, 0, st>>>(
-      B, ldb, int(K), int(N), tp->eb, const_cast<uint16_t *>(tp->Bh),
-      const_cast<uint16_t *>(tp->Bl), tp->ldbh, tp->xb, tp->sb2, tp->w2b, tp->fb);
+  // the same grid as pass 1 (1024-column blocks x row ranges, ~8 blocks per SM)
+  prep16_b_kernel<<<g1, 256, 0, st>>>(B, ldb, int(K), int(N), int(rows), tp->eb,
+                                     const_cast<uint16_t *>(tp->Bh), const_cast<uint16_t *>(tp->Bl),
+                                     tp->ldbh, tp->xb, tp->sb2, tp->w2b, tp->fb);
   compact16_b_kernel<<<unsigned((tp->wb + 7) / 8), 256, 0, st>>>(
       B, ldb, int(N), int(K), tp->Bh, tp->Bl, tp->ldbh, tp->eb, tp->xb, tp->sb2, tp->w2b, tp->fb,
       tp->bcnt, tp->blist);
