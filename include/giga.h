@@ -51,15 +51,19 @@
  *                        B and the gather fused into the GEMM epilogue) [nccl]
  *   GIGA_BCAST_CHUNKS, GIGA_GATHER_CHUNKS  chunk counts of the N > 1 plans [6 / 16 p2p, 4]
  *   GIGA_COMM_SMS, GIGA_NCCL_MAX_CTAS      SMs left to NCCL beside the GEMM [8, = COMM_SMS]
+ *   GIGA_NCCL_CTA_GBPS   per-CTA NCCL rate of the N > 1 plan's transfer model [50]
  *   GIGA_FORCE_COMM      1: run the NCCL pipeline even at one GPU (testing) [0]
- *   GIGA_TRACE           1: print a JSON timeline of each pipelined call on stderr [0]
- *   GIGA_HOST_H2D_GBS, GIGA_HOST_D2H_GBS, GIGA_HOST_GEMM_TFLOPS  rates of the host-path
- *                        schedule model [50, 50, 255]
- *   GIGA_SCHEME          3xtf32 | tf32bf16: force the product scheme (once) [by shape]
+ *   GIGA_TRACE           1: print a JSON timeline of each pipelined call on stderr (CUDA-event
+ *                        times, transfer GB/s, p2p: %globaltimer copy / GEMM-CTA intervals) [0]
+ *   GIGA_HOST_H2D_GBS, GIGA_HOST_D2H_GBS, GIGA_HOST_GEMM_TFLOPS, GIGA_HOST_GEMM4_TFLOPS
+ *                        rates of the host-path schedule model [50, 50, 250, 400 (3xFP16)]
+ *   GIGA_HOST_PLAN       "Me,P,Q": force that host-path schedule (measurements) [planned]
+ *   GIGA_SCHEME          3xtf32 | tf32bf16 | 3xfp16: force the product scheme (once) [by shape]
  *   GIGA_HI_RN, GIGA_A_PRE, GIGA_B_PRE  TF32 + BF16: 0 = truncated hi / A' / B' built on chip
  *                        instead of RN hi / prepared in HBM (measurements; once) [1, 1, 1]
  *   GIGA_LO_PRESPLIT     1: 3xTF32 low parts split in HBM (comparison mode; once) [0]
- *   GIGA_PROMOTE_KBLOCKS TMEM accumulation interval in 16-deep k-blocks (once) [8]
+ *   GIGA_PROMOTE_KBLOCKS TMEM accumulation interval in k-blocks, 16 deep (32 for 3xFP16)
+ *                        (once) [8]
  *   GIGA_CTA_GROUP       1 | 2: force the GEMM tile variant (once) [by shape]
  *   GIGA_WAVE_SYNC, GIGA_TAIL_SPLIT  0 disables the GEMM's wave barrier / tail split (once) [1]
  *   GIGA_GROUP_M, GIGA_L2_PROMO      raster group, TMA L2 promotion (once) [8, 2 = 128 B]

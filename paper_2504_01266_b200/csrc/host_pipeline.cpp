@@ -31,7 +31,25 @@ int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M
   int nsm = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, d.dev));
   rates.clusters = std::max(1, nsm / 2);
-  const HostPlan plan = host_plan_choose(M, N, K, rates);
+  HostPlan plan = host_plan_choose(M, N, K, rates);
+  // $GIGA_HOST_PLAN = "Me,P,Q" (measurements): that plan with equal K-chunks and row blocks
+  if (const char *e = getenv("GIGA_HOST_PLAN")) {
+    long long me = 0, pp = 1, qq = 1;
+    if (sscanf(e, "%lld,%lld,%lld", &me, &pp, &qq) == 3 && me >= 0 && me <= M && pp >= 1 &&
+        pp <= kHostMaxChunks && qq >= 1 && qq <= kHostMaxChunks) {
+      HostPlan f;
+      f.Me = me;
+      f.P = me > 0 ? int(pp) : 1;
+      for (int c = 0; c <= f.P; ++c) f.kb[c] = c == f.P ? K : (K * c / f.P) / 16 * 16;
+      f.Q = me < M ? int(qq) : 0;
+      if (f.Q > 0)
+        for (int q = 0; q <= f.Q; ++q) f.rb[q] = me + (M - me) * q / f.Q;
+      else
+        f.rb[0] = M;
+      f.t_model = host_plan_model(f, M, N, K, rates);
+      plan = f;
+    }
+  }
   static_assert(kHostMaxChunks <= kMaxChunks, "event arrays");
   const int64_t Me = plan.Me;
   const int P = plan.P, Q = plan.Q;
