@@ -117,3 +117,60 @@ def test_fuzz_p2p_virtual(torch_cuda, monkeypatch, M, N, K):
     finally:
         g.finalize()
         g.init(1)
+
+
+@pytest.mark.parametrize("cta_group", [1, 2])
+@pytest.mark.parametrize("M,N,K", [(M, N - N % 4 or 4, K - K % 4 or 4) for M, N, K in SHAPES[:10]])
+def test_fuzz_3xfp16_building_block(giga, torch_cuda, M, N, K, cta_group):
+    """The 3xFP16 scheme (terms = 4) on the fuzz shapes: integer inputs bit-exact, and d5
+    (full-significand floats: scales, exceptions and the fixes all live) within the bound."""
+    from oracle.check import check_close
+    torch = torch_cuda
+    A, B, ref = _inputs(M, N, K)
+    dC = torch.full((M, N), float("nan"), device="cuda")
+    giga.gemm_3xtf32(torch.from_numpy(A).cuda(), None, torch.from_numpy(B).cuda(), None, dC,
+                     M, N, K, terms=4, cta_group=cta_group)
+    assert check_exact(dC.cpu().numpy(), ref)[0], "d3"
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, "d5")
+    B = synth.gen_matrix(K, N, synth.MATRIX_B, "d5")
+    A[::7, ::5] *= np.float32(2.0 ** -27)  # exceptions in both operands
+    B[::5, ::7] *= np.float32(2.0 ** -27)
+    ref, S = oracle.gemm(A, B)
+    dC.fill_(float("nan"))
+    giga.gemm_3xtf32(torch.from_numpy(A).cuda(), None, torch.from_numpy(B).cuda(), None, dC,
+                     M, N, K, terms=4, cta_group=cta_group)
+    ok, st = check_close(dC.cpu().numpy(), ref, S)
+    assert ok, st
+
+
+def test_fuzz_3xfp16_forced_ragged_paths(torch_cuda):
+    """$GIGA_SCHEME=3xfp16 (a subprocess: the scheme is read once) through the host call and
+    the padded path of the ragged fuzz shapes (K, N not multiples of 4)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, os
+import numpy as np, torch
+sys.path.insert(0, os.getcwd())
+import oracle, synth
+from oracle.check import check_exact
+from paper_2504_01266_b200 import giga
+giga.init(1)
+for (M, N, K) in [(700, 301, 523), (33, 517, 1031), (513, 5, 1023), (257, 255, 4), (1, 1, 1)]:
+    A = synth.gen_matrix(M, K, synth.MATRIX_A, "d3"); B = synth.gen_matrix(K, N, synth.MATRIX_B, "d3")
+    ref, _ = oracle.gemm(A, B)
+    C = np.full((M, N), np.nan, np.float32)
+    giga.matmul(A, B, C, M, N, K, 1)
+    assert check_exact(C, ref)[0], ("host", M, N, K)
+    dC = torch.full((M, N), float("nan"), device="cuda")
+    giga.matmul_sharded([torch.from_numpy(A).cuda()], [torch.from_numpy(B).cuda()], [dC], M, N, K)
+    assert check_exact(dC.cpu().numpy(), ref)[0], ("sharded", M, N, K)
+giga.finalize()
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root,
+                       env=dict(os.environ, GIGA_SCHEME="3xfp16"), capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
