@@ -17,10 +17,10 @@ DEBUG_LIB = os.path.join(HERE, "libgiga_debug.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["gemm_3xtf32.cu", "vecops.cu"]
+CU_SOURCES = ["gemm_3xtf32.cu", "prep16.cu", "vecops.cu"]
 CPP_SOURCES = ["api.cpp", "runtime.cpp", "pipeline_nccl.cpp", "p2p.cpp", "host_pipeline.cpp",
                "host_plan.cpp", "nccl_loader.cpp"]
-HEADERS = ["ptx.cuh", "kernels.h", "nccl_loader.h", "host_plan.h", "runtime.h", "debug_kernels.cu"]
+HEADERS = ["ptx.cuh", "split16.cuh", "kernels.h", "nccl_loader.h", "host_plan.h", "runtime.h", "debug_kernels.cu"]
 
 
 def nccl_paths():

@@ -128,6 +128,9 @@ cudaError_t launch_stamp(uint64_t *slot, cudaStream_t st);
 cudaError_t launch_fix16(const float *A, int64_t lda, const float *B, int64_t ldb, int64_t M,
                          int64_t N, int64_t K, const TermsPrep *tp, float *C, int64_t ldc,
                          const GemmExtra *ex, cudaStream_t st);
+// B's preparation kernels alone (prep16.cu; launch_prep16_b adds the reuse bookkeeping).
+cudaError_t prep16_b_kernels(const float *B, int64_t ldb, int64_t N, int64_t K,
+                             const TermsPrep *tp, cudaStream_t st);
 // Kernels launch_prep16_b / launch_prep16_a / launch_fix16 issue (bench.py's launch count).
 constexpr int kPrep16BLaunches = 4, kPrep16ALaunches = 1, kFix16Launches = 1;
 cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B,
