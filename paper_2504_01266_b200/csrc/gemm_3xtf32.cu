@@ -1189,9 +1189,11 @@ int default_promote_kblocks(int terms) {
     return -1;
   }();
   if (v >= 0) return v;
-  return terms == 2 ? kDefaultPromoteKBlocksT2
-         : terms == 4 ? kDefaultPromoteKBlocksT4
-                      : kDefaultPromoteKBlocks;
+  static const int v4 = [] {  // $GIGA_PROMOTE_KBLOCKS_T4: the 3xFP16 scheme's alone
+    const char *e = getenv("GIGA_PROMOTE_KBLOCKS_T4");
+    return (e && *e && atoi(e) > 0) ? atoi(e) : kDefaultPromoteKBlocksT4;
+  }();
+  return terms == 2 ? kDefaultPromoteKBlocksT2 : terms == 4 ? v4 : kDefaultPromoteKBlocks;
 }
 
 static int forced_scheme() {
