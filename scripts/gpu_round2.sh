@@ -10,3 +10,5 @@ for c in c3_16384 c2_4096 c4_tall; do timeout -s KILL 600 python bench.py --conf
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm|prep|fix|compact" --csv --log-file gpurun_out/launches_bench_c5.csv python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1; echo launches_rc=$?
 bash scripts/gpu_sanitize.sh > /dev/null 2>&1; head -12 gpurun_out/compute_sanitizer.txt
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/nvls_probe scripts/nvls_probe.cu -lcuda && timeout -s KILL 120 /tmp/nvls_probe > gpurun_out/nvls_probe.jsonl 2>&1; cat gpurun_out/nvls_probe.jsonl
+MNK=32768,32768,32768 PKS=8 TERMS=4 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:gemm_3xtf32 -s 2 -c 1 -o gpurun_out/prof_c5_fp16 python scripts/sweep_gemm.py > gpurun_out/ncu_c5.log 2>&1; echo ncu_full_rc=$?
+python scripts/ncu_summary.py gpurun_out/prof_c5_fp16.ncu-rep > gpurun_out/prof_c5_fp16_summary.json 2>&1; head -30 gpurun_out/prof_c5_fp16_summary.json
