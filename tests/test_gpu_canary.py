@@ -65,7 +65,7 @@ def _check_canary(outer, rows, cols, ld, what):
 @pytest.mark.parametrize("M,N,K,dist", [(1000, 520, 1040, "d3"),   # ragged, 1-CTA tiles
                                         (4096, 4096, 4096, "d3"),  # k-split reduce (3 waves + 34)
                                         (512, 1536, 2048, "d2"),   # k-split workspace
-                                        (4096, 8192, 2048, "d1")])  # TF32 + BF16 product scheme
+                                        (8192, 8192, 2048, "d5")])  # the 3xFP16 product scheme
 def test_sharded_one_gpu_guard_rows(lib, torch_cuda, M, N, K, dist):
     torch = torch_cuda
     giga = lib([0])
