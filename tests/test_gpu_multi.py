@@ -160,8 +160,14 @@ def _rank_worker(rank, world, port, M, N, K, q, transport="p2p", own_device=Fals
         q.put((rank, False, False, False, repr(e)))
 
 
-@pytest.mark.parametrize("world,M,N,K", [(2, 1000, 520, 1040), (3, 517, 256, 2064)])
-def test_rank_p2p_across_processes(torch_cuda, world, M, N, K):
+@pytest.mark.parametrize("world,M,N,K,scheme", [(2, 1000, 520, 1040, None),
+                                                (3, 517, 256, 2064, None),
+                                                (2, 1000, 520, 2064, "3xfp16"),
+                                                (3, 517, 256, 2064, "3xfp16")])
+def test_rank_p2p_across_processes(torch_cuda, world, M, N, K, scheme):
+    """Processes sharing cuda:0 through the rank API, p2p transport; with $GIGA_SCHEME=3xfp16
+    the load-C epilogue, the operand scales and the A-side fix's mirror writes go into the
+    peers' C_full through CUDA IPC."""
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as so:
@@ -169,7 +175,9 @@ def test_rank_p2p_across_processes(torch_cuda, world, M, N, K):
         port = so.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rank_worker, args=(r, world, port, M, N, K, q))
+    env = {"GIGA_SCHEME": scheme} if scheme else None
+    procs = [ctx.Process(target=_rank_worker,
+                         args=(r, world, port, M, N, K, q, "p2p", False, env))
              for r in range(world)]
     for p in procs:
         p.start()
