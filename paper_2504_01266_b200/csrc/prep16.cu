@@ -290,8 +290,8 @@ __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__
 // (rep(b) rows are contiguous). Both sum in fp64 in ascending k and round once into C
 // (deterministic); fix16_a mirrors the new values to the peers' copies when the epilogue also
 // wrote those (fused gather), and skips rows without exceptions -- the common case: float
-// data has ~1e-6 of its elements more than 2^20 below their row / column maximum (the synth
-// distributions, fixed-point grids, have none).
+// data has ~1e-6 of its elements more than 2^20 below their row / column maximum (synth d5
+// has them at that rate; d1-d4, fixed-point grids, have none).
 struct PeerC {
   float *p[kMaxCDst - 1];
   int n;
