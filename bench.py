@@ -452,13 +452,11 @@ def main():
                          f"TF32-equivalent tensor work (3 or 2 x 2 rows N K per launch) / "
                          f"event time of the GEMM launches of a step",
             "scheme": scheme,
-            "limit_note": ("tensor pipe (3 TF32 MMAs per k8 step) at the power-capped clock"
-                           if terms_set == [3] else
-                           "tensor pipe (3 FP16 MMAs per k16 step) at the power-capped clock"
-                           if terms_set == [4] else
-                           "operand feed: 32 KiB of TMA fills per CTA per 2-MMA stage against "
-                           "the per-SM fill ceiling (roofline.feed; multicast measured not to "
-                           "raise it), and the power cap: DESIGN.md 6.7"),
+            "limit_note": ("operand feed: 32 KiB of TMA fills per CTA per 2-MMA stage against "
+                           "the per-SM fill rate (roofline.feed), and the power cap: DESIGN.md 6.7"
+                           if 2 in terms_set else
+                           "tensor pipe (three MMAs per k8 step with 3xTF32, per k16 step with "
+                           "3xFP16) at the power-capped clock"),
             "prep_ms_per_step": round(kt["split_ms"] / args.steps, 4),
             "prep_launches_per_step": round(kt["split_launches"] / args.steps, 2)}
     if terms_set == [4] and achieved:
