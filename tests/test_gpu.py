@@ -405,7 +405,8 @@ def _sampled_rows(M, rng, extra=256):
 
 @pytest.mark.parametrize("M,N,K,dist", [(4096, 4096, 4096, "d2"), (16384, 16384, 16384, "d2"),
                                         (262144, 1024, 1024, "d2"), (32768, 32768, 32768, "d1"),
-                                        (16384, 16384, 16384, "d3"), (16384, 16384, 16384, "d5")])
+                                        (16384, 16384, 16384, "d3"), (16384, 16384, 16384, "d5"),
+                                        (32768, 32768, 32768, "d5")])
 def test_full_size_sampled_rows(giga, torch_cuda, M, N, K, dist):
     """BASELINE configs at full size through the sharded device path bench.py times
     (ngpus = 1), oracle on sampled rows (every element of each sampled row). 32768^3 with the
