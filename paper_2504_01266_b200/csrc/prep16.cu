@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(256) fix16_a_kernel(
   __shared__ int ks[kFixCap];
   __shared__ double ds[kFixCap];
   __shared__ int n_sh, s_sh, nrows;
-  __shared__ int rows[256];
+  __shared__ int rows[32];  // the flagged rows of the current 32-row window
   // this block's columns: chunk blockIdx.y of gridDim.y (multiples of 4)
   const int chunk = ((N + int(gridDim.y) - 1) / int(gridDim.y) + 3) & ~3;
   const int jlo = int(blockIdx.y) * chunk, jhi = min(N, jlo + chunk);
