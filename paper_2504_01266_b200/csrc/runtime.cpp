@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 
 namespace giga {
 
@@ -398,6 +399,25 @@ static bool geometric_bounds(int64_t total, int n, double ratio, int64_t align,
 // previous gather): big shards keep 4 chunks, small ones (c2 on 2 GPUs) take fewer launches.
 // $GIGA_BCAST_CHUNKS / $GIGA_GATHER_CHUNKS force the counts; $GIGA_LAUNCH_US sets O.
 // E.g. 32768^3 on 8 GPUs (NCCL): 6 chunks, 4 row chunks; 4096^3 on 2 GPUs: 3 and 2.
+// Modelled time of one K-chunk GEMM launch over `rows` rows, operand preparation included:
+// the scheme product_terms picks for it at that scheme's rate for this K -- short chunks pay
+// the per-tile fill / epilogue and, for 3xFP16, the preparation of the whole Kc x N chunk of B
+// (profiles/r02_chunk_rate_sweep.jsonl: 3xFP16 ~430 k / (k + 900) TFLOP/s, 3xTF32
+// ~260 k / (k + 64), TF32 + BF16 ~255 k / (k + 128)) -- times the last-wave quantisation of
+// its 256 x 256 pair tiles on the 70 pairs the pipeline leaves to the GEMM, plus a launch
+// cost O.
+static double chunk_gemm_time(int64_t rows, int64_t N, int64_t Kc, double O) {
+  if (rows <= 0 || Kc <= 0) return 0.0;
+  const int t = product_terms(nullptr, rows, N, Kc);
+  const double k = double(Kc);
+  const double rate = t == 4 ? 430e12 * k / (k + 900.0)
+                      : t == 2 ? 255e12 * k / (k + 128.0)
+                               : 260e12 * k / (k + 64.0);
+  const double waves = double((rows + 255) / 256) * double((N + 255) / 256) / 70.0;
+  const double quant = waves / std::ceil(waves);
+  return O + 2.0 * double(rows) * double(N) * k / (rate * quant);
+}
+
 Plan make_plan(int64_t M, int64_t N, int64_t K, int world, bool aligned) {
   Plan pl;
   int64_t rows_max = 0;
@@ -436,7 +456,18 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, int world, bool aligned) {
       for (int c = 0; c < pb; ++c) b[c] = (K * c / pb) / 16 * 16;
       b[pb] = K;
     }
-    const double cost = hops * 4.0 * double(b[1]) * double(N) / bw + O * pb;
+    // the start-up (the first chunk's transfer, down the chain for p2p) plus the chunks'
+    // GEMMs: more chunks start sooner but run shorter, slower launches (round 2: with the
+    // 3xFP16 GEMM the short first chunks cost more than the start-up they save)
+    double cost = hops * 4.0 * double(b[1]) * double(N) / bw;
+    for (int c = 0; c + 1 < pb; ++c) cost += chunk_gemm_time(rows_max, N, b[c + 1] - b[c], O);
+    // the last chunk runs as row chunks (below; ~4 of 0.7-geometric sizes when rows allow)
+    const int64_t kl = K - b[pb - 1];
+    const int npc = int(std::min<int64_t>(4, std::max<int64_t>(1, rows_max / 256)));
+    int64_t rb[kMaxChunks + 1];
+    if (!geometric_bounds(rows_max, npc, 0.7, 256, 256, rb))
+      for (int i = 0; i <= npc; ++i) rb[i] = rows_max * i / npc;
+    for (int q = 0; q < npc; ++q) cost += chunk_gemm_time(rb[q + 1] - rb[q], N, kl, O);
     if (cost < best) {
       best = cost;
       pl.pb = pb;

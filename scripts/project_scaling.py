@@ -3,7 +3,8 @@ enqueues exactly the GEMM launches a rank issues at world N (K-chunks accumulati
 chunk in row chunks, 140 of 148 SMs) without the communication. With B's broadcast and C's
 gather overlapped the N-GPU step cannot be faster than this; the
 exposed part of the exchange adds to it. Prints one JSON line per config:
-{"config", "N": {"compute_ms", "ratio_to_N1"}, "t_comm_model_ms"}.
+{"config", "N": {"compute_ms", "ratio_to_N1", "t_comm_model_ms", "kchunks", "row_chunks",
+"startup_model_ms"}}.
 Usage: python scripts/project_scaling.py [c3_16384 c5_32768 c4_tall c2_4096]."""
 import json, os, sys
 import torch
@@ -39,6 +40,12 @@ for name in names:
         t_comm = 4.0 * ((K * N if world > 1 else 0) + (M - min(rows)) * N) / (NV_GBS * 1e6)
         out[str(world)] = {"compute_ms": round(ms, 3), "tflops_per_gpu": round(
             2.0 * rows[r] * N * K / ms / 1e9, 1), "t_comm_model_ms": round(t_comm, 3)}
+        kb, rc = giga.pipeline_plan(M, N, K, world)
+        out[str(world)]["kchunks"] = [int(b - a) for a, b in zip(kb[:-1], kb[1:])]
+        out[str(world)]["row_chunks"] = int(rc)
+        # before the first GEMM can start: the first K-chunk of B arrives (one ring pass)
+        out[str(world)]["startup_model_ms"] = round(
+            4.0 * int(kb[1] - kb[0]) * N / (NV_GBS * 1e6), 3) if world > 1 else 0.0
         del A, C
     for world in (2, 4, 8):
         out[str(world)]["compute_speedup_vs_1"] = round(
