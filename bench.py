@@ -306,6 +306,11 @@ def main():
                     choices=["nccl", "p2p"],
                     help="N > 1: NCCL pipeline (default) or the peer-to-peer transport "
                          "(copy-engine B chain + gather fused into the GEMM epilogue)")
+    ap.add_argument("--gather", default="unicast", choices=["unicast", "mc"],
+                    help="--transport p2p, N > 1: the fused gather's stores -- one per peer "
+                         "(unicast) or one per piece into an NVLink multicast team of C_full "
+                         "buffers (mc; falls back to unicast where the driver refuses "
+                         "multicast, noted in config.gather)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     os.environ["GIGA_TRANSPORT"] = args.transport
@@ -357,6 +362,15 @@ def main():
     else:
         B = torch.empty((K, N), dtype=torch.float32, device=dev)
     C = torch.empty((M, N), dtype=torch.float32, device=dev)
+    gather_note = None
+    if world > 1 and args.transport == "p2p" and args.gather == "mc":
+        # C_full bound into one multicast team (giga_rank_mc_*): the epilogue writes each
+        # piece once and the NVSwitch fills every rank's copy
+        try:
+            C = giga.as_float_tensor(giga.rank_mc_alloc(M * N * 4), M * N, dev).view(M, N)
+            gather_note = "multicast (one multimem.st per piece)"
+        except giga.GigaError as e:
+            gather_note = f"unicast (multicast refused: {str(e)[:120]})"
     if world > 1 and args.transport == "p2p":  # register B / C_full with every peer (IPC)
         blobs = [None] * world
         pg.all_gather_object(blobs, giga.p2p_export(B, C))
@@ -554,6 +568,7 @@ def main():
             "config": {"workload": f"{args.config} M={M} N={N} K={K}", "dist": args.dist,
                        "parallelism": f"row-split x{world}",
                        "transport": args.transport if world > 1 else "none (1 GPU)",
+                       **({"gather": gather_note} if gather_note else {}),
                        "l2": "L2 flushed between timed steps (512 MiB write outside the "
                              "per-step events)"},
             "roofline": roof, "roofline_step": step_roof, "cpu_baseline": cpu, "e2e": e2e,

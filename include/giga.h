@@ -49,6 +49,9 @@
  * Environment (read at call time unless noted; defaults in brackets):
  *   GIGA_TRANSPORT       nccl | p2p: the N > 1 exchange (NCCL collectives, or copy engines for
  *                        B and the gather fused into the GEMM epilogue) [nccl]
+ *   GIGA_P2P_STORE       tma | vec: how the p2p fused gather writes the peers' C_full from the
+ *                        epilogue -- TMA stores, or 16-byte st.global stores (the code path
+ *                        of the multicast gather, giga_mc_alloc, one store per peer) [tma]
  *   GIGA_BCAST_CHUNKS, GIGA_GATHER_CHUNKS  chunk counts of the N > 1 plans [6 / 16 p2p, 4]
  *   GIGA_COMM_SMS, GIGA_NCCL_MAX_CTAS      SMs left to NCCL beside the GEMM [8, = COMM_SMS]
  *   GIGA_NCCL_CTA_GBPS   per-CTA NCCL rate of the N > 1 plan's transfer model [50]
@@ -72,6 +75,7 @@
 #ifndef GIGA_H_
 #define GIGA_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -241,6 +245,45 @@ int giga_rank_p2p_export(const float *B, float *C_full, uint8_t *blob);
 int giga_rank_p2p_import(const uint8_t *blobs, int world);
 
 /* ------------------------------------------------------------------------------------ */
+/* NVLink multicast C_full buffers: the fused gather with ONE store per piece of C (SURVEY.md
+ * 8(f) N4). The gather is a concatenation of the GPUs' row blocks (S4.2.3;
+ * PAPER.md:291, S4.2.7). When the C_full buffers the p2p transport is given were allocated
+ * here, they are bound into one cuMulticastCreate team: the last K-chunk's GEMM epilogue (and
+ * the 3xFP16 A-side fix) writes each 16-byte piece of its rows once, with multimem.st to the
+ * team's multicast address, and the NVSwitch replicates it into every GPU's C_full -- NVLink
+ * egress 1 x the GPU's rows instead of (g - 1) x with the unicast stores to every peer. With
+ * ordinary buffers the transport keeps the unicast gather. Requires N % 4 == 0 (as the p2p
+ * transport does). The buffers are zero-filled device memory owned by the library, valid
+ * until freed / giga_finalize. NOT RUN on hardware yet: the 1-GPU pool this was built on
+ * refuses cuMulticastCreate.
+ * Errors: UNSUPPORTED (the driver refuses multicast: no NVSwitch / fabric manager, device
+ * attribute MULTICAST_SUPPORTED = 0, pidfd_getfd not permitted), NOT_INITIALIZED,
+ * INVALID_ARG, OOM, CUDA. */
+
+/* Single process (giga_init over distinct devices): C_full[g] (out) = GPU g's buffer of
+ * `bytes` (rounded up to the multicast granularity) for g < ngpus. Pass them as the C_full
+ * of giga_matmul_sharded with $GIGA_TRANSPORT=p2p. Repeated devices: INVALID_ARG. */
+int giga_mc_alloc(int ngpus, size_t bytes, float **C_full);
+/* Releases the team whose GPU-0 buffer is C_full0 (after its work finished). */
+int giga_mc_free(float *C_full0);
+
+/* Rank API ($GIGA_TRANSPORT=p2p): three collective phases, each on every rank, with a host
+ * barrier (e.g. torch.distributed) between them:
+ *   1. rank 0: giga_rank_mc_create(bytes, blob) -- makes the team object for `world`
+ *      devices and fills GIGA_MC_BLOB_BYTES bytes (its pid and POSIX descriptor); the caller
+ *      broadcasts the blob;
+ *   2. every rank: giga_rank_mc_join(blob) -- imports the object (pidfd_getfd; rank 0 uses
+ *      its own) and adds this rank's device;  barrier;
+ *   3. every rank: giga_rank_mc_bind(&C_full) -- binds this rank's buffer and maps the
+ *      multicast address; barrier.
+ * Then register C_full with giga_rank_p2p_export (every rank must use its team buffer) and
+ * call giga_matmul_rank with it. One team per process; released by giga_finalize. */
+#define GIGA_MC_BLOB_BYTES 64
+int giga_rank_mc_create(size_t bytes, uint8_t *blob);
+int giga_rank_mc_join(const uint8_t *blob);
+int giga_rank_mc_bind(float **C_full);
+
+/* ------------------------------------------------------------------------------------ */
 /* Single-device building blocks (device pointers on the current CUDA device; work is
  * enqueued on `stream`, a cudaStream_t, 0 = legacy default stream; no host sync). They do
  * not need giga_init. */
@@ -281,6 +324,24 @@ int giga_gemm_3xtf32(const float *A, const float *A_lo, const float *B, const fl
 int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const float *B_lo,
                         float *C, int64_t M, int64_t N, int64_t K, int64_t ldc, int terms,
                         int promote_kblocks, int cta_group, void *stream);
+
+/* The shard GEMM with its fused-gather epilogue exposed (tests / probes; current device):
+ * C = A * B (ldc row stride) written by the epilogue to C and to peer_c[0..n_peer) (same
+ * shape and ldc; any device memory this device can store to: NVLink peers, or buffers of the
+ * same device as the tests use) with store_mode 0 = TMA bulk stores (the p2p transport's
+ * default), 1 = 16-byte st.global stores ($GIGA_P2P_STORE=vec), 2 = 16-byte multimem.st to
+ * C as the multicast address (n_peer = 0). Mode 2 is the multicast gather's store path:
+ * given a giga_mc_alloc / giga_rank_mc_bind team address it writes every member; given an
+ * ordinary address (what a pool without multicast allows) the same SASS store (STG.E.128:
+ * multimem.st and st.global assemble alike on sm_100a -- the multicast is in the address)
+ * writes that buffer alone, which is how tests check its addressing -- outside the PTX
+ * contract, a test hook. terms = 0: the product path's scheme choice (and, for 3xFP16,
+ * its exception fixes mirrored to the peers / multicast); 1-4 as giga_gemm_3xtf32_ex.
+ * Needs K % 4 == N % 4 == ldc % 4 == 0 and 16-byte aligned pointers. Errors: INVALID_ARG,
+ * UNSUPPORTED ($GIGA_LO_PRESPLIT=1), CUDA. */
+int giga_gemm_gather_ex(const float *A, const float *B, float *C, float *const *peer_c,
+                        int n_peer, int64_t M, int64_t N, int64_t K, int64_t ldc, int terms,
+                        int store_mode, void *stream);
 
 /* Measurement tool for the N > 1 pipeline on a single GPU: enqueues on `stream` (current
  * device) exactly the GEMM launches rank `rank` of `world` issues in giga_matmul_rank /

@@ -19,7 +19,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["gemm_3xtf32.cu", "prep16.cu", "vecops.cu"]
 CPP_SOURCES = ["api.cpp", "runtime.cpp", "pipeline_nccl.cpp", "p2p.cpp", "host_pipeline.cpp",
-               "host_plan.cpp", "nccl_loader.cpp"]
+               "host_plan.cpp", "nccl_loader.cpp", "mcast.cpp"]
 HEADERS = ["ptx.cuh", "split16.cuh", "kernels.h", "nccl_loader.h", "host_plan.h", "runtime.h", "debug_kernels.cu"]
 
 

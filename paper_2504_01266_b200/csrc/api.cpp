@@ -269,6 +269,7 @@ int giga_finalize(void) {
   g.rank_comm = nullptr;
   if (!g.devs.empty()) cudaSetDevice(g.devs[0].dev);
   p2p_release();
+  mc_release_all();
   release_gemm_caches();
   for (auto &d : g.devs) ctx_destroy(d);
   g.devs.clear();
@@ -551,6 +552,8 @@ namespace {
 struct P2PBlob {
   cudaIpcMemHandle_t hB, hC, hF;
   uint64_t offB, offC;
+  uint32_t mc;  // 1: C_full is this rank's multicast team buffer (no IPC handle: the epilogue
+                // reaches every peer's copy through the team address)
 };
 static_assert(sizeof(P2PBlob) <= GIGA_P2P_BLOB_BYTES, "blob too small");
 
@@ -581,7 +584,8 @@ int giga_rank_p2p_export(const float *B, float *C_full, uint8_t *blob) {
   }
   P2PBlob b{};
   TRY(ipc_handle(B, &b.hB, &b.offB));
-  TRY(ipc_handle(C_full, &b.hC, &b.offC));
+  b.mc = rank_mc_buffer(C_full) ? 1u : 0u;
+  if (!b.mc) TRY(ipc_handle(C_full, &b.hC, &b.offC));
   uint64_t off0 = 0;
   TRY(ipc_handle(x.flags, &b.hF, &off0));
   x.B = const_cast<float *>(B);
@@ -599,6 +603,18 @@ int giga_rank_p2p_import(const uint8_t *blobs, int world) {
     return fail(GIGA_ERR_INVALID_ARG, "giga_rank_p2p_import: call export first, world=%d", world);
   DevCtx &d = g.devs[0];
   CK(cudaSetDevice(d.dev));
+  // every rank's C_full is a multicast team buffer, or none is
+  P2PBlob mine;
+  memcpy(&mine, blobs + size_t(g.rank) * GIGA_P2P_BLOB_BYTES, sizeof mine);
+  for (int q = 0; q < world; ++q) {
+    P2PBlob b;
+    memcpy(&b, blobs + size_t(q) * GIGA_P2P_BLOB_BYTES, sizeof b);
+    if (b.mc != mine.mc)
+      return fail(GIGA_ERR_INVALID_ARG,
+                  "giga_rank_p2p_import: rank %d's C_full is %sa multicast team buffer, rank "
+                  "%d's is %s",
+                  q, b.mc ? "" : "not ", g.rank, mine.mc ? "" : "not");
+  }
   for (void *p : x.opened) cudaIpcCloseMemHandle(p);
   x.opened.clear();
   x.peerB.assign(world, nullptr);
@@ -616,12 +632,14 @@ int giga_rank_p2p_import(const uint8_t *blobs, int world) {
     void *pb = nullptr, *pc = nullptr, *pf = nullptr;
     CK(cudaIpcOpenMemHandle(&pb, b.hB, cudaIpcMemLazyEnablePeerAccess));
     x.opened.push_back(pb);
-    CK(cudaIpcOpenMemHandle(&pc, b.hC, cudaIpcMemLazyEnablePeerAccess));
-    x.opened.push_back(pc);
+    if (!b.mc) {
+      CK(cudaIpcOpenMemHandle(&pc, b.hC, cudaIpcMemLazyEnablePeerAccess));
+      x.opened.push_back(pc);
+    }
     CK(cudaIpcOpenMemHandle(&pf, b.hF, cudaIpcMemLazyEnablePeerAccess));
     x.opened.push_back(pf);
     x.peerB[q] = reinterpret_cast<float *>(static_cast<char *>(pb) + b.offB);
-    x.peerC[q] = reinterpret_cast<float *>(static_cast<char *>(pc) + b.offC);
+    x.peerC[q] = pc ? reinterpret_cast<float *>(static_cast<char *>(pc) + b.offC) : nullptr;
     x.peerF[q] = static_cast<uint32_t *>(pf);
   }
   // call numbers stay monotonic across re-registrations: the flag pages keep old values
@@ -693,6 +711,41 @@ int giga_gemm_3xtf32_ex(const float *A, const float *A_lo, const float *B, const
   CK(timed(0, st, [&] {
     return launch_gemm_3xtf32(A, A_lo, B, B_lo, C, M, N, K, ldc, terms, promote_kblocks, st,
                               cta_group);
+  }));
+  return GIGA_OK;
+}
+
+int giga_gemm_gather_ex(const float *A, const float *B, float *C, float *const *peer_c,
+                        int n_peer, int64_t M, int64_t N, int64_t K, int64_t ldc, int terms,
+                        int store_mode, void *stream) {
+  if (!A || !B || !C || n_peer < 0 || n_peer > kMaxCDst - 1 || (n_peer && !peer_c) ||
+      terms < 0 || terms > 4 || store_mode < 0 || store_mode > 2 ||
+      (store_mode == 2 && n_peer))
+    return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_gather_ex: bad arguments");
+  TRY(check_dims(M, N, K));
+  if ((K & 3) || (N & 3) || (ldc & 3) || ldc < N || !aligned16(A) || !aligned16(B) ||
+      !aligned16(C))
+    return fail(GIGA_ERR_INVALID_ARG,
+                "giga_gemm_gather_ex: needs K%%4 == N%%4 == ldc%%4 == 0, ldc >= N, 16B-aligned");
+  for (int i = 0; i < n_peer; ++i)
+    if (!peer_c[i] || !aligned16(peer_c[i]))
+      return fail(GIGA_ERR_INVALID_ARG, "giga_gemm_gather_ex: peer %d NULL / misaligned", i);
+  if (lo_presplit())
+    return fail(GIGA_ERR_UNSUPPORTED, "giga_gemm_gather_ex: not with GIGA_LO_PRESPLIT=1");
+  if (ensure_tma_encoder() != 0) return fail(GIGA_ERR_CUDA, "TMA encoder unavailable");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  GemmExtra ex;
+  ex.lda = K;
+  ex.ldb = N;
+  float *peers[kMaxCDst];
+  for (int i = 0; i < n_peer; ++i) peers[i] = peer_c[i];
+  ex.peer_c = peers;
+  ex.n_peer_c = n_peer;
+  ex.vec_store = store_mode == 1 ? 1 : 0;
+  ex.mc_c = store_mode == 2 ? C : nullptr;
+  if (terms == 0) return run_gemm(A, nullptr, B, nullptr, C, M, N, K, ldc, ex, st);
+  CK(timed(0, st, [&] {
+    return launch_gemm_3xtf32(A, nullptr, B, nullptr, C, M, N, K, ldc, terms, -1, st, 0, &ex);
   }));
   return GIGA_OK;
 }

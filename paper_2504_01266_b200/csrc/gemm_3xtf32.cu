@@ -124,6 +124,10 @@ struct GemmParams {
   int wave_sync;  // 1: a producer starts unit u's loads once every unit of the previous waves
                   // (u / clusters) has been issued by all its CTAs
   int n_cdst;     // C destinations in CMaps (1 + peers when the gather is fused)
+  // how the epilogue writes C: kStoreTma (CMaps), kStoreVec (16-byte st.global to vdst[0..
+  // n_cdst)), kStoreMulticast (multimem.st to the team address vdst[0]; n_cdst = 1)
+  int st_mode;
+  float *vdst[kMaxCDst];
   int lo_smem;    // 1: lo tiles computed in smem from the raw tiles; 0: TMA-loaded (A_lo, B_lo)
   int hi_rn;      // terms == 2: hi = RN tf32(x) written over the raw tile (else hi = trunc)
   int b_pre;      // terms == 2: B_hi and B' precomputed in HBM by prep_b_kernel (TMA-loaded
@@ -148,6 +152,8 @@ struct GemmParams {
   const int4 *blist;
   uint64_t *cta_ns;  // $GIGA_TRACE: [2 blockIdx.x] = this CTA's start, [+1] = its end (ns)
 };
+
+enum { kStoreTma = 0, kStoreVec = 1, kStoreMulticast = 2 };
 
 // C tensor maps: [0] this GPU's C, [1..] the same rows of the peers' C_full buffers.
 struct CMaps {
@@ -282,6 +288,31 @@ __device__ __forceinline__ void fix_b_block(const GemmParams &p, float *stg, int
     // staging tile: row `lane`, 16-byte chunk (jb / 4) ^ (lane & 7), 128-byte rows
     float *v = stg + lane * 32 + (((jb >> 2) ^ (lane & 7)) << 2) + (jb & 3);
     *v = float(double(*v) + t);
+  }
+}
+
+// The staged 32 x 32 block (rows row0.., columns col0..) written with 16-byte stores instead of
+// the TMA unit (kStoreVec: to C and every peer; kStoreMulticast: once, to the team address,
+// which the NVSwitch replicates into every GPU's C_full -- DESIGN.md 7.4). Each 8-lane group
+// writes one 128-byte row segment per instruction (4 rows per warp store, coalesced), reading
+// the staging tile's swizzled chunks (chunk j of row r at j ^ (r & 7): conflict-free). Rows
+// >= M and columns >= N are clipped here (N % 4 == 0: a chunk is all in or all out).
+__device__ __forceinline__ void vec_store_block(const GemmParams &p, uint32_t stg, int row0,
+                                                int col0, int lane) {
+  const int col = col0 + 4 * (lane & 7);
+#pragma unroll 1
+  for (int i = 0; i < 8; ++i) {  // (not unrolled: the epilogue's registers hold the sums)
+    const int r = 4 * i + (lane >> 3);
+    const float4 v =
+        ptx::ld_shared_v4(stg + uint32_t(r) * 128 + uint32_t(((lane & 7) ^ (r & 7)) * 16));
+    if (row0 + r < p.M && col < p.N) {
+      const int64_t off = int64_t(row0 + r) * p.ldc + col;
+      if (p.st_mode == kStoreMulticast) {
+        ptx::multimem_st_v4(p.vdst[0] + off, v);
+      } else {
+        for (int d = 0; d < p.n_cdst; ++d) ptx::st_global_v4(p.vdst[d] + off, v);
+      }
+    }
   }
 }
 
@@ -1017,6 +1048,13 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
             fix_b_block(p, stgf, crow0 + lane, ccol0 + 32 * c, lane);
           else if (cnt > 0)
             fix_b_list(p, stgf, crow0 + lane, strip, cnt, lane);
+        }
+        if (p.st_mode != kStoreTma) {
+          __syncwarp();  // every lane's staged row (and the B-side fix) is in place
+          vec_store_block(p, stg, crow0, ccol0 + 32 * c, lane);
+          __syncwarp();  // all reads done before the block is overwritten (or TMA-loaded into)
+          ptx::fence_proxy_async_smem();
+          continue;
         }
         ptx::fence_proxy_async_smem();
         __syncwarp();
@@ -1886,7 +1924,22 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   p.n_kb = int((K + bk - 1) / bk);
   int pk = promote_kblocks < 0 ? default_promote_kblocks(terms) : promote_kblocks;
   p.p_kb = (pk == 0 || pk > p.n_kb) ? p.n_kb : pk;
-  const bool plain = !p.accumulate && !p.load_c && ex->n_peer_c == 0;
+  // C's store mode: TMA, or 16-byte stores (unicast / one multicast store per piece)
+  p.st_mode = ex->mc_c ? kStoreMulticast : ex->vec_store ? kStoreVec : kStoreTma;
+  for (int i = 0; i < kMaxCDst; ++i) p.vdst[i] = nullptr;
+  if (p.st_mode != kStoreTma) {
+    if (p.accumulate || (N & 3) || (ldc & 3) || (reinterpret_cast<uintptr_t>(C) & 15) ||
+        (ex->mc_c && (ex->n_peer_c || (reinterpret_cast<uintptr_t>(ex->mc_c) & 15))))
+      return cudaErrorInvalidValue;
+    p.vdst[0] = ex->mc_c ? ex->mc_c : C;
+    for (int i = 0; i < ex->n_peer_c; ++i) {
+      if (reinterpret_cast<uintptr_t>(ex->peer_c[i]) & 15) return cudaErrorInvalidValue;
+      p.vdst[1 + i] = ex->peer_c[i];
+    }
+  }
+  // (vector / multicast stores have no reduce-add: never the kSplitReduce K-split)
+  const bool plain =
+      !p.accumulate && !p.load_c && ex->n_peer_c == 0 && p.st_mode == kStoreTma;
   const GemmSchedule sch = gemm_schedule(M, N, K, num_sms, cg, plain, p.p_kb, bk);
   p.m_tiles = sch.m_tiles;
   p.n_tiles = sch.n_tiles;

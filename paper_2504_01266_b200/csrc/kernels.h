@@ -120,6 +120,15 @@ struct GemmExtra {
   int defer_fix = 0;
   // $GIGA_TRACE: 2 x (grid size) slots; each CTA writes %globaltimer at its start and its end
   uint64_t *cta_ns = nullptr;
+  // How the epilogue writes the staged C blocks:
+  //   mc_c != nullptr: the NVLink multicast address of the same rows as C (C and every peer's
+  //     C_full bound into one cuMulticastCreate team): each 16-byte piece is written ONCE with
+  //     multimem.st and the switch replicates it into every member, C included (peer_c must
+  //     be empty). Needs N % 4 == 0 and 16-byte aligned C; no accumulate.
+  //   vec_store = 1: C and peer_c written with 16-byte st.global stores from the staging tile
+  //     (the same addressing as the multicast mode, unicast; no accumulate) instead of TMA.
+  float *mc_c = nullptr;
+  int vec_store = 0;
 };
 // One thread writes %globaltimer (ns) to *slot when `st` reaches it (trace stamps).
 cudaError_t launch_stamp(uint64_t *slot, cudaStream_t st);

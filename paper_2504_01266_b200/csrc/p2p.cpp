@@ -38,8 +38,18 @@ static GemmExtra chunk_extra(const GemmExtra &ex, int c, int pb) {
   if (!last) {
     e.peer_c = nullptr;
     e.n_peer_c = 0;
+    e.mc_c = nullptr;  // earlier chunks stay local (TMA stores / reduce-adds)
+    e.vec_store = 0;
   }
   return e;
+}
+
+// $GIGA_P2P_STORE=vec: the unicast fused gather with 16-byte st.global stores from the
+// epilogue instead of TMA stores -- the multicast mode's code path with one store per peer
+// (how that path is exercised where no multicast team can be made).
+static bool p2p_vec_store() {
+  const char *e = getenv("GIGA_P2P_STORE");
+  return e && strcmp(e, "vec") == 0;
 }
 
 bool transport_p2p() {
@@ -98,21 +108,27 @@ int run_p2p(std::vector<Part> &parts, int64_t M, int64_t N, int64_t K, bool gath
       TRY(tr[i].mark("bcast", p.d->comm, i > 0 ? 4.0 * double(cnt) : 0.0));
     }
   }
-  // 2. GEMMs over the K-chunks; every tile also goes to the peers' C_full
+  // 2. GEMMs over the K-chunks; every tile also goes to the peers' C_full: through the
+  // multicast team address when the C_full buffers are one giga_mc_alloc team (one store per
+  // piece, the switch writes every copy), else one store per peer
   GemmExtra ex;
   ex.lda = K;
   ex.ldb = N;
+  float *const mc = gather ? mc_address(parts, M, N) : nullptr;
+  for (auto &t : tr) t.meta("gather", mc ? 2 : (gather ? 1 : 0));
   for (auto &p : parts) {
     CK(cudaSetDevice(p.d->dev));
     int64_t r0, rows;
     partition_rows(M, world, p.rank, &r0, &rows);
     float *peer[kMaxCDst];
     int np = 0;
-    if (gather)
+    if (gather && !mc)
       for (auto &q : parts)
         if (&q != &p) peer[np++] = q.C + r0 * N;
     ex.peer_c = peer;
     ex.n_peer_c = np;
+    ex.mc_c = mc ? mc + r0 * N : nullptr;
+    ex.vec_store = (gather && !mc && p2p_vec_store()) ? 1 : 0;
     float *Cr = gather ? p.C + r0 * N : p.C_rows;
     for (int c = 0; c < plan.pb; ++c) {
       const int64_t Kc = plan.kb[c + 1] - plan.kb[c];
@@ -247,16 +263,24 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
     TRY(tr.mark("b_chunk", d.comm));
     if (r < world - 1) TRY(write_flag(d.comm, flag_ready(x.peerF[r + 1], c), s));
   }
-  // GEMMs over the K-chunks, every tile also stored into the peers' C_full
+  // GEMMs over the K-chunks, every tile also stored into the peers' C_full (one multicast
+  // store per piece when C_full is this rank's team buffer, else one store per peer)
+  float *const mc = rank_mc_address(C, M, N);
+  if (rank_mc_buffer(C) && !mc)
+    return fail(GIGA_ERR_INVALID_ARG, "p2p transport: M x N exceeds the multicast C_full");
   float *peer[kMaxCDst];
   int np = 0;
-  for (int q = 0; q < world; ++q)
-    if (q != r) peer[np++] = x.peerC[q] + r0 * N;
+  if (!mc)
+    for (int q = 0; q < world; ++q)
+      if (q != r) peer[np++] = x.peerC[q] + r0 * N;
   GemmExtra ex;
   ex.lda = K;
   ex.ldb = N;
   ex.peer_c = peer;
   ex.n_peer_c = np;
+  ex.mc_c = mc ? mc + r0 * N : nullptr;
+  ex.vec_store = (!mc && p2p_vec_store()) ? 1 : 0;
+  tr.meta("gather", mc ? 2 : 1);
   for (int c = 0; c < plan.pb; ++c) {
     const int64_t Kc = plan.kb[c + 1] - plan.kb[c];
     CK(cudaStreamWaitEvent(st, d.ev_kchunk[c], 0));

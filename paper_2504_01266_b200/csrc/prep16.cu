@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__
 struct PeerC {
   float *p[kMaxCDst - 1];
   int n;
+  float *mc;  // non-null: the multicast address of C's rows (C and every peer in one store)
 };
 constexpr int kFixCap = 1024;  // exceptions staged in shared memory per pass
 
@@ -412,9 +413,13 @@ __global__ void __launch_bounds__(256) fix16_a_kernel(
           const float4 c = *reinterpret_cast<const float4 *>(crow + j);
           const float4 v = make_float4(float(double(c.x) + t0), float(double(c.y) + t1),
                                        float(double(c.z) + t2), float(double(c.w) + t3));
-          *reinterpret_cast<float4 *>(crow + j) = v;
-          for (int pi = 0; pi < peers.n; ++pi)
-            *reinterpret_cast<float4 *>(peers.p[pi] + int64_t(i) * ldc + j) = v;
+          if (peers.mc) {  // the switch writes it into C and every peer's copy
+            ptx::multimem_st_v4(peers.mc + int64_t(i) * ldc + j, v);
+          } else {
+            *reinterpret_cast<float4 *>(crow + j) = v;
+            for (int pi = 0; pi < peers.n; ++pi)
+              *reinterpret_cast<float4 *>(peers.p[pi] + int64_t(i) * ldc + j) = v;
+          }
         }
         __syncthreads();  // the next pass overwrites the staged exceptions
       }
@@ -487,6 +492,7 @@ cudaError_t launch_fix16(const float *A, int64_t lda, const float *B, int64_t ld
   PeerC peers;
   peers.n = ex->n_peer_c;
   for (int i = 0; i < peers.n; ++i) peers.p[i] = ex->peer_c[i];
+  peers.mc = ex->mc_c;
   // grid-strided rows / strips: blocks of rows or strips without exceptions only read a flag
   const int64_t cap = int64_t(sms_for_grids()) * 4;
   // row windows x column chunks (each flagged row is fixed by gridDim.y blocks side by side)

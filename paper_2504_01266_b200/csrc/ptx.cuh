@@ -114,6 +114,20 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, fl
                : "memory");
 }
 
+// 16-byte global store (generic proxy) -- the epilogue's vector-store mode (unicast peers).
+__device__ __forceinline__ void st_global_v4(float *p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+// 16-byte store to an NVLink multicast address (cuMulticastCreate team): the NVSwitch
+// replicates it into every member GPU's bound memory (one egress from this GPU).
+__device__ __forceinline__ void multimem_st_v4(float *p, float4 v) {
+  asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 __device__ __forceinline__ void st_shared_v4_u32(uint32_t addr, uint32_t a, uint32_t b,
                                                  uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),

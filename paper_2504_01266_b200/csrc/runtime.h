@@ -290,6 +290,12 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
 int p2p_dot_allreduce(DevCtx &d, cudaStream_t st, double *result);
 void p2p_release();
 
+// ---- mcast.cpp: NVLink multicast teams (fused gather with one store per piece) -------------
+float *mc_address(const std::vector<Part> &parts, int64_t M, int64_t N);
+float *rank_mc_address(const float *C_full, int64_t M, int64_t N);
+bool rank_mc_buffer(const float *p);
+void mc_release_all();
+
 // ---- host_pipeline.cpp ---------------------------------------------------------------------
 int host_pipeline(DevCtx &d, const float *A, const float *B, float *C, int64_t M, int64_t N,
                   int64_t K);

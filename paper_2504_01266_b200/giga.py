@@ -28,9 +28,11 @@ EXPORTS = (
     "giga_timing_enable", "giga_timing_reset", "giga_timing_read", "giga_pipeline_plan",
     "giga_plan_block", "giga_dot", "giga_l2norm", "giga_dot_rank", "giga_init_devices",
     "giga_rank_p2p_export", "giga_rank_p2p_import", "giga_host_plan", "giga_gemm_schedule",
-    "giga_rank_compute_only", "giga_product_scheme",
+    "giga_rank_compute_only", "giga_product_scheme", "giga_gemm_gather_ex", "giga_mc_alloc",
+    "giga_mc_free", "giga_rank_mc_create", "giga_rank_mc_join", "giga_rank_mc_bind",
 )
 P2P_BLOB_BYTES = 256
+MC_BLOB_BYTES = 64
 
 
 class GigaError(RuntimeError):
@@ -86,6 +88,12 @@ def _load():
         "giga_gemm_schedule": ([i64, i64, i64, i32, P64], i32),
         "giga_product_scheme": ([i64, i64, i64, ctypes.POINTER(ctypes.c_int)], i32),
         "giga_rank_compute_only": ([p, p, p, i64, i64, i64, i32, i32, p], i32),
+        "giga_gemm_gather_ex": ([p, p, p, p, i32, i64, i64, i64, i64, i32, i32, p], i32),
+        "giga_mc_alloc": ([i32, ctypes.c_size_t, p], i32),
+        "giga_mc_free": ([p], i32),
+        "giga_rank_mc_create": ([ctypes.c_size_t, p], i32),
+        "giga_rank_mc_join": ([p], i32),
+        "giga_rank_mc_bind": ([p], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -198,6 +206,72 @@ def p2p_import(blobs):
     raw = b"".join(blobs)
     buf = (ctypes.c_uint8 * len(raw)).from_buffer_copy(raw)
     _check(lib.giga_rank_p2p_import(ctypes.cast(buf, ctypes.c_void_p), len(blobs)))
+
+
+class _DevBuf:
+    """A library-owned device buffer seen through __cuda_array_interface__ (torch.as_tensor
+    wraps it without a copy)."""
+
+    def __init__(self, ptr: int, numel: int):
+        self.__cuda_array_interface__ = {"shape": (numel,), "typestr": "<f4",
+                                         "data": (ptr, False), "version": 3}
+
+
+def as_float_tensor(ptr: int, numel: int, device):
+    """A float32 torch view of `numel` floats at device pointer `ptr` on `device`."""
+    import torch
+    with torch.cuda.device(device):
+        return torch.as_tensor(_DevBuf(ptr, numel), device=device)
+
+
+def mc_alloc(ngpus: int, nbytes: int):
+    """giga_mc_alloc: device pointers (ints) of ngpus C_full buffers bound into one NVLink
+    multicast team (GigaError GIGA_ERR_UNSUPPORTED where the driver has no multicast)."""
+    out = (ctypes.c_void_p * ngpus)()
+    _check(lib.giga_mc_alloc(ngpus, nbytes, ctypes.cast(out, ctypes.c_void_p)))
+    return [int(x) for x in out]
+
+
+def mc_free(C_full0: int):
+    _check(lib.giga_mc_free(ctypes.c_void_p(C_full0)))
+
+
+def rank_mc_alloc(nbytes: int, group=None) -> int:
+    """The rank API's multicast C_full (giga_rank_mc_create / _join / _bind, include/giga.h):
+    rank 0's blob is broadcast and every phase ends in a barrier over torch.distributed.
+    Collective: every rank calls it, and every rank raises if any rank failed."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    blob = (ctypes.c_uint8 * MC_BLOB_BYTES)()
+    rc = 0
+    if rank == 0:
+        rc = lib.giga_rank_mc_create(nbytes, ctypes.cast(blob, ctypes.c_void_p))
+    msg = [(rc, last_error() if rc else "", bytes(blob))]
+    dist.broadcast_object_list(msg, src=0, group=group)
+    rc0, err0, raw = msg[0]
+    if rc0:
+        raise GigaError(rc0, f"rank 0: {err0}")
+    buf = (ctypes.c_uint8 * MC_BLOB_BYTES).from_buffer_copy(raw)
+    for phase in ("join", "bind"):
+        ptr = ctypes.c_void_p()
+        rc = (lib.giga_rank_mc_join(ctypes.cast(buf, ctypes.c_void_p)) if phase == "join"
+              else lib.giga_rank_mc_bind(ctypes.byref(ptr)))
+        codes = [None] * dist.get_world_size(group)
+        dist.all_gather_object(codes, (rc, last_error() if rc else ""), group=group)
+        for q, (c, e) in enumerate(codes):
+            if c:
+                raise GigaError(c, f"rank {q} ({phase}): {e}")
+    return int(ptr.value)
+
+
+def gemm_gather_ex(A, B, C, peers, M: int, N: int, K: int, ldc=None, terms=0, store_mode=0,
+                   stream=None):
+    """giga_gemm_gather_ex: C (and every peer buffer) = A * B through the fused-gather
+    epilogue with store_mode 0 TMA / 1 st.global / 2 multimem.st."""
+    arr = (ctypes.c_void_p * max(1, len(peers)))(*[_ptr(q) for q in peers])
+    _check(lib.giga_gemm_gather_ex(_ptr(A), _ptr(B), _ptr(C), ctypes.cast(arr, ctypes.c_void_p),
+                                   len(peers), M, N, K, N if ldc is None else ldc, terms,
+                                   store_mode, _stream(stream)))
 
 
 def matmul_rank(A_shard, B, C_full, M: int, N: int, K: int, stream=None):

@@ -70,6 +70,18 @@ def test_not_initialized_paths(giga):
     with pytest.raises(giga.GigaError) as e:
         giga.matmul_rank(a, a, a, 2, 2, 2)
     assert e.value.status == "GIGA_ERR_NOT_INITIALIZED"
+    # multicast teams (N4) need an initialised library; no driver call is made before that
+    with pytest.raises(giga.GigaError) as e:
+        giga.mc_alloc(1, 1 << 20)
+    assert e.value.status == "GIGA_ERR_NOT_INITIALIZED"
+    import ctypes
+    blob = (ctypes.c_uint8 * giga.MC_BLOB_BYTES)()
+    assert giga.lib.giga_rank_mc_create(1 << 20, blob) == -2
+    assert giga.lib.giga_rank_mc_join(blob) == -2
+    assert giga.lib.giga_rank_mc_bind(ctypes.byref(ctypes.c_void_p())) == -2
+    with pytest.raises(giga.GigaError) as e:
+        giga.mc_free(4096)
+    assert e.value.status == "GIGA_ERR_INVALID_ARG"
     giga.finalize()  # finalize when not initialised is OK
 
 
