@@ -994,16 +994,18 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
       const int crow0 = mb * T::TILE_M + int(rank) * BM + quad * 32;
       const int ccol0 = nb * BN + half * 128;
       if (p.ea) {
-        // 3xFP16: undo the power-of-two operand scales (exact; ldexpf rounds only a result
-        // that leaves the normal range). ea / eb are padded to whole tiles.
+        // 3xFP16: undo the power-of-two operand scales (pow2_scale: exact for every normal
+        // result, two multiplications). ea / eb are padded to whole tiles.
+        // (lane l holds the exponents of columns 4l..4l+3; the warp shares them by shuffles,
+        // which keeps 4 registers live instead of 128 hoisted loads)
         const int ei = p.ea[crow0 + lane];
+        const int4 fl = *reinterpret_cast<const int4 *>(p.eb + ccol0 + 4 * lane);
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
-          const int4 f = *reinterpret_cast<const int4 *>(p.eb + ccol0 + 4 * q);
-          sum[4 * q] = ldexpf(sum[4 * q], ei + f.x);
-          sum[4 * q + 1] = ldexpf(sum[4 * q + 1], ei + f.y);
-          sum[4 * q + 2] = ldexpf(sum[4 * q + 2], ei + f.z);
-          sum[4 * q + 3] = ldexpf(sum[4 * q + 3], ei + f.w);
+          sum[4 * q] = pow2_scale(sum[4 * q], ei + __shfl_sync(0xffffffffu, fl.x, q));
+          sum[4 * q + 1] = pow2_scale(sum[4 * q + 1], ei + __shfl_sync(0xffffffffu, fl.y, q));
+          sum[4 * q + 2] = pow2_scale(sum[4 * q + 2], ei + __shfl_sync(0xffffffffu, fl.z, q));
+          sum[4 * q + 3] = pow2_scale(sum[4 * q + 3], ei + __shfl_sync(0xffffffffu, fl.w, q));
         }
       }
 #pragma unroll

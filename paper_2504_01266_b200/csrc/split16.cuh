@@ -62,6 +62,21 @@ __device__ __forceinline__ void mark_exception(unsigned *bits, int64_t word, uns
   *reinterpret_cast<volatile int *>(flag) = 1;
 }
 
+// x 2^e in the GEMM epilogue (e = ea[i] + eb[j], in [-328, 224] by scale_exp's range): two
+// multiplications by normal powers of two, 2^e1 with e1 = clamp(e, -126, 127), then 2^(e - e1)
+// (clamped). Exact whenever x 2^e is a normal float (then no intermediate leaves the normal
+// range) -- the bits ldexpf gives -- and a single rounding, as ldexpf's, whenever e1 = e. Only a
+// subnormal result with e < -126 can differ from ldexpf, by the second rounding (1 subnormal
+// ulp; outside the contract's normal range, reading R16). Below e = -252 both give 0:
+// |x| < K 2^32 < 2^63. ~8 instructions where ldexpf took ~45 (measured: the epilogue's
+// scaling was a third of the epilogue warps' samples at K = 1024).
+__device__ __forceinline__ float pow2_scale(float x, int e) {
+  const int e1 = max(-126, min(127, e));
+  const int e2 = max(-126, min(127, e - e1));
+  return __fmul_rn(__fmul_rn(x, __int_as_float((e1 + 127) << 23)),
+                   __int_as_float((e2 + 127) << 23));
+}
+
 __device__ __forceinline__ double rep16(uint16_t h, uint16_t l, int e) {
   return ldexp(double(__half2float(__ushort_as_half(h))) + double(__half2float(__ushort_as_half(l))), e);
 }

@@ -81,3 +81,37 @@ def test_product_error_of_the_three_terms():
     exact = a.astype(np.float64) * b.astype(np.float64)
     rel = np.abs(got - exact) / np.abs(exact)
     assert rel.max() <= 3 * 2.0 ** -22
+
+
+def pow2_scale(x, e):
+    """Emulation of the epilogue's x 2^e (split16.cuh pow2_scale): two float32 multiplications
+    by normal powers of two, 2^clamp(e, -126, 127) then 2^clamp(e - e1, -126, 127)."""
+    e1 = np.clip(e, -126, 127)
+    e2 = np.clip(e - e1, -126, 127)
+    f1 = np.ldexp(np.float32(1), e1).astype(np.float32)
+    f2 = np.ldexp(np.float32(1), e2).astype(np.float32)
+    with np.errstate(over="ignore", under="ignore"):
+        return (x.astype(np.float32) * f1).astype(np.float32) * f2
+
+
+def test_pow2_scale_matches_ldexp_for_normal_results():
+    """The epilogue's scaling equals the correctly rounded x 2^e (numpy's float64 ldexp, then
+    one rounding to float32) for every result in float32's normal range, over the exponent
+    range scale_exp produces (ea + eb in [-328, 224]) and sums |x| < 2^63; and whenever
+    e is itself in [-126, 127] (a single rounding, subnormal results included)."""
+    rng = np.random.default_rng(16)
+    n = 400000
+    x = (rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-149, 63, n)).astype(np.float32)
+    e = rng.integers(-328, 225, n)
+    got = pow2_scale(x, e)
+    with np.errstate(over="ignore", under="ignore"):
+        want = np.ldexp(x.astype(np.float64), e).astype(np.float32)
+    normal = np.abs(want) >= np.float32(2.0 ** -126)
+    single = (e >= -126) & (e <= 127)
+    sel = normal | single | (want == 0)
+    assert sel.sum() > n // 2
+    assert np.array_equal(got[sel].view(np.uint32), want[sel].view(np.uint32))
+    # outside: a subnormal result reached through two roundings, within one subnormal ulp
+    rest = ~sel
+    assert np.all(np.abs(got[rest].astype(np.float64) - want[rest].astype(np.float64))
+                  <= 2.0 ** -149)
