@@ -59,7 +59,7 @@
  *   GIGA_TRACE           1: print a JSON timeline of each pipelined call on stderr (CUDA-event
  *                        times, transfer GB/s, p2p: %globaltimer copy / GEMM-CTA intervals) [0]
  *   GIGA_HOST_H2D_GBS, GIGA_HOST_D2H_GBS, GIGA_HOST_GEMM_TFLOPS, GIGA_HOST_GEMM4_TFLOPS
- *                        rates of the host-path schedule model [50, 50, 250, 400 (3xFP16)]
+ *                        rates of the host-path schedule model [50, 50, 250, 440 (3xFP16)]
  *   GIGA_HOST_PLAN       "Me,P,Q": force that host-path schedule (measurements) [planned]
  *   GIGA_SCHEME          3xtf32 | tf32bf16 | 3xfp16: force the product scheme (once) [by shape]
  *   GIGA_HI_RN, GIGA_A_PRE, GIGA_B_PRE  TF32 + BF16: 0 = truncated hi / A' / B' built on chip

@@ -121,8 +121,9 @@ struct GemmParams {
   // issued (the producers' wave barrier), sched[2] = CTAs finished. nullptr: static
   // round-robin units, no wave barrier (no counters could be had, e.g. inside a capture).
   unsigned *sched;
-  int wave_sync;  // 1: a producer starts unit u's loads once every unit of the previous waves
-                  // (u / clusters) has been issued by all its CTAs
+  int wave_sync;  // s >= 1: a producer starts unit u's loads once every unit of waves
+                  // <= wave(u) - s (wave = u / clusters) has been issued by all its CTAs
+                  // (s = 1: every earlier wave); 0: no barrier
   int n_cdst;     // C destinations in CMaps (1 + peers when the gather is fused)
   // how the epilogue writes C: kStoreTma (CMaps), kStoreVec (16-byte st.global to vdst[0..
   // n_cdst)), kStoreMulticast (multimem.st to the team address vdst[0]; n_cdst = 1)
@@ -616,7 +617,7 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
         }
         if (u < 0) break;
         const int wave = u / num_clusters;
-        if (p.sched && p.wave_sync && wave > 0) {
+        if (p.sched && p.wave_sync && wave >= p.wave_sync) {
           // Wave barrier among the producers: start loading unit u only when every unit of
           // the earlier waves has been issued by all its CTAs, so the clusters sharing A / B
           // panels stay within about one tile of each other and hit in L2 (unsynchronised,
@@ -624,7 +625,8 @@ __global__ void __launch_bounds__(cfg::NUM_THREADS, 1)
           // DRAM reads at 16384^3). Deadlock-free: units are claimed in increasing order, only
           // by running clusters, and the loads of a claimed unit wait for nothing but earlier
           // units. The 2 ms cap only bounds a locality hint (never needed for correctness).
-          const uint32_t target = uint32_t(CG) * uint32_t(wave) * uint32_t(num_clusters);
+          const uint32_t target =
+              uint32_t(CG) * uint32_t(wave + 1 - p.wave_sync) * uint32_t(num_clusters);
           const uint64_t t_start = ptx::globaltimer_ns();
           while (ptx::ld_acquire_gpu(&p.sched[1]) < target &&
                  ptx::globaltimer_ns() - t_start < 2000000ull)
@@ -1256,17 +1258,16 @@ int product_terms(const float *A_lo, int64_t M, int64_t N, int64_t K) {
   if (forced) return forced;
   const double mnk = double(M) * double(N) * double(K);
   // measured crossover, operand preparation and exception fixes included
-  // (profiles/r02_scheme_crossover*.jsonl, scripts/scheme_crossover.py, bench.py): 3xFP16 wins
-  // from 8192 x 8192 x 2048 (+10%), 2048 x 16384^2 (+5%) and 65536 x 2048^2 (+21%) up to
-  // +52-58% at 16384^3 and 32768^3, and on 16384 x 32768 x 1024 (+8%); it loses where the
-  // preparation (~12 B per element of A and B) is not amortised or the tiles are short:
-  // 4096^3 (-9%), 2048 x 4096^2, the tall 262144 x 1024^2 (-13%: 227 vs 262 in bench.py),
-  // K = 576 (-19%)
-  if (M >= 2048 && mnk >= 0x1p37 && ((K >= 2048 && N >= 2048) || (K >= 1024 && N >= 8192)))
-    return 4;
-  // below that, TF32 + BF16 only ties 3xTF32 (16384 x 32768 x 576: 219 vs 217; r01: it won
-  // 3-10% on 16384 x 32768 x (576..1792), the host schedule's K-chunks, before 3xFP16)
-  return (M >= 4096 && N >= 8192 && K >= 512 && mnk >= 0x1p38) ? 2 : 3;
+  // (profiles/r02_scheme_crossover_e.jsonl, scripts/scheme_crossover.py), after the epilogue's
+  // scaling became two multiplications (pow2_scale): 3xFP16 wins from 2^35 multiply-adds with
+  // K >= 512 -- 4096^3 +28%, 2048 x 4096^2 +10%, 4096^2 x 2048 +16%, 32768 x 1024^2 +3%, the
+  // tall 262144 x 1024^2 +23%, 16384 x 32768 x 512 +49%, up to +82% at 16384^3 -- and loses
+  // below (2048^3: -21%, 1024^3: -40%, where B's preparation and the per-launch costs are not
+  // amortised); at K = 256 the three schemes tie
+  if (M >= 2048 && N >= 1024 && K >= 512 && mnk >= 0x1p35) return 4;
+  // (TF32 + BF16 is no longer chosen by shape -- 3xFP16 covers its old range; $GIGA_SCHEME
+  // forces it)
+  return 3;
 }
 
 // CTA-group size: 2 (CTA pairs) unless the problem has fewer 256-row tiles than SM pairs,
@@ -1990,9 +1991,11 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
     if (e != cudaSuccess) return e;
   }
   p.num_units = p.first_split + (p.num_tiles - p.first_split) * p.split_s;
-  static const bool wave_env = [] {  // producers' per-wave barrier; $GIGA_WAVE_SYNC=0 disables
+  // producers' per-wave barrier: $GIGA_WAVE_SYNC=0 disables it, s >= 1 lets a producer run
+  // s - 1 waves ahead of the slowest cluster [1]
+  static const int wave_env = [] {
     const char *e = getenv("GIGA_WAVE_SYNC");
-    return !(e && *e == '0');
+    return (e && *e >= '0' && *e <= '9') ? atoi(e) : 1;
   }();
   static const bool dyn_env = [] {  // $GIGA_DYNAMIC_SCHED=0: static round-robin units
     const char *e = getenv("GIGA_DYNAMIC_SCHED");
@@ -2001,7 +2004,7 @@ cudaError_t launch_gemm_3xtf32(const float *A, const float *A_lo, const float *B
   // the launch's dynamic-schedule counters (per device and stream: concurrent launches on
   // other streams have their own); none inside a capture that has not seen this stream yet
   if (dyn_env) p.sched = sched_counters(st);
-  p.wave_sync = (wave_env && p.num_units > nclu) ? 1 : 0;
+  p.wave_sync = p.num_units > nclu ? wave_env : 0;
   cudaError_t e = cudaSuccess;
 
   if (cg == 1) {

@@ -40,8 +40,9 @@ double gemm_time(int64_t m, int64_t n, int64_t k, const HostRates &r, bool accum
   if (m <= 0 || n <= 0 || k <= 0) return 0.0;
   const int terms = product_terms(nullptr, std::max(m, scheme_rows), n, k);
   // 3xFP16's short-K launches run below its full rate (shorter tiles, per-tile epilogue and
-  // preparation weigh more): measured ~310-340 TFLOP/s at K = 2048, ~250 at K = 1024
-  const double rate = terms == 4 ? r.gemm4 * double(k) / double(k + 512)
+  // preparation weigh more): measured on 8192 / 16384 x 32768 chunks ~310-340 TFLOP/s at
+  // K = 512, ~370-380 at K = 1024, ~400-440 at K = 2048 (profiles/r02_chunk_rate_sweep_b.jsonl)
+  const double rate = terms == 4 ? r.gemm4 * double(k) / double(k + 256)
                       : terms == 2 ? r.gemm2
                                    : r.gemm;
   const int64_t tiles = ((m + 255) / 256) * ((n + 255) / 256);

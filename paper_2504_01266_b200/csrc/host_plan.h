@@ -21,7 +21,7 @@ struct HostRates {
   double d2h = 50e9;     // bytes/s device -> host
   // logical fp32-accurate flop/s of the shard GEMM by the scheme a launch runs
   // (giga_product_scheme; measured): 3xTF32, TF32 + BF16, 3xFP16
-  double gemm = 250e12, gemm2 = 265e12, gemm4 = 400e12;
+  double gemm = 250e12, gemm2 = 265e12, gemm4 = 440e12;
   double prep = 5e12;    // bytes/s of the operand preparation (~12 B per element, HBM-bound)
   int clusters = 74;     // concurrent 256 x 256 tiles (CTA pairs on 148 SMs)
 };

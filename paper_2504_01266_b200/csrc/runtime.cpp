@@ -402,15 +402,16 @@ static bool geometric_bounds(int64_t total, int n, double ratio, int64_t align,
 // Modelled time of one K-chunk GEMM launch over `rows` rows, operand preparation included:
 // the scheme product_terms picks for it at that scheme's rate for this K -- short chunks pay
 // the per-tile fill / epilogue and, for 3xFP16, the preparation of the whole Kc x N chunk of B
-// (profiles/r02_chunk_rate_sweep.jsonl: 3xFP16 ~430 k / (k + 900) TFLOP/s, 3xTF32
-// ~260 k / (k + 64), TF32 + BF16 ~255 k / (k + 128)) -- times the last-wave quantisation of
+// (profiles/r02_chunk_rate_sweep_b.jsonl, after the 3xFP16 epilogue fix: 3xFP16
+// ~460 k / (k + 530) TFLOP/s, 3xTF32 ~260 k / (k + 64), TF32 + BF16 ~255 k / (k + 128);
+// r02_chunk_rate_sweep.jsonl had 3xFP16 at ~430 k / (k + 900)) -- times the last-wave quantisation of
 // its 256 x 256 pair tiles on the 70 pairs the pipeline leaves to the GEMM, plus a launch
 // cost O.
 static double chunk_gemm_time(int64_t rows, int64_t N, int64_t Kc, double O) {
   if (rows <= 0 || Kc <= 0) return 0.0;
   const int t = product_terms(nullptr, rows, N, Kc);
   const double k = double(Kc);
-  const double rate = t == 4 ? 430e12 * k / (k + 900.0)
+  const double rate = t == 4 ? 460e12 * k / (k + 530.0)
                       : t == 2 ? 255e12 * k / (k + 128.0)
                                : 260e12 * k / (k + 64.0);
   const double waves = double((rows + 255) / 256) * double((N + 255) / 256) / 70.0;

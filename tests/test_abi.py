@@ -97,18 +97,18 @@ def test_init_without_gpu_reports_no_device(giga):
 
 def test_product_scheme_selection():
     """giga_product_scheme (host-only): 3xFP16 where its per-launch operand preparation is
-    amortised, TF32 + BF16 on the long, shallow launches just below that, 3xTF32 for the small
-    and skinny configs (profiles/r02_scheme_crossover*.jsonl)."""
+    amortised (>= 2^35 multiply-adds, K >= 512), 3xTF32 for the small, shallow and thin configs
+    (profiles/r02_scheme_crossover_e.jsonl). TF32 + BF16 is forced only."""
     from paper_2504_01266_b200 import giga
     for shape in [(16384, 16384, 16384), (32768, 32768, 32768), (4096, 32768, 32768),
                   (8192, 8192, 2048), (2048, 16384, 16384), (16384, 32768, 1024),
-                  (65536, 2048, 2048), (8192, 16384, 1024)]:
+                  (65536, 2048, 2048), (8192, 16384, 1024), (4096, 4096, 4096),
+                  (32768, 1024, 1024), (262144, 1024, 1024), (2048, 4096, 4096),
+                  (16384, 32768, 576), (32768, 16384, 1000), (65536, 4096, 512),
+                  (4096, 32768, 768)]:
         assert giga.product_scheme(*shape) == 4, shape
-    for shape in [(16384, 32768, 576), (32768, 16384, 1000)]:
-        assert giga.product_scheme(*shape) == 2, shape
-    for shape in [(512, 512, 512), (4096, 4096, 4096), (32768, 1024, 1024), (262144, 1024, 1024),
-                  (2048, 4096, 4096), (16384, 16384, 256), (65536, 4096, 512),
-                  (1024, 32768, 32768), (4096, 32768, 768)]:
+    for shape in [(512, 512, 512), (2048, 2048, 2048), (16384, 16384, 256),
+                  (1024, 32768, 32768), (4096, 4096, 1024), (32768, 512, 2048)]:
         assert giga.product_scheme(*shape) == 3, shape
     with pytest.raises(Exception):
         giga.product_scheme(0, 4, 4)

@@ -39,8 +39,9 @@ def _common(d, steps, warmup):
 
 
 def test_bench_line_3xtf32_workload():
+    # (c2 runs 3xFP16 by the product rule since the epilogue fix: the scheme is forced)
     d = _line(["--config", "c2_4096", "--steps", "3", "--warmup", "3", "--e2e-steps", "2",
-               "--no-cpu-baseline"])
+               "--no-cpu-baseline"], env={"GIGA_SCHEME": "3xtf32"})
     _common(d, 3, 3)
     assert d["roofline"]["scheme"] == "3xTF32" and "feed" not in d["roofline"]
     assert d["gpu_launches"] == 3  # one GEMM launch per step, no preparation

@@ -14,7 +14,7 @@ import pytest
 from paper_2504_01266_b200 import giga
 
 H2D = D2H = 50e9
-RATE = {3: 250e12, 2: 265e12, 4: 400e12}  # logical TFLOP/s per scheme (host_plan.h)
+RATE = {3: 250e12, 2: 265e12, 4: 440e12}  # logical TFLOP/s per scheme (host_plan.h)
 PREP = 5e12  # bytes/s of the TF32 + BF16 / 3xFP16 operand preparation, ~12 B per element
 CLUSTERS = 74
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -27,7 +27,7 @@ def gemm_t(m, n, k, accumulate=False, scheme_rows=0, b_prepared=False):
         return 0.0
     terms = giga.product_scheme(max(m, scheme_rows), n, k)
     tiles = math.ceil(m / 256) * math.ceil(n / 256)
-    rate = RATE[terms] * (k / (k + 512) if terms == 4 else 1.0)  # 3xFP16's short-K rate
+    rate = RATE[terms] * (k / (k + 256) if terms == 4 else 1.0)  # 3xFP16's short-K rate
     wave = 2e-6 + 2 * 256 * 256 * k / (rate / CLUSTERS)
     prep = 12.0 * (m * k + (0 if b_prepared else k * n)) / PREP if terms in (2, 4) else 0.0
     return 10e-6 + prep + math.ceil(tiles / CLUSTERS) * wave * (1.1 if accumulate else 1.0)
