@@ -232,6 +232,10 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
                 "giga_rank_p2p_export");
   if ((K % 4) || (N % 4) || !aligned16(A) || !aligned16(B) || !aligned16(C))
     return fail(GIGA_ERR_UNSUPPORTED, "p2p transport needs K %% 4 == N %% 4 == 0, aligned");
+  // the multicast team address of C_full's rows (checked before the call takes a number)
+  float *const mc = rank_mc_address(C, M, N);
+  if (rank_mc_buffer(C) && !mc)
+    return fail(GIGA_ERR_INVALID_ARG, "p2p transport: M x N exceeds the multicast C_full");
   const uint32_t s = ++x.step;
   const Plan plan = make_plan(M, N, K, world, true);
   int64_t r0, rows;
@@ -265,9 +269,6 @@ int run_p2p_rank(DevCtx &d, cudaStream_t st, const float *A, float *B, float *C,
   }
   // GEMMs over the K-chunks, every tile also stored into the peers' C_full (one multicast
   // store per piece when C_full is this rank's team buffer, else one store per peer)
-  float *const mc = rank_mc_address(C, M, N);
-  if (rank_mc_buffer(C) && !mc)
-    return fail(GIGA_ERR_INVALID_ARG, "p2p transport: M x N exceeds the multicast C_full");
   float *peer[kMaxCDst];
   int np = 0;
   if (!mc)
