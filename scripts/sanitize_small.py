@@ -81,6 +81,28 @@ giga.matmul_sharded(shards, Bs, Cs, M, N, K)
 ref = torch.from_numpy(A.astype(np.float64) @ B.astype(np.float64)).float()
 for C in Cs:
     assert torch.equal(C.cpu(), ref)
+# the same with the epilogue's 16-byte store mode ($GIGA_P2P_STORE=vec, the multicast
+# gather's code path with one store per peer)
+os.environ["GIGA_P2P_STORE"] = "vec"
+Cs = [torch.full((M, N), float("nan"), device="cuda") for _ in range(3)]
+giga.matmul_sharded(shards, Bs, Cs, M, N, K)
+for C in Cs:
+    assert torch.equal(C.cpu(), ref)
+del os.environ["GIGA_P2P_STORE"]
 giga.finalize()
 del os.environ["GIGA_TRANSPORT"]
+# the fused-gather epilogue's store modes on one device (TMA / st.global / multimem.st given
+# an ordinary address), 3xFP16 with exceptions (the fixes write every destination)
+dAe, dBe = torch.from_numpy(Ae).cuda(), torch.from_numpy(Be).cuda()
+Me_, Ne_ = Ae.shape[0], Be.shape[1]
+outs = []
+for mode, npeer in ((0, 2), (1, 2), (2, 0)):
+    Cm = torch.full((Me_, Ne_), float("nan"), device="cuda")
+    peers = [torch.full((Me_, Ne_), float("nan"), device="cuda") for _ in range(npeer)]
+    giga.gemm_gather_ex(dAe, dBe, Cm, peers, Me_, Ne_, Ae.shape[1], terms=4, store_mode=mode)
+    torch.cuda.synchronize()
+    for q in peers:
+        assert torch.equal(q, Cm), mode
+    outs.append(Cm)
+assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
 print("sanitize script ok")
