@@ -373,12 +373,12 @@ int giga_gemm_schedule(int64_t M, int64_t N, int64_t K, int num_sms, int64_t *ou
 /* The fp32-accurate scheme the product path uses for one M x N x K GEMM launch (host-only,
  * DESIGN.md 6.7, 6.8): *terms = 4 (3xFP16, see giga_gemm_3xtf32_ex: per-product split error
  * <= 2 * 2^-20 + 2^-22 |a||b|; 4 preparation kernels and 2 exception-fix kernels per launch)
- * when M >= 2048, M N K >= 2^37 and either K, N >= 2048 or K >= 1024 with N >= 8192; else 2
- * (TF32 + BF16: a_hi*b_hi
- * as one kind::tf32 MMA plus a_lo*b + a_hi*b_lo as one K=16 kind::f16 MMA, hi = RN tf32(x),
- * operands prepared once per launch; split error <= 3 * 2^-19 |a||b|) when M >= 4096,
- * N >= 8192, K >= 512 and M N K >= 2^38; else 3 (3xTF32: three kind::tf32 MMAs per k8
- * step, no preparation). The thresholds are measured crossovers (preparation included);
+ * when M >= 2048, N >= 1024, K >= 512 and M N K >= 2^35; else 3 (3xTF32: three kind::tf32
+ * MMAs per k8 step, no preparation). 2 (TF32 + BF16: a_hi*b_hi as one kind::tf32 MMA plus
+ * a_lo*b + a_hi*b_lo as one K=16 kind::f16 MMA, hi = RN tf32(x), operands prepared once per
+ * launch; split error <= 3 * 2^-19 |a||b|) is no longer chosen by shape (3xFP16 wins its old
+ * range since the round-2 epilogue fix). The thresholds are measured crossovers (preparation
+ * included, profiles/r02_scheme_crossover_e.jsonl);
  * $GIGA_SCHEME = 3xtf32 | tf32bf16 | 3xfp16 forces one. Errors: INVALID_ARG. */
 int giga_product_scheme(int64_t M, int64_t N, int64_t K, int *terms);
 
