@@ -160,14 +160,17 @@ def _rank_worker(rank, world, port, M, N, K, q, transport="p2p", own_device=Fals
         q.put((rank, False, False, False, repr(e)))
 
 
-@pytest.mark.parametrize("world,M,N,K,scheme", [(2, 1000, 520, 1040, None),
-                                                (3, 517, 256, 2064, None),
-                                                (2, 1000, 520, 2064, "3xfp16"),
-                                                (3, 517, 256, 2064, "3xfp16")])
-def test_rank_p2p_across_processes(torch_cuda, world, M, N, K, scheme):
+@pytest.mark.parametrize("world,M,N,K,scheme,store", [(2, 1000, 520, 1040, None, None),
+                                                      (3, 517, 256, 2064, None, None),
+                                                      (2, 1000, 520, 2064, "3xfp16", None),
+                                                      (3, 517, 256, 2064, "3xfp16", None),
+                                                      (3, 517, 256, 2064, None, "vec"),
+                                                      (2, 1000, 520, 2064, "3xfp16", "vec")])
+def test_rank_p2p_across_processes(torch_cuda, world, M, N, K, scheme, store):
     """Processes sharing cuda:0 through the rank API, p2p transport; with $GIGA_SCHEME=3xfp16
     the load-C epilogue, the operand scales and the A-side fix's mirror writes go into the
-    peers' C_full through CUDA IPC."""
+    peers' C_full through CUDA IPC; with $GIGA_P2P_STORE=vec the epilogue writes them with
+    16-byte stores (the multicast gather's code path, one store per peer)."""
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as so:
@@ -175,7 +178,11 @@ def test_rank_p2p_across_processes(torch_cuda, world, M, N, K, scheme):
         port = so.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    env = {"GIGA_SCHEME": scheme} if scheme else None
+    env = {}
+    if scheme:
+        env["GIGA_SCHEME"] = scheme
+    if store:
+        env["GIGA_P2P_STORE"] = store
     procs = [ctx.Process(target=_rank_worker,
                          args=(r, world, port, M, N, K, q, "p2p", False, env))
              for r in range(world)]
