@@ -94,6 +94,8 @@ enum giga_status {
   GIGA_ERR_COMM = -7,                /* NCCL / peer-transport failure */
   GIGA_ERR_UNSUPPORTED = -8          /* valid request this build cannot serve */
 };
+/* SURVEY.md 8(b)'s name for the communication failure (it also covers the p2p transport). */
+#define GIGA_ERR_NCCL GIGA_ERR_COMM
 
 /* ------------------------------------------------------------------------------------ */
 /* Single-process API: one process drives g GPUs (the paper's GigaGPU object). */
