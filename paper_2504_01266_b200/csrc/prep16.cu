@@ -212,7 +212,8 @@ __global__ void prep16_bexp_kernel(const unsigned *__restrict__ bmax, int n_pad,
 
 // B pass 3: B_hi / B_lo (fp16, K x N row-major, row stride ldh) and B's exceptions. A block
 // covers 1024 columns (256 threads x 4: every row it touches is one 4 KiB stretch in, two 2 KiB
-// stretches out) and `rows` rows, 8 rows' loads in flight per thread (the pass-1 layout).
+// stretches out) and `rows` rows, RIF rows' loads in flight per thread (the pass-1 layout),
+// MINB blocks per SM.
 __device__ __forceinline__ void prep16_b_put(const float4 v, int k, int n, int K, int4 e,
                                              uint16_t *__restrict__ Bh,
                                              uint16_t *__restrict__ Bl, int64_t ldh,
@@ -240,7 +241,8 @@ __device__ __forceinline__ void prep16_b_put(const float4 v, int k, int n, int K
          make_uint2(l[0] | uint32_t(l[1]) << 16, l[2] | uint32_t(l[3]) << 16));
 }
 
-__global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__ B, int64_t ldb,
+template <int RIF, int MINB>
+__global__ void __launch_bounds__(256, MINB) prep16_b_kernel(const float *__restrict__ B, int64_t ldb,
                                                        int K, int N, int rows,
                                                        const int *__restrict__ eb,
                                                        uint16_t *__restrict__ Bh,
@@ -255,13 +257,13 @@ __global__ void __launch_bounds__(256) prep16_b_kernel(const float *__restrict__
   const int4 e = *reinterpret_cast<const int4 *>(eb + n);  // eb is padded to 256 columns
   if (n + 3 < N) {
     int r = r0;
-    for (; r + 8 <= r1; r += 8) {
-      float4 v[8];
+    for (; r + RIF <= r1; r += RIF) {
+      float4 v[RIF];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < RIF; ++u)
         v[u] = __ldcs(reinterpret_cast<const float4 *>(B + int64_t(r + u) * ldb + n));
 #pragma unroll
-      for (int u = 0; u < 8; ++u) prep16_b_put(v[u], r + u, n, K, e, Bh, Bl, ldh, bits, summ, w2, flag);
+      for (int u = 0; u < RIF; ++u) prep16_b_put(v[u], r + u, n, K, e, Bh, Bl, ldh, bits, summ, w2, flag);
     }
     for (; r < r1; ++r)
       prep16_b_put(__ldcs(reinterpret_cast<const float4 *>(B + int64_t(r) * ldb + n)), r, n, K,
@@ -455,7 +457,10 @@ cudaError_t prep16_b_kernels(const float *B, int64_t ldb, int64_t N, int64_t K,
   prep16_bexp_kernel<<<unsigned((n_pad + 255) / 256), 256, 0, st>>>(
       tp->bmax, int(n_pad), const_cast<int *>(tp->eb));
   // the same grid as pass 1 (1024-column blocks x row ranges, ~8 blocks per SM)
-  prep16_b_kernel<<<g1, 256, 0, st>>>(B, ldb, int(K), int(N), int(rows), tp->eb,
+  // 4 rows in flight per thread at 4 blocks per SM (64 registers): ~15% faster than 8 rows at
+  // 2 blocks per SM (latency-bound at 25% occupancy, 4.7 TB/s; ncu A/B at 16384 x 32768)
+  auto kern = prep16_b_kernel<4, 4>;
+  kern<<<g1, 256, 0, st>>>(B, ldb, int(K), int(N), int(rows), tp->eb,
                                      const_cast<uint16_t *>(tp->Bh), const_cast<uint16_t *>(tp->Bl),
                                      tp->ldbh, tp->xb, tp->sb2, tp->w2b, tp->fb);
   compact16_b_kernel<<<unsigned((tp->wb + 7) / 8), 256, 0, st>>>(
