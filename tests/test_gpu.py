@@ -469,7 +469,9 @@ def test_oom_leaves_no_leak(giga, torch_cuda):
     assert e.value.status == "GIGA_ERR_OOM", str(e.value)
     torch.cuda.synchronize()
     free1, _ = torch.cuda.mem_get_info()
-    assert free1 == free0
+    # nothing allocated stays behind (usage never grows); it may shrink: run after other
+    # modules, one 2 MiB granule released by the driver during the call was seen once
+    assert free1 >= free0, (free0, free1)
     g = load("spec_2x2.txt")
     assert np.array_equal(run_host(giga, g["A"], g["B"]), g["C"])
 
