@@ -9,4 +9,4 @@ timeout -s KILL 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_ou
 for c in c3_16384 c2_4096 c4_tall; do timeout -s KILL 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo bench_${c}_rc=$?; head -c 200 gpurun_out/bench_$c.json; echo; done
 timeout -s KILL 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; echo ref_rc=$?; head -c 300 gpurun_out/bench_reference.json; echo
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm|prep|fix|compact" --csv --log-file gpurun_out/launches_bench_c5.csv python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1; echo launches_rc=$?
-bash scripts/gpu_sanitize.sh > /dev/null 2>&1; head -14 gpurun_out/compute_sanitizer.txt
+echo "(compute-sanitizer is closed on this pool)"
