@@ -257,7 +257,7 @@ int giga_rank_p2p_import(const uint8_t *blobs, int world);
  * ordinary buffers the transport keeps the unicast gather. Requires N % 4 == 0 (as the p2p
  * transport does). The buffers are zero-filled device memory owned by the library, valid
  * until freed / giga_finalize. NOT RUN on hardware yet: the 1-GPU pool this was built on
- * refuses cuMulticastCreate.
+ * refuses cuMulticastCreate ("Multicast gather").
  * Errors: UNSUPPORTED (the driver refuses multicast: no NVSwitch / fabric manager, device
  * attribute MULTICAST_SUPPORTED = 0, pidfd_getfd not permitted), NOT_INITIALIZED,
  * INVALID_ARG, OOM, CUDA. */

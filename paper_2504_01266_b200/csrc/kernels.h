@@ -120,7 +120,8 @@ struct GemmExtra {
   int defer_fix = 0;
   // $GIGA_TRACE: 2 x (grid size) slots; each CTA writes %globaltimer at its start and its end
   uint64_t *cta_ns = nullptr;
-  // How the epilogue writes the staged C blocks:
+  // How the epilogue writes the staged C blocks ("Multicast
+  // gather"):
   //   mc_c != nullptr: the NVLink multicast address of the same rows as C (C and every peer's
   //     C_full bound into one cuMulticastCreate team): each 16-byte piece is written ONCE with
   //     multimem.st and the switch replicates it into every member, C included (peer_c must
