@@ -296,9 +296,9 @@ __device__ __forceinline__ void fix_b_block(const GemmParams &p, float *stg, int
 // the TMA unit (kStoreVec: to C and every peer; kStoreMulticast: once, to the team address,
 // which the NVSwitch replicates into every GPU's C_full -- DESIGN.md 7, "Multicast gather").
 // Each 8-lane group writes one 128-byte row segment per instruction (4 rows per warp store,
-// coalesced), reading
-// the staging tile's swizzled chunks (chunk j of row r at j ^ (r & 7): conflict-free). Rows
-// >= M and columns >= N are clipped here (N % 4 == 0: a chunk is all in or all out).
+// coalesced), reading the staging tile's swizzled chunks (chunk j of row r at j ^ (r & 7):
+// conflict-free). Rows >= M and columns >= N are clipped here (N % 4 == 0: a chunk is all in
+// or all out).
 __device__ __forceinline__ void vec_store_block(const GemmParams &p, uint32_t stg, int row0,
                                                 int col0, int lane) {
   const int col = col0 + 4 * (lane & 7);
