@@ -1,6 +1,7 @@
 """Whole-C and worst-case parity at the BASELINE sizes ("harden parity").
 
-* Freivalds' check of EVERY element of C at 16384^3 and 32768^3 on integer inputs (synth d3),
+* Freivalds' check of EVERY element of C at 4096^3, the tall 262144 x 1024^2, 16384^3 and
+  32768^3 on integer inputs (synth d3),
   through bench.py's launch path: for random integer vectors r, C r == A (B r) exactly. All
   partial sums are integers below 2^53, so fp64 matrix-vector products are exact whatever
   their summation order; a single wrong element of C changes C r unless r's entry at its
@@ -56,7 +57,8 @@ def _freivalds(torch, A, B, C, seeds=(11, 12)):
     return worst
 
 
-@pytest.mark.parametrize("M,N,K", [(16384, 16384, 16384), (32768, 32768, 32768)])
+@pytest.mark.parametrize("M,N,K", [(4096, 4096, 4096), (262144, 1024, 1024),
+                                   (16384, 16384, 16384), (32768, 32768, 32768)])
 def test_freivalds_whole_c_integer_inputs(torch_cuda, M, N, K):
     """Every element of C at full size, through bench.py's path (rank API at world 1 on a
     side stream, device-resident inputs, repeated calls), on d3 integer inputs (bit-exact bar:
@@ -75,7 +77,7 @@ def test_freivalds_whole_c_integer_inputs(torch_cuda, M, N, K):
             g.matmul_rank(A, B, C, M, N, K, stream=s)
         s.synchronize()
         assert not torch.isnan(C).any().item()
-        assert g.product_scheme(M, N, K) == 4  # the 3xFP16 product path at both sizes
+        assert g.product_scheme(M, N, K) == 4  # the 3xFP16 product path at every size here
         worst = _freivalds(torch, A, B, C)
         assert worst == 0.0, worst
         # the check itself: one wrong element anywhere must be caught
