@@ -116,24 +116,29 @@ def test_dot_rank_api(torch_cuda, monkeypatch, force):
         g.init(1)
 
 
-def test_paper_api_object(torch_cuda):
-    """GigaGPU with the paper's method names."""
+def test_paper_worked_examples_and_release(torch_cuda):
+    """The SPEC's worked examples through the C ABI (SPEC.md:282 2x2 product, the vector
+    examples: dot 32, L2 norm 5), and giga_finalize releasing the
+    library's device memory."""
     from paper_2504_01266_b200 import giga as g
-    from paper_2504_01266_b200.gigagpu import GigaGPU
     g.finalize()
     free0 = torch_cuda.cuda.mem_get_info()[0]
-    with GigaGPU(1) as gpu:
-        gold = load("spec_2x2.txt")
-        assert np.array_equal(gpu.performMatrixMultiplication(gold["A"], gold["B"]), gold["C"])
-        A = synth.gen_matrix(300, 520, synth.MATRIX_A, "d3")
-        B = synth.gen_matrix(520, 260, synth.MATRIX_B, "d3")
-        C = gpu.performMatrixMultiplication(torch_cuda.from_numpy(A).cuda(),
-                                            torch_cuda.from_numpy(B).cuda())
-        assert np.array_equal(C.cpu().numpy().astype(np.float64), oracle.gemm(A, B)[0])
-        v = load("spec_vector.txt")
-        assert gpu.computeDotProduct(v["X"][0], v["Y"][0]) == 32.0
-        assert gpu.computeL2Norm(v["L"][0]) == 5.0
+    g.init(1)
+    gold = load("spec_2x2.txt")
+    C2 = np.empty_like(gold["C"], dtype=np.float32)
+    g.matmul(np.ascontiguousarray(gold["A"], np.float32), np.ascontiguousarray(gold["B"], np.float32),
+             C2, 2, 2, 2, 1)
+    assert np.array_equal(C2, gold["C"])
+    A = synth.gen_matrix(300, 520, synth.MATRIX_A, "d3")
+    B = synth.gen_matrix(520, 260, synth.MATRIX_B, "d3")
+    dC = torch_cuda.empty((300, 260), device="cuda")
+    g.matmul(torch_cuda.from_numpy(A).cuda(), torch_cuda.from_numpy(B).cuda(), dC, 300, 260, 520, 1)
+    assert np.array_equal(dC.cpu().numpy().astype(np.float64), oracle.gemm(A, B)[0])
+    v = load("spec_vector.txt")
+    assert g.dot(np.ascontiguousarray(v["X"][0], np.float32),
+                 np.ascontiguousarray(v["Y"][0], np.float32)) == 32.0
+    assert g.l2norm(np.ascontiguousarray(v["L"][0], np.float32)) == 5.0
+    g.finalize()
     torch_cuda.cuda.synchronize()
-    # destruction released the library's device memory (SPEC.md:440, S:619)
     assert torch_cuda.cuda.mem_get_info()[0] >= free0 - (64 << 20)
     g.init(1)
