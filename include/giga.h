@@ -350,6 +350,8 @@ int giga_gemm_gather_ex(const float *A, const float *B, float *C, float *const *
  * giga_matmul_sharded over NCCL -- the K-chunks of giga_pipeline_plan accumulating into the
  * rank's rows of C_full, the last K-chunk in its row chunks, on all SMs but $GIGA_COMM_SMS --
  * with no communication: B is read as if it had arrived. world = 1 is the single-GPU GEMM.
+ * With $GIGA_TRANSPORT=p2p: that transport's GEMMs instead -- all SMs, one launch per K-chunk
+ * of its plan, the last one load-C (run_p2p_rank's launches without the peer stores).
  * Timing it bounds the per-GPU compute time of the N-GPU step from below
  * (scripts/project_scaling.py). A_shard: the rank's giga_partition rows x K; B: K x N; C_full: M x N (the
  * rank's rows are written). K % 4 == N % 4 == 0, 16-byte aligned pointers. Does not need

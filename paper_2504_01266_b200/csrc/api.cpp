@@ -771,11 +771,31 @@ int giga_rank_compute_only(const float *A_shard, const float *B, float *C_full, 
   ex.ldb = N;
   ex.max_ctas = world > 1 ? pipeline_max_ctas(dev) : 0;
   auto none = [](int) { return int(GIGA_OK); };
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (world == 1)  // the single-GPU path: one whole GEMM on all SMs
-    return run_gemm(A_shard, nullptr, B, nullptr, C_full, M, N, K, N, GemmExtra(),
-                    static_cast<cudaStream_t>(stream));
-  return rank_gemms(plan, ex, M, N, K, world, rank, A_shard, nullptr, B, nullptr, C_full,
-                    static_cast<cudaStream_t>(stream), none, none);
+    return run_gemm(A_shard, nullptr, B, nullptr, C_full, M, N, K, N, GemmExtra(), st);
+  if (transport_p2p()) {
+    // the p2p transport's GEMMs (run_p2p_rank): all SMs (copy engines move B), one launch per
+    // K-chunk accumulating into the rank's rows, the last one reading the partial back
+    // (load-C; its stores into the peers' C_full are left out like every transfer here)
+    int64_t r0, rows;
+    partition_rows(M, world, rank, &r0, &rows);
+    if (rows == 0) return GIGA_OK;
+    ex.max_ctas = 0;
+    for (int c = 0; c < plan.pb; ++c) {
+      GemmExtra e = ex;
+      const bool last = c == plan.pb - 1;
+      e.accumulate = (c > 0 && !last) ? 1 : 0;
+      e.load_c = (c > 0 && last) ? 1 : 0;
+      e.rows_hint = rows;
+      const int64_t Kc = plan.kb[c + 1] - plan.kb[c];
+      TRY(gemm_chunk(A_shard + plan.kb[c], nullptr, B + plan.kb[c] * N, nullptr, C_full + r0 * N,
+                     rows, N, Kc, e, st));
+    }
+    return GIGA_OK;
+  }
+  return rank_gemms(plan, ex, M, N, K, world, rank, A_shard, nullptr, B, nullptr, C_full, st,
+                    none, none);
 }
 
 int giga_product_scheme(int64_t M, int64_t N, int64_t K, int *terms) {

@@ -18,7 +18,8 @@ NV_GBS = 770.0  # per-direction NVLink rate the north_star roofline uses (bench.
 names = sys.argv[1:] or ["c2_4096", "c3_16384", "c4_tall", "c5_32768"]
 for name in names:
     M, N, K = CONFIGS[name]
-    out = {"config": name, "M": M, "N": N, "K": K}
+    out = {"config": name, "M": M, "N": N, "K": K,
+           "transport": os.environ.get("GIGA_TRANSPORT", "nccl")}
     B = synth.gen_rows_torch(0, K, N, 2, "d2", device="cuda")
     for world in (1, 2, 4, 8):
         rows = [giga.partition(M, world, r)[1] for r in range(world)]
